@@ -1,0 +1,266 @@
+/*
+ * sddg.h -- C-ABI of the B200-native stochastic domain decomposition (SDD)
+ * mesh generator (arXiv 1310.3435), the drop-in boundary for the reference
+ * sddmesh hot path.
+ *
+ * The reference (/root/reference/proj, C++20) has no FFI; its seams are C++
+ * functions.  Each entry point below names the reference function it
+ * replaces.  Plain pointers and sizes only; no torch or C++ types; never
+ * throws.  Every call returns an sddg_status mirroring the reference's
+ * exception classes (proj/include/sdd/errors.hpp:8-32); the message of the
+ * last failure on a context is sddg_last_error().
+ *
+ * Library: paper_1310_3435_b200/_lib/libsddg.so (sm_100a only).  There is no
+ * CPU fallback: without a usable B200 every compute entry point fails with
+ * SDDG_ERR_CUDA.
+ */
+#ifndef SDDG_H
+#define SDDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDDG_ABI_VERSION 1
+
+typedef enum {
+    SDDG_OK = 0,
+    SDDG_ERR_VALIDATION = 1,    /* sdd::ValidationError  */
+    SDDG_ERR_OUT_OF_DOMAIN = 2, /* sdd::OutOfDomainError */
+    SDDG_ERR_EVALUATION = 3,    /* sdd::EvaluationError  */
+    SDDG_ERR_NUMERICAL = 4,     /* sdd::NumericalError   */
+    SDDG_ERR_LAYOUT = 5,        /* sdd::LayoutError      */
+    SDDG_ERR_CUDA = 6,          /* no B200 / CUDA failure (no fallback) */
+    SDDG_ERR_INTERNAL = 7
+} sddg_status;
+
+/* Density descriptor.  A GPU cannot call the reference's std::function
+ * density (proj/include/sdd/monitor.hpp:68), so densities are data.
+ * Kinds 0-4 are the reference builtins given as rho
+ * (proj/include/sdd/monitor.hpp:11-18, formulas proj/src/monitor.cpp:121-223).
+ * Kinds 16-18 are the BASELINE.json densities given as the diffusion weight
+ * w, which the reference receives as MonitorFunction::user_supplied(rho=1/w)
+ * (proj/src/monitor.cpp:73-80). */
+typedef enum {
+    SDDG_DENS_CONSTANT = 0,
+    SDDG_DENS_RUNNING = 1,
+    SDDG_DENS_HUANG_SLOAN = 2,
+    SDDG_DENS_MACKENZIE = 3,
+    SDDG_DENS_FIVE_RING = 4,
+    SDDG_DENS_RING_W = 16,   /* w = 1+10 exp(-200 ((x-.5)^2+(y-.5)^2-1/16)^2)     */
+    SDDG_DENS_SHOCK_W = 17,  /* w = 1+20 sech^2(50 (y-.5-.15 sin 2 pi x))         */
+    SDDG_DENS_TWOBUMP_W = 18 /* w = 1+15 e^{-100|x-(.3,.3)|^2}+15 e^{-100|x-(.7,.6)|^2} */
+} sddg_density_kind;
+
+typedef enum {
+    /* What the reference computes: the builtin analytic gradient for kinds
+     * 0-4, the user_supplied central difference of rho = 1/w with step fd_h
+     * for kinds 16-18 (proj/src/monitor.cpp:206-219). */
+    SDDG_GRAD_REFERENCE = 0,
+    /* Analytic drift grad(w)/w for kinds 16-18 (BASELINE.json configs). */
+    SDDG_GRAD_ANALYTIC = 1
+} sddg_grad_mode;
+
+typedef struct {
+    int32_t kind;      /* sddg_density_kind */
+    int32_t grad_mode; /* sddg_grad_mode */
+    double R, alpha;   /* builtin parameters (monitor.hpp:26-38) */
+    double fd_h;       /* user_supplied FD step, reference default 1e-6 */
+} sddg_density;
+
+typedef struct {
+    double xmin, xmax, ymin, ymax; /* sdd::RectDomain (geometry.hpp:27-46) */
+} sddg_domain;
+
+/* sdd::BoundaryData (proj/include/sdd/boundary.hpp:12-18): Dirichlet tables
+ * tabulated at the nodes of an nx x ny grid over dom; index 0..3 = bottom,
+ * top, left, right (sdd::Edge, geometry.hpp:19); bottom/top have nx entries,
+ * left/right ny.  f carries xi, g eta. */
+typedef struct {
+    sddg_domain dom;
+    int32_t nx, ny;
+    const double* f[4];
+    const double* g[4];
+} sddg_boundary;
+
+typedef enum { SDDG_SCHEME_LINEAR = 0, SDDG_SCHEME_EXPONENTIAL = 1 } sddg_scheme;
+typedef enum { SDDG_FP64 = 0, SDDG_FP32 = 1 } sddg_precision;
+
+/* sdd::WalkConfig (proj/include/sdd/sde.hpp:16-26) + precision. */
+typedef struct {
+    int32_t scheme;    /* sddg_scheme */
+    int32_t precision; /* sddg_precision: FP32 walks keep fp64 sums (config 3) */
+    double dt;         /* linear step */
+    double lambda;     /* exponential rate */
+    int64_t walks;     /* paths per node */
+    uint64_t seed;
+    int64_t max_steps; /* steps per epoch before a restart */
+    int32_t bridge_test;
+    int32_t reserved;
+} sddg_walk_config;
+
+/* sdd::McEstimate (proj/include/sdd/sde.hpp:61-68) + the raw fixed-order
+ * sums and the executed path-steps (all epochs). */
+typedef struct {
+    double xi, eta, se_xi, se_eta;
+    int64_t walks, restarts;
+    int32_t warn; /* reliability_warning: restarts > walks/100 */
+    int32_t reserved;
+    int64_t edge_hits[4];
+    double sum_f, sum_g, sum_ff, sum_gg;
+    int64_t path_steps;
+} sddg_estimate;
+
+/* One walk's result (the anonymous WalkResult, proj/src/sde.cpp:144-149,
+ * plus the exit point). */
+typedef struct {
+    double f, g, ex, ey;
+    int64_t steps;
+    int32_t epoch, edge;
+} sddg_path;
+
+typedef struct sddg_ctx sddg_ctx;
+
+/* ---------------------------------------------------------------- context */
+const char* sddg_version(void);
+int sddg_abi_version(void);
+sddg_status sddg_device_count(int32_t* n);
+/* Owns one device, its stream, device buffers and scratch; calls on one ctx
+ * are serialised. */
+sddg_status sddg_create(int32_t device, sddg_ctx** out);
+void sddg_destroy(sddg_ctx* ctx);
+const char* sddg_last_error(const sddg_ctx* ctx);
+/* Path-steps executed and kernels launched by the last compute call. */
+sddg_status sddg_last_stats(const sddg_ctx* ctx, int64_t* path_steps, int64_t* launches,
+                            double* kernel_ms);
+
+/* ------------------------------------------------------------- walk seams */
+
+/* Replaces the per-node loop of sdd::mc_estimate calls
+ * (proj/include/sdd/sde.hpp:75-77, called at proj/src/decomposition.cpp:173
+ * and proj/src/cli.cpp:261): one Feynman-Kac estimate per start point, walk w
+ * of point k on the stream (seed, point_id[k], w) with the reference's 256-walk
+ * chunk-order reduction.  Host buffers. */
+sddg_status sddg_mc_estimate_batch(sddg_ctx* ctx, const sddg_density* dens,
+                                   const sddg_domain* dom, const sddg_boundary* bd,
+                                   const sddg_walk_config* cfg, const double* px,
+                                   const double* py, const uint64_t* point_id, int64_t n,
+                                   sddg_estimate* out);
+
+/* Same with device-resident start points and output, enqueued on `stream`
+ * (a cudaStream_t, or NULL for the context stream); returns after the
+ * work completes. */
+sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* dens,
+                                          const sddg_domain* dom, const sddg_boundary* bd,
+                                          const sddg_walk_config* cfg, const double* d_px,
+                                          const double* d_py, const uint64_t* d_point_id,
+                                          int64_t n, sddg_estimate* d_out, void* stream);
+
+/* Per-path results of walks [walk_lo, walk_lo+n) at one start point: the
+ * parity view of run_walk (proj/src/sde.cpp:151-183). */
+sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                           const sddg_boundary* bd, const sddg_walk_config* cfg, double px,
+                           double py, uint64_t point_id, int64_t walk_lo, int64_t n,
+                           sddg_path* out);
+
+/* ----------------------------------------------------------- solver seams */
+
+typedef struct {
+    int32_t i0, j0, nx, ny; /* sdd::Subdomain (decomposition.hpp:21-24) */
+} sddg_subdomain;
+
+typedef enum {
+    SDDG_SOLVER_JACOBI = 0, /* the reference iteration (detsolver.cpp:150-189) */
+    SDDG_SOLVER_RBSOR = 1   /* red-black SOR, same fixed point */
+} sddg_solver_method;
+
+/* sdd::SolverConfig (proj/include/sdd/detsolver.hpp:11-18) + method. */
+typedef struct {
+    double tol;
+    int64_t max_iters; /* 0: 200 max(nx,ny)^2 */
+    int32_t init_blend;
+    int32_t method; /* sddg_solver_method */
+    double omega;   /* SOR factor; <= 0 picks the optimal one for the grid */
+} sddg_solver_config;
+
+typedef struct {
+    int64_t iterations;
+    double final_update;
+    int32_t converged;
+    int32_t reserved;
+} sddg_solve_info;
+
+/* Replaces the per-subdomain sdd::solve_dirichlet calls
+ * (proj/include/sdd/detsolver.hpp:44-45; proj/src/decomposition.cpp:349-350):
+ * n_solves independent Dirichlet problems on blocks of the global weight
+ * array w_global (gnx x gny, index j*gnx+i) with the global spacings hx, hy.
+ * bc_packed holds, per solve, bottom[nx] top[nx] left[ny] right[ny] back to
+ * back; u_packed receives each solution (nx*ny, index j*nx+i) back to back. */
+sddg_status sddg_solve_dirichlet_batch(sddg_ctx* ctx, const double* w_global, int32_t gnx,
+                                       int32_t gny, double hx, double hy, int64_t n_solves,
+                                       const sddg_subdomain* subs, const double* bc_packed,
+                                       const sddg_solver_config* scfg, double* u_packed,
+                                       sddg_solve_info* info);
+
+/* ---------------------------------------------------- decomposition seams */
+
+typedef enum {
+    SDDG_PLACE_ALL = 0,
+    SDDG_PLACE_EQUISPACED = 1,
+    SDDG_PLACE_OPTIMAL = 2
+} sddg_placement; /* sdd::PlacementStrategy (decomposition.hpp:40) */
+
+typedef enum {
+    SDDG_BC_REFERENCE = 0, /* make_boundary_data: 1D equidistribution (boundary.cpp:44-56) */
+    SDDG_BC_IDENTITY = 1   /* xi = x, eta = y (BASELINE.json) */
+} sddg_bc_mode;
+
+/* Host: sdd::make_boundary_data (proj/src/boundary.cpp:44-56) into 8
+ * caller arrays (f bottom,top,left,right; g bottom,top,left,right). */
+sddg_status sddg_make_boundary_data(const sddg_density* dens, const sddg_domain* dom,
+                                    int32_t nx, int32_t ny, int32_t bc_mode, double* tables8[8]);
+
+/* Host: build_layout + plan_interface_points
+ * (proj/src/decomposition.cpp:26-53,112-145).  Lines in layout order
+ * (vertical first); nodes of line l at out_nodes[sum counts[<l]].  Capacity:
+ * (sx-1)+(sy-1) lines, max(nx,ny) nodes each. */
+sddg_status sddg_plan_interface_points(const sddg_density* dens, const sddg_domain* dom,
+                                       int32_t nx, int32_t ny, int32_t sx, int32_t sy,
+                                       int32_t placement, int32_t k, int32_t* n_lines,
+                                       int32_t* out_vertical, int32_t* out_fixed,
+                                       int32_t* out_counts, int32_t* out_nodes);
+
+typedef struct {
+    double t_bd, t_stoc, t_sub, t_smooth; /* seconds, as SddResult (decomposition.hpp:79-86) */
+    int64_t mc_points, subdomain_solves, restarts, path_steps;
+    int32_t warnings;
+    int32_t reserved;
+} sddg_sdd_stats;
+
+/* Replaces sdd::solve_interfaces (proj/include/sdd/decomposition.hpp:70-72):
+ * line values (layout order, full node ranges back to back) of xi, eta and
+ * their stderrs. */
+sddg_status sddg_solve_interfaces(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                  int32_t nx, int32_t ny, int32_t sx, int32_t sy,
+                                  int32_t placement, int32_t k, const sddg_boundary* bd,
+                                  const sddg_walk_config* cfg, double* xi_lines,
+                                  double* eta_lines, double* se_xi_lines, double* se_eta_lines,
+                                  sddg_sdd_stats* stats);
+
+/* Replaces sdd::solve_sdd (proj/include/sdd/decomposition.hpp:91-94):
+ * boundary data, interface walks, subdomain solves, assembly into the global
+ * xi, eta (nx*ny, index j*nx+i). */
+sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                           int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t placement,
+                           int32_t k, int32_t bc_mode, const sddg_walk_config* cfg,
+                           const sddg_solver_config* scfg, double* xi, double* eta,
+                           sddg_sdd_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDDG_H */

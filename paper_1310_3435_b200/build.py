@@ -1,0 +1,74 @@
+"""Build the sm_100a shared library paper_1310_3435_b200/_lib/libsddg.so.
+
+Explicit nvcc, in-tree output (it travels to the GPU box with the repo
+snapshot).  Translation units that must reproduce the reference's rounding
+sequence (walk_ref.cu, solver.cu) are compiled with -fmad=false; the others
+may contract to FMA.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT_DIR = os.path.join(PKG, "_lib")
+OBJ_DIR = os.path.join(OUT_DIR, "obj")
+LIB = os.path.join(OUT_DIR, "libsddg.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          "-I" + os.path.join(ROOT, "include")]
+UNITS = {
+    "walk_ref.cu": ["-fmad=false"],
+    "walk_fast.cu": ["-fmad=true"],
+    "reduce.cu": ["-fmad=false"],
+    "solver.cu": ["-fmad=false"],
+    "runtime.cu": [],
+}
+HEADERS = ["density.cuh", "philox.cuh", "walk_kernel.cuh", "sddg_internal.h", "host_density.h"]
+
+
+def _mtime(p):
+    return os.path.getmtime(p) if os.path.exists(p) else -1.0
+
+
+def _compile(unit, flags, verbose):
+    src = os.path.join(CSRC, unit)
+    obj = os.path.join(OBJ_DIR, unit.replace(".cu", ".o"))
+    deps = [src] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "sddg.h")]
+    if _mtime(obj) >= max(_mtime(d) for d in deps):
+        return obj, False
+    cmd = [NVCC] + ARCH + COMMON + flags + ["-c", src, "-o", obj]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {unit}:\n{r.stderr}")
+    if verbose and r.stderr:
+        sys.stderr.write(r.stderr)
+    return obj, True
+
+
+def build(verbose=False, force=False):
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    if force:
+        for f in os.listdir(OBJ_DIR):
+            os.remove(os.path.join(OBJ_DIR, f))
+    with cf.ThreadPoolExecutor(max_workers=len(UNITS)) as ex:
+        results = list(ex.map(lambda kv: _compile(kv[0], kv[1], verbose), UNITS.items()))
+    objs = [o for o, _ in results]
+    if any(changed for _, changed in results) or _mtime(LIB) < max(_mtime(o) for o in objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -1,0 +1,107 @@
+// philox.cuh -- device Philox4x32-10 with the reference counter layout.
+//
+// Reference: Philox4x32::block and RandomStream (proj/include/sdd/rng.hpp:12-83).
+// Key (k0, k1) = (seed lo, seed hi); counter = {block, walk, point_id lo32,
+// (point_id >> 32 & 0xFFFF) | epoch << 16}.  u64 number n of a stream is
+// (hi << 32 | lo) with lo, hi = words 2(n&1), 2(n&1)+1 of block n >> 1: the
+// reference hands out 4-word blocks two words at a time (rng.hpp:41-55), so a
+// u64 never straddles two blocks.  A lane's stream state is therefore just the
+// u64 index n plus the upper half of the last block it generated.
+#pragma once
+#include <cstdint>
+
+namespace sddg {
+
+struct PhiloxWords {
+    uint32_t w0, w1, w2, w3;
+};
+
+__device__ __forceinline__ PhiloxWords philox4x32_10(uint32_t k0, uint32_t k1, uint32_t c0,
+                                                     uint32_t c1, uint32_t c2, uint32_t c3) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+        c0 = hi1 ^ c1 ^ k0;
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ k1;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return {c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ uint64_t join64(uint32_t lo, uint32_t hi) {
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+// Per-lane stream (one walk, one epoch).
+struct LaneStream {
+    uint32_t k0, k1;   // seed
+    uint32_t c1;       // walk
+    uint32_t c2, c3;   // point id lo, point id hi16 | epoch << 16
+    uint32_t n;        // u64s consumed this epoch
+    uint32_t cw2, cw3; // words 2,3 of the last generated block
+
+    __device__ __forceinline__ void init(uint64_t seed, uint64_t pid, uint32_t walk,
+                                         uint32_t epoch) {
+        k0 = static_cast<uint32_t>(seed);
+        k1 = static_cast<uint32_t>(seed >> 32);
+        c1 = walk;
+        c2 = static_cast<uint32_t>(pid);
+        c3 = static_cast<uint32_t>((pid >> 32) & 0xFFFFu) | (epoch << 16);
+        n = 0;
+        cw2 = cw3 = 0;
+    }
+
+    // Two consecutive u64s (n, n+1): exactly one new block, index (n+1)>>1,
+    // for either parity of n -- the per-step Philox call is warp-uniform.
+    __device__ __forceinline__ void next_pair(uint64_t& a, uint64_t& b) {
+        const PhiloxWords w = philox4x32_10(k0, k1, (n + 1) >> 1, c1, c2, c3);
+        if (n & 1u) {
+            a = join64(cw2, cw3);
+            b = join64(w.w0, w.w1);
+        } else {
+            a = join64(w.w0, w.w1);
+            b = join64(w.w2, w.w3);
+        }
+        cw2 = w.w2;
+        cw3 = w.w3;
+        n += 2;
+    }
+
+    // One u64 (bridge / exponential draws): a new block only when n is even.
+    __device__ __forceinline__ uint64_t next_one() {
+        uint64_t v;
+        if (n & 1u) {
+            v = join64(cw2, cw3);
+        } else {
+            const PhiloxWords w = philox4x32_10(k0, k1, n >> 1, c1, c2, c3);
+            v = join64(w.w0, w.w1);
+            cw2 = w.w2;
+            cw3 = w.w3;
+        }
+        n += 1;
+        return v;
+    }
+};
+
+// rng.hpp:58 u01 = (u >> 11) 2^-53 in [0,1); rng.hpp:61-63 u01_open.
+__device__ __forceinline__ double u01_d(uint64_t u) {
+    return __dmul_rn(static_cast<double>(u >> 11), 0x1.0p-53);
+}
+__device__ __forceinline__ double u01_open_d(uint64_t u) {
+    return __dmul_rn(__dadd_rn(static_cast<double>(u >> 12), 0.5), 0x1.0p-52);
+}
+// fp32 views of the same draws: the top 24 bits.
+__device__ __forceinline__ float u01_f(uint64_t u) {
+    return static_cast<float>(static_cast<uint32_t>(u >> 40)) * 0x1.0p-24f;
+}
+__device__ __forceinline__ float u01_open_f(uint64_t u) {
+    return __fmaf_rn(static_cast<float>(static_cast<uint32_t>(u >> 40)), 0x1.0p-24f, 0x1.0p-25f);
+}
+
+}  // namespace sddg

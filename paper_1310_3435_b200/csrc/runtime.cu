@@ -1,0 +1,1044 @@
+// runtime.cu -- host runtime behind include/sddg.h.
+//
+// Owns the device context (stream, grow-only device buffers, event timers)
+// and implements the reference's host-side orchestration around the two GPU
+// kernels: validation with the reference's error classes, node batching for
+// the walk kernel (K1) and its fixed-order finalize (K2), the subdomain solve
+// batch (K3), and the decomposition logic of proj/src/decomposition.cpp
+// (layout, placement, interface fill, assembly).  No compute path runs on the
+// CPU: every Monte Carlo walk and every subdomain iteration is a kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "host_density.h"
+#include "sddg_internal.h"
+
+using namespace sddg;
+
+namespace {
+
+struct Fail {
+    sddg_status st;
+    std::string msg;
+};
+
+[[noreturn]] void fail(sddg_status st, const std::string& m) { throw Fail{st, m}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SDDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* ensure(size_t bytes) {
+        if (bytes <= cap) return p;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = std::max<size_t>(bytes, 256);
+        ck(cudaMalloc(&p, want), "cudaMalloc");
+        cap = want;
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct Counters {
+    unsigned long long next, steps, err_info;
+    int err_flag;
+    int pad;
+};
+
+__global__ void set_next_kernel(Counters* c, unsigned long long v) { c->next = v; }
+
+thread_local std::string g_free_err;
+
+}  // namespace
+
+struct sddg_ctx {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+    std::mutex mu;
+    DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump;
+    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err;
+    int64_t last_steps = 0, last_launches = 0;
+    double last_ms = 0.0;
+    std::map<int, int> occ;  // (dv*2+prec) -> blocks per SM
+};
+
+namespace {
+
+// ------------------------------------------------------------ validation
+
+void validate_walk(const sddg_walk_config& c) {
+    // WalkConfig::validate (proj/src/sde.cpp:12-19)
+    if (c.scheme == SDDG_SCHEME_LINEAR && !(c.dt > 0.0))
+        fail(SDDG_ERR_VALIDATION, "WalkConfig: linear scheme needs dt > 0");
+    if (c.scheme == SDDG_SCHEME_EXPONENTIAL && !(c.lambda > 0.0))
+        fail(SDDG_ERR_VALIDATION, "WalkConfig: exponential scheme needs lambda > 0");
+    if (c.scheme != SDDG_SCHEME_LINEAR && c.scheme != SDDG_SCHEME_EXPONENTIAL)
+        fail(SDDG_ERR_VALIDATION, "WalkConfig: unknown scheme");
+    if (c.walks < 1) fail(SDDG_ERR_VALIDATION, "WalkConfig: walks must be >= 1");
+    if (c.walks > 0xFFFFFFFFLL)
+        fail(SDDG_ERR_VALIDATION, "WalkConfig: walks must fit the 32-bit stream walk id");
+    if (c.max_steps < 1) fail(SDDG_ERR_VALIDATION, "WalkConfig: max_steps must be >= 1");
+    if (c.precision != SDDG_FP64 && c.precision != SDDG_FP32)
+        fail(SDDG_ERR_VALIDATION, "WalkConfig: unknown precision");
+}
+
+int drift_variant(const sddg_density& d, int precision) {
+    const bool wkind = d.kind >= SDDG_DENS_RING_W && d.kind <= SDDG_DENS_TWOBUMP_W;
+    const bool builtin = d.kind >= SDDG_DENS_CONSTANT && d.kind <= SDDG_DENS_FIVE_RING;
+    if (!wkind && !builtin) fail(SDDG_ERR_VALIDATION, "unknown density kind");
+    if (d.grad_mode == SDDG_GRAD_ANALYTIC) {
+        if (!wkind)
+            fail(SDDG_ERR_VALIDATION,
+                 "analytic grad(w)/w drift exists for the BASELINE densities (kinds 16-18)");
+        return 32 + (d.kind - SDDG_DENS_RING_W);
+    }
+    if (d.grad_mode != SDDG_GRAD_REFERENCE) fail(SDDG_ERR_VALIDATION, "unknown grad_mode");
+    if (precision == SDDG_FP32)
+        fail(SDDG_ERR_VALIDATION,
+             "fp32 walks need the analytic drift (grad_mode SDDG_GRAD_ANALYTIC)");
+    if (wkind && !(d.fd_h > 0.0)) fail(SDDG_ERR_VALIDATION, "fd_h must be > 0");
+    return d.kind;
+}
+
+HostDensity host_density(const sddg_density& d) { return HostDensity{d.kind, d.R, d.alpha, d.fd_h}; }
+
+// MonitorFunction::check_positivity (proj/src/monitor.cpp:105-119) over the
+// density's domain: the builtins' own, the caller's for user_supplied kinds.
+void check_positivity(const sddg_density& d, const sddg_domain& dom) {
+    sddg_domain pd = dom;
+    if (d.kind <= SDDG_DENS_MACKENZIE) pd = {0, 1, 0, 1};
+    if (d.kind == SDDG_DENS_FIVE_RING) pd = {-1, 1, -1, 1};
+    const HostDensity h = host_density(d);
+    for (int j = 0; j < 33; ++j)
+        for (int i = 0; i < 33; ++i) {
+            const double x = pd.xmin + (pd.xmax - pd.xmin) * i / 32;
+            const double y = pd.ymin + (pd.ymax - pd.ymin) * j / 32;
+            double r;
+            try {
+                r = h.rho(x, y);
+            } catch (const std::exception&) {
+                r = NAN;
+            }
+            if (!std::isfinite(r) || r <= 0.0)
+                fail(SDDG_ERR_EVALUATION, "monitor density not finite/positive");
+        }
+}
+
+void check_domain(const sddg_domain& d) {
+    if (!(d.xmin < d.xmax) || !(d.ymin < d.ymax))
+        fail(SDDG_ERR_VALIDATION, "RectDomain: requires xmin < xmax and ymin < ymax");
+}
+
+void check_boundary(const sddg_boundary& b) {
+    check_domain(b.dom);
+    if (b.nx < 3 || b.ny < 3) fail(SDDG_ERR_VALIDATION, "GridSpec: needs nx >= 3 and ny >= 3");
+    for (int k = 0; k < 4; ++k)
+        if (!b.f[k] || !b.g[k]) fail(SDDG_ERR_VALIDATION, "boundary table pointer is NULL");
+}
+
+// ------------------------------------------------------------ K1 + K2
+
+int walk_grid(sddg_ctx* c, int dv, int prec, uint64_t total) {
+    const int key = dv * 2 + prec;
+    auto it = c->occ.find(key);
+    int bps;
+    if (it == c->occ.end()) {
+        ck(walk_occupancy(dv, prec, &bps), "occupancy");
+        c->occ[key] = bps;
+    } else {
+        bps = it->second;
+    }
+    const uint64_t full = static_cast<uint64_t>(std::max(1, bps)) * c->sms;
+    const uint64_t need = (total + kWalkBlock - 1) / kWalkBlock;
+    return static_cast<int>(std::max<uint64_t>(1, std::min(full, need)));
+}
+
+int64_t batch_budget_walks() {
+    const char* e = std::getenv("SDDG_MAX_BATCH_WALKS");
+    if (e) {
+        const long long v = std::atoll(e);
+        if (v > 0) return v;
+    }
+    return int64_t(1) << 27;  // 2.7 GB of walk records
+}
+
+void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
+               const sddg_boundary& bd, const sddg_walk_config& cfg, const double* dtab) {
+    std::memset(&a, 0, sizeof(a));
+    a.xmin = dom.xmin;
+    a.xmax = dom.xmax;
+    a.ymin = dom.ymin;
+    a.ymax = dom.ymax;
+    a.txmin = bd.dom.xmin;
+    a.tymin = bd.dom.ymin;
+    a.thx = (bd.dom.xmax - bd.dom.xmin) / (bd.nx - 1);  // GridSpec::hx (geometry.hpp:52)
+    a.thy = (bd.dom.ymax - bd.dom.ymin) / (bd.ny - 1);
+    a.tnx = bd.nx;
+    a.tny = bd.ny;
+    const int64_t nx = bd.nx, ny = bd.ny;
+    const int64_t offs[4] = {0, nx, 2 * nx, 2 * nx + ny};
+    for (int k = 0; k < 4; ++k) {
+        a.tf[k] = dtab + offs[k];
+        a.tg[k] = dtab + 2 * (nx + ny) + offs[k];
+    }
+    a.R = d.R;
+    a.alpha = d.alpha;
+    a.fd_h = d.fd_h;
+    a.scheme = cfg.scheme;
+    a.bridge = cfg.bridge_test ? 1 : 0;
+    a.dt = cfg.dt;
+    a.sqrt2dt = std::sqrt(2.0 * cfg.dt);  // step_linear (sde.cpp:27)
+    a.lambda = cfg.lambda;
+    a.nu2 = 2.0 * std::sqrt(cfg.lambda);  // step_exponential (sde.cpp:135)
+    a.bridge_thr = 40.0 * cfg.dt * (1.0 + (cfg.precision == SDDG_FP32 ? 1e-5 : 1e-12));
+    a.seed = cfg.seed;
+    a.max_steps = cfg.max_steps;
+}
+
+double* upload_tables(sddg_ctx* c, const sddg_boundary& bd) {
+    const size_t nx = bd.nx, ny = bd.ny;
+    std::vector<double> h(4 * (nx + ny));
+    const size_t lens[4] = {nx, nx, ny, ny};
+    size_t o = 0;
+    for (int fg = 0; fg < 2; ++fg)
+        for (int k = 0; k < 4; ++k) {
+            const double* src = fg == 0 ? bd.f[k] : bd.g[k];
+            std::memcpy(h.data() + o, src, sizeof(double) * lens[k]);
+            o += lens[k];
+        }
+    double* d = static_cast<double*>(c->tables.ensure(sizeof(double) * h.size()));
+    ck(cudaMemcpyAsync(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c->stream),
+       "upload tables");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    return d;
+}
+
+void raise_kernel_error(const Counters& hc) {
+    if (hc.err_flag == 3)
+        fail(SDDG_ERR_EVALUATION,
+             "drift not finite (point_id " + std::to_string(hc.err_info) + ")");
+    if (hc.err_flag == 4)
+        fail(SDDG_ERR_NUMERICAL, "mc_estimate: walk failed to exit after 1024 restarts (point_id " +
+                                     std::to_string(hc.err_info) + ")");
+}
+
+// Walks + finalize for n device-resident nodes; estimates to d_out.
+void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
+                   const sddg_boundary& bd, const sddg_walk_config& cfg, const double* d_px,
+                   const double* d_py, const uint64_t* d_pid, int64_t n, sddg_estimate* d_out,
+                   cudaStream_t st) {
+    const int dv = drift_variant(d, cfg.precision);
+    const double* dtab = upload_tables(c, bd);
+    Counters* cnt = static_cast<Counters*>(c->counters.ensure(sizeof(Counters)));
+    ck(cudaMemsetAsync(cnt, 0, sizeof(Counters), st), "memset counters");
+    const int64_t W = cfg.walks;
+    const int64_t npb = std::max<int64_t>(1, batch_budget_walks() / W);
+    const int64_t cap = std::min(npb, n) * W;
+    double* rf = static_cast<double*>(c->rec_f.ensure(sizeof(double) * cap));
+    double* rg = static_cast<double*>(c->rec_g.ensure(sizeof(double) * cap));
+    uint32_t* rm = static_cast<uint32_t*>(c->rec_meta.ensure(sizeof(uint32_t) * cap));
+    WalkArgs a;
+    fill_args(a, d, dom, bd, cfg, dtab);
+    a.walks = W;
+    a.walk_lo = 0;
+    a.next = &cnt->next;
+    a.steps = &cnt->steps;
+    a.err_flag = &cnt->err_flag;
+    a.err_info = &cnt->err_info;
+    a.rec_f = rf;
+    a.rec_g = rg;
+    a.rec_meta = rm;
+    int64_t launches = 0;
+    ck(cudaEventRecord(c->ev0, st), "event");
+    for (int64_t b = 0; b < n; b += npb) {
+        const int64_t nb = std::min(npb, n - b);
+        a.px = d_px + b;
+        a.py = d_py + b;
+        a.pid = d_pid + b;
+        a.total = static_cast<uint64_t>(nb) * W;
+        const int grid = walk_grid(c, dv, cfg.precision, a.total);
+        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * kWalkBlock);
+        ck(cudaGetLastError(), "set_next");
+        ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
+        ck(launch_reduce(rf, rg, rm, W, nb, d_out + b, st), "reduce launch");
+        launches += 3;
+    }
+    ck(cudaEventRecord(c->ev1, st), "event");
+    Counters hc;
+    ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "read counters");
+    ck(cudaStreamSynchronize(st), "walk kernels");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    c->last_ms = ms;
+    c->last_steps = static_cast<int64_t>(hc.steps);
+    c->last_launches = launches;
+    raise_kernel_error(hc);
+}
+
+void check_points(const sddg_domain& dom, const double* px, const double* py, int64_t n) {
+    for (int64_t k = 0; k < n; ++k)
+        if (!(px[k] > dom.xmin && px[k] < dom.xmax && py[k] > dom.ymin && py[k] < dom.ymax))
+            fail(SDDG_ERR_OUT_OF_DOMAIN, "mc_estimate: start point must be strictly inside");
+}
+
+void estimates_host(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
+                    const sddg_boundary& bd, const sddg_walk_config& cfg, const double* px,
+                    const double* py, const uint64_t* pid, int64_t n, sddg_estimate* out) {
+    validate_walk(cfg);
+    check_domain(dom);
+    check_boundary(bd);
+    drift_variant(d, cfg.precision);
+    check_positivity(d, dom);
+    check_points(dom, px, py, n);
+    if (n <= 0) return;
+    char* buf = static_cast<char*>(c->nodes.ensure(n * (2 * sizeof(double) + sizeof(uint64_t))));
+    double* dpx = reinterpret_cast<double*>(buf);
+    double* dpy = dpx + n;
+    uint64_t* dpid = reinterpret_cast<uint64_t*>(dpy + n);
+    ck(cudaMemcpyAsync(dpx, px, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaMemcpyAsync(dpy, py, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaMemcpyAsync(dpid, pid, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
+    sddg_estimate* dout = static_cast<sddg_estimate*>(c->est.ensure(sizeof(sddg_estimate) * n));
+    run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream);
+    ck(cudaMemcpyAsync(out, dout, sizeof(sddg_estimate) * n, cudaMemcpyDeviceToHost, c->stream),
+       "d2h");
+    ck(cudaStreamSynchronize(c->stream), "d2h sync");
+}
+
+// ------------------------------------------------------------ K3
+
+void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx, double hy,
+                      int64_t n, const sddg_subdomain* subs, const double* bc,
+                      const sddg_solver_config& sc, double* u, sddg_solve_info* info) {
+    if (!(sc.tol > 0.0)) fail(SDDG_ERR_VALIDATION, "SolverConfig: tol must be > 0");
+    if (sc.max_iters < 0) fail(SDDG_ERR_VALIDATION, "SolverConfig: max_iters must be >= 0");
+    if (sc.method != SDDG_SOLVER_JACOBI && sc.method != SDDG_SOLVER_RBSOR)
+        fail(SDDG_ERR_VALIDATION, "SolverConfig: unknown method");
+    if (n <= 0) return;
+    for (int64_t k = 0; k < static_cast<int64_t>(gnx) * gny; ++k)
+        if (!std::isfinite(w[k]) || w[k] <= 0.0)
+            fail(SDDG_ERR_EVALUATION, "solve_dirichlet: non-positive diffusion weight");
+    std::vector<SolveJob> jobs(n);
+    int64_t boff = 0, uoff = 0;
+    int max_n = 0, max_int = 0, max_dim = 0;
+    for (int64_t s = 0; s < n; ++s) {
+        const sddg_subdomain& q = subs[s];
+        if (q.nx < 3 || q.ny < 3) fail(SDDG_ERR_VALIDATION, "solve_dirichlet: grid too small");
+        if (q.i0 < 0 || q.j0 < 0 || q.i0 + q.nx > gnx || q.j0 + q.ny > gny)
+            fail(SDDG_ERR_VALIDATION, "solve_dirichlet: subdomain outside the weight grid");
+        const double* B = bc + boff;
+        const double* T = B + q.nx;
+        const double* L = T + q.nx;
+        const double* R = L + q.ny;
+        auto mismatch = [](double a, double b) {
+            return std::abs(a - b) > 1e-12 * (1.0 + std::abs(a) + std::abs(b));
+        };
+        if (mismatch(B[0], L[0]) || mismatch(B[q.nx - 1], R[0]) || mismatch(T[0], L[q.ny - 1]) ||
+            mismatch(T[q.nx - 1], R[q.ny - 1]))
+            fail(SDDG_ERR_VALIDATION, "solve_dirichlet: boundary data disagrees at a corner");
+        jobs[s] = SolveJob{q.i0, q.j0, q.nx, q.ny, boff, uoff};
+        boff += 2 * (q.nx + q.ny);
+        uoff += static_cast<int64_t>(q.nx) * q.ny;
+        max_n = std::max(max_n, q.nx * q.ny);
+        max_int = std::max(max_int, (q.nx - 2) * (q.ny - 2));
+        max_dim = std::max(max_dim, std::max(q.nx, q.ny));
+    }
+    const size_t smem_cap = 227 * 1024;
+    const bool coef_smem = sizeof(double) * 4 * static_cast<size_t>(max_n) <= smem_cap;
+    if (sizeof(double) * static_cast<size_t>(max_n) > smem_cap)
+        fail(SDDG_ERR_VALIDATION, "solve_dirichlet: subdomain exceeds the on-chip solver (" +
+                                      std::to_string(smem_cap / 8) + " nodes)");
+    if (sc.method == SDDG_SOLVER_JACOBI && max_int > solver_max_points())
+        fail(SDDG_ERR_VALIDATION, "solve_dirichlet: Jacobi batch limited to " +
+                                      std::to_string(solver_max_points()) +
+                                      " interior nodes per subdomain; use RBSOR");
+    double omega = sc.omega;
+    if (sc.method == SDDG_SOLVER_RBSOR && !(omega > 0.0)) {
+        const double kPi = 3.14159265358979323846;
+        omega = 2.0 / (1.0 + std::sin(kPi / (max_dim - 1)));
+    }
+    if (sc.method == SDDG_SOLVER_JACOBI) omega = 1.0;
+    const size_t wbytes = sizeof(double) * static_cast<size_t>(gnx) * gny;
+    double* dw = static_cast<double*>(c->s_w.ensure(wbytes));
+    SolveJob* dj = static_cast<SolveJob*>(c->s_jobs.ensure(sizeof(SolveJob) * n));
+    double* dbc = static_cast<double*>(c->s_bc.ensure(sizeof(double) * boff));
+    double* du = static_cast<double*>(c->s_u.ensure(sizeof(double) * uoff));
+    sddg_solve_info* dinfo = static_cast<sddg_solve_info*>(c->s_info.ensure(sizeof(sddg_solve_info) * n));
+    int* derr = static_cast<int*>(c->s_err.ensure(sizeof(int)));
+    double* dcoef = nullptr;
+    if (!coef_smem) dcoef = static_cast<double*>(c->s_coef.ensure(sizeof(double) * 3 * max_n * n));
+    cudaStream_t st = c->stream;
+    ck(cudaMemcpyAsync(dw, w, wbytes, cudaMemcpyHostToDevice, st), "h2d w");
+    ck(cudaMemcpyAsync(dj, jobs.data(), sizeof(SolveJob) * n, cudaMemcpyHostToDevice, st), "h2d jobs");
+    ck(cudaMemcpyAsync(dbc, bc, sizeof(double) * boff, cudaMemcpyHostToDevice, st), "h2d bc");
+    ck(cudaMemsetAsync(derr, 0, sizeof(int), st), "memset");
+    ck(cudaEventRecord(c->ev0, st), "event");
+    ck(launch_solve_batch(dw, gnx, hx, hy, n, dj, dbc, sc.tol, sc.max_iters, sc.init_blend,
+                          sc.method, omega, du, dinfo, derr, st, max_n, max_int, dcoef,
+                          coef_smem ? 1 : 0),
+       "solver launch");
+    ck(cudaEventRecord(c->ev1, st), "event");
+    int herr = 0;
+    ck(cudaMemcpyAsync(u, du, sizeof(double) * uoff, cudaMemcpyDeviceToHost, st), "d2h u");
+    ck(cudaMemcpyAsync(info, dinfo, sizeof(sddg_solve_info) * n, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h err");
+    ck(cudaStreamSynchronize(st), "solver");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    c->last_ms = ms;
+    c->last_launches = 1;
+    c->last_steps = 0;
+    if (herr == 4) fail(SDDG_ERR_NUMERICAL, "solve_dirichlet: maximum principle violated");
+}
+
+// ------------------------------------------------------------ decomposition
+
+struct Line {
+    bool vertical;
+    int fixed;
+    int length;
+};
+
+struct Layout {
+    int nx, ny, sx, sy, bx, by;
+    sddg_domain dom;
+    std::vector<Line> lines;
+    double hx() const { return (dom.xmax - dom.xmin) / (nx - 1); }
+    double hy() const { return (dom.ymax - dom.ymin) / (ny - 1); }
+};
+
+// build_layout (proj/src/decomposition.cpp:26-53)
+Layout build_layout(const sddg_domain& dom, int nx, int ny, int sx, int sy) {
+    check_domain(dom);
+    if (nx < 3 || ny < 3) fail(SDDG_ERR_VALIDATION, "GridSpec: needs nx >= 3 and ny >= 3");
+    if (sx < 1 || sy < 1) fail(SDDG_ERR_LAYOUT, "build_layout: subdomain counts must be >= 1");
+    if ((nx - 1) % sx != 0)
+        fail(SDDG_ERR_LAYOUT, "build_layout: nx-1=" + std::to_string(nx - 1) +
+                                  " not divisible by " + std::to_string(sx) + " (x axis)");
+    if ((ny - 1) % sy != 0)
+        fail(SDDG_ERR_LAYOUT, "build_layout: ny-1=" + std::to_string(ny - 1) +
+                                  " not divisible by " + std::to_string(sy) + " (y axis)");
+    Layout L{nx, ny, sx, sy, (nx - 1) / sx, (ny - 1) / sy, dom, {}};
+    if (L.bx < 2 || L.by < 2)
+        fail(SDDG_ERR_LAYOUT, "build_layout: subdomains need at least 3 nodes per axis");
+    for (int a = 1; a < sx; ++a) L.lines.push_back({true, a * L.bx, ny});
+    for (int b = 1; b < sy; ++b) L.lines.push_back({false, b * L.by, nx});
+    return L;
+}
+
+void mark_extrema(const std::vector<double>& v, std::vector<char>& marks) {
+    const int n = static_cast<int>(v.size());
+    double vmax = 0.0;
+    for (double x : v) vmax = std::max(vmax, std::abs(x));
+    const double floor_mag = 1e-9 * vmax;
+    for (int i = 1; i + 1 < n; ++i) {
+        if (std::abs(v[i]) < floor_mag) continue;
+        const bool is_max = v[i] > v[i - 1] && v[i] > v[i + 1];
+        const bool is_min = v[i] < v[i - 1] && v[i] < v[i + 1];
+        if (is_max || is_min) marks[i] = 1;
+    }
+}
+
+// plan_interface_points (proj/src/decomposition.cpp:81-145)
+std::vector<std::vector<int>> plan(const sddg_density& d, const Layout& L, int strategy, int k) {
+    std::vector<std::vector<int>> out;
+    const HostDensity h = host_density(d);
+    for (const Line& line : L.lines) {
+        const int n = line.length;
+        std::vector<int> nodes;
+        if (strategy == SDDG_PLACE_ALL) {
+            for (int p = 1; p + 1 < n; ++p) nodes.push_back(p);
+        } else if (strategy == SDDG_PLACE_EQUISPACED) {
+            if (k < 1 || k > n - 2)
+                fail(SDDG_ERR_VALIDATION, "plan_interface_points: equispaced count " +
+                                              std::to_string(k) + " not in [1, " +
+                                              std::to_string(n - 2) + "]");
+            for (int j = 1; j <= k; ++j) {
+                const int pos = static_cast<int>(std::lround(static_cast<double>(j) * (n - 1) / (k + 1)));
+                nodes.push_back(std::clamp(pos, 1, n - 2));
+            }
+            nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+        } else if (strategy == SDDG_PLACE_OPTIMAL) {
+            const double hstep = line.vertical ? L.hy() : L.hx();
+            std::vector<double> d1(n), d2(n, 0.0);
+            for (int p = 0; p < n; ++p) {
+                const double x = line.vertical ? L.dom.xmin + line.fixed * L.hx() : L.dom.xmin + p * L.hx();
+                const double y = line.vertical ? L.dom.ymin + p * L.hy() : L.dom.ymin + line.fixed * L.hy();
+                double gx, gy;
+                h.grad(x, y, gx, gy);
+                d1[p] = line.vertical ? gy : gx;
+            }
+            for (int p = 1; p + 1 < n; ++p) d2[p] = (d1[p + 1] - d1[p - 1]) / (2.0 * hstep);
+            std::vector<char> marks(n, 0);
+            mark_extrema(d1, marks);
+            mark_extrema(d2, marks);
+            for (int p = 1; p + 1 < n; ++p) {
+                if (!marks[p]) continue;
+                if (!nodes.empty() && p - nodes.back() < 2) continue;
+                nodes.push_back(p);
+            }
+            if (nodes.empty()) nodes.push_back(n / 2);
+        } else {
+            fail(SDDG_ERR_VALIDATION, "unknown placement strategy");
+        }
+        out.push_back(std::move(nodes));
+    }
+    return out;
+}
+
+// make_boundary_data (proj/src/boundary.cpp:44-56) / identity tables.
+std::vector<std::vector<double>> boundary_tables(const sddg_density& d, const sddg_domain& dom,
+                                                 int nx, int ny, int mode) {
+    const double hx = (dom.xmax - dom.xmin) / (nx - 1), hy = (dom.ymax - dom.ymin) / (ny - 1);
+    std::vector<std::vector<double>> t(8);
+    if (mode == SDDG_BC_IDENTITY) {
+        std::vector<double> fx(nx), gy(ny);
+        for (int i = 0; i < nx; ++i) fx[i] = ((dom.xmin + i * hx) - dom.xmin) / (dom.xmax - dom.xmin);
+        for (int j = 0; j < ny; ++j) gy[j] = ((dom.ymin + j * hy) - dom.ymin) / (dom.ymax - dom.ymin);
+        fx[0] = 0.0;
+        fx[nx - 1] = 1.0;
+        gy[0] = 0.0;
+        gy[ny - 1] = 1.0;
+        t = {fx, fx, std::vector<double>(ny, 0.0), std::vector<double>(ny, 1.0),
+             std::vector<double>(nx, 0.0), std::vector<double>(nx, 1.0), gy, gy};
+        return t;
+    }
+    if (mode != SDDG_BC_REFERENCE) fail(SDDG_ERR_VALIDATION, "unknown bc_mode");
+    const HostDensity h = host_density(d);
+    // solve_1d_boundary (proj/src/detsolver.cpp:20-48)
+    auto solve1d = [&](int edge) {
+        const bool horiz = edge < 2;
+        const int n = horiz ? nx : ny;
+        std::vector<double> rho(n), u(n);
+        for (int k = 0; k < n; ++k) {
+            double x, y;
+            switch (edge) {
+                case 0: x = dom.xmin + k * hx; y = dom.ymin + 0 * hy; break;
+                case 1: x = dom.xmin + k * hx; y = dom.ymin + (ny - 1) * hy; break;
+                case 2: x = dom.xmin + 0 * hx; y = dom.ymin + k * hy; break;
+                default: x = dom.xmin + (nx - 1) * hx; y = dom.ymin + k * hy; break;
+            }
+            rho[k] = h.rho(x, y);
+            if (!(rho[k] > 0.0))
+                fail(SDDG_ERR_EVALUATION, "solve_1d_boundary: non-positive density on an edge");
+        }
+        u[0] = 0.0;
+        for (int k = 1; k < n; ++k) u[k] = u[k - 1] + 0.5 * (rho[k - 1] + rho[k]);
+        const double total = u[n - 1];
+        for (int k = 1; k < n - 1; ++k) u[k] /= total;
+        u[n - 1] = 1.0;
+        return u;
+    };
+    t[0] = solve1d(0);
+    t[1] = solve1d(1);
+    t[2] = std::vector<double>(ny, 0.0);
+    t[3] = std::vector<double>(ny, 1.0);
+    t[4] = std::vector<double>(nx, 0.0);
+    t[5] = std::vector<double>(nx, 1.0);
+    t[6] = solve1d(2);
+    t[7] = solve1d(3);
+    return t;
+}
+
+struct IfcResult {
+    std::vector<std::vector<double>> xi, eta, sxi, seta;
+    int64_t mc_points = 0, restarts = 0, path_steps = 0;
+    int warnings = 0;
+};
+
+// solve_interfaces (proj/src/decomposition.cpp:147-248), walks on the GPU.
+IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
+                           const std::vector<std::vector<int>>& pl, const sddg_boundary& bd,
+                           const sddg_walk_config& cfg) {
+    std::map<uint64_t, size_t> index_of;
+    std::vector<double> px, py;
+    std::vector<uint64_t> gid;
+    auto node_xy = [&](const Line& ln, int pos, double& x, double& y) {
+        const int i = ln.vertical ? ln.fixed : pos, j = ln.vertical ? pos : ln.fixed;
+        x = L.dom.xmin + i * L.hx();
+        y = L.dom.ymin + j * L.hy();
+    };
+    auto node_gid = [&](const Line& ln, int pos) -> uint64_t {
+        const uint64_t i = ln.vertical ? ln.fixed : pos, j = ln.vertical ? pos : ln.fixed;
+        return j * static_cast<uint64_t>(L.nx) + i;
+    };
+    for (size_t l = 0; l < L.lines.size(); ++l)
+        for (int pos : pl[l]) {
+            const uint64_t g = node_gid(L.lines[l], pos);
+            if (index_of.emplace(g, px.size()).second) {
+                double x, y;
+                node_xy(L.lines[l], pos, x, y);
+                px.push_back(x);
+                py.push_back(y);
+                gid.push_back(g);
+            }
+        }
+    IfcResult out;
+    std::vector<sddg_estimate> est(px.size());
+    if (!px.empty()) {
+        estimates_host(c, d, L.dom, bd, cfg, px.data(), py.data(), gid.data(),
+                       static_cast<int64_t>(px.size()), est.data());
+        out.path_steps = c->last_steps;
+    }
+    out.mc_points = static_cast<int64_t>(px.size());
+    for (const auto& e : est) {
+        out.restarts += e.restarts;
+        if (e.warn) ++out.warnings;
+    }
+    const size_t nl = L.lines.size();
+    out.xi.resize(nl);
+    out.eta.resize(nl);
+    out.sxi.resize(nl);
+    out.seta.resize(nl);
+    for (size_t l = 0; l < nl; ++l) {
+        const Line& ln = L.lines[l];
+        const int n = ln.length, fi = ln.fixed;
+        std::vector<double> xi(n, 0.0), eta(n, 0.0), sx(n, 0.0), se(n, 0.0);
+        std::vector<char> known(n, 0);
+        xi[0] = ln.vertical ? bd.f[0][fi] : bd.f[2][fi];
+        eta[0] = ln.vertical ? bd.g[0][fi] : bd.g[2][fi];
+        xi[n - 1] = ln.vertical ? bd.f[1][fi] : bd.f[3][fi];
+        eta[n - 1] = ln.vertical ? bd.g[1][fi] : bd.g[3][fi];
+        known[0] = known[n - 1] = 1;
+        for (int pos = 1; pos + 1 < n; ++pos) {
+            auto it = index_of.find(node_gid(ln, pos));
+            if (it == index_of.end()) continue;
+            const sddg_estimate& e = est[it->second];
+            xi[pos] = e.xi;
+            eta[pos] = e.eta;
+            sx[pos] = e.se_xi;
+            se[pos] = e.se_eta;
+            known[pos] = 1;
+        }
+        int prev = 0;
+        for (int pos = 1; pos < n; ++pos) {
+            if (!known[pos]) continue;
+            for (int q = prev + 1; q < pos; ++q) {
+                const double t = static_cast<double>(q - prev) / (pos - prev);
+                xi[q] = (1.0 - t) * xi[prev] + t * xi[pos];
+                eta[q] = (1.0 - t) * eta[prev] + t * eta[pos];
+            }
+            prev = pos;
+        }
+        out.xi[l] = std::move(xi);
+        out.eta[l] = std::move(eta);
+        out.sxi[l] = std::move(sx);
+        out.seta[l] = std::move(se);
+    }
+    for (size_t lv = 0; lv < nl; ++lv) {
+        if (!L.lines[lv].vertical) continue;
+        for (size_t lh = 0; lh < nl; ++lh) {
+            if (L.lines[lh].vertical) continue;
+            const int iv = L.lines[lv].fixed, jh = L.lines[lh].fixed;
+            const uint64_t g = static_cast<uint64_t>(jh) * L.nx + iv;
+            if (index_of.count(g)) continue;
+            out.xi[lh][iv] = out.xi[lv][jh];
+            out.eta[lh][iv] = out.eta[lv][jh];
+        }
+    }
+    return out;
+}
+
+sddg_boundary make_boundary_view(const sddg_domain& dom, int nx, int ny,
+                                 const std::vector<std::vector<double>>& t) {
+    sddg_boundary b;
+    b.dom = dom;
+    b.nx = nx;
+    b.ny = ny;
+    for (int k = 0; k < 4; ++k) {
+        b.f[k] = t[k].data();
+        b.g[k] = t[4 + k].data();
+    }
+    return b;
+}
+
+sddg_status finish(sddg_ctx* c, const Fail& f) {
+    if (c) c->err = f.msg;
+    else g_free_err = f.msg;
+    return f.st;
+}
+
+#define API_BEGIN(ctx)                                   \
+    if (!(ctx)) {                                        \
+        g_free_err = "NULL context";                     \
+        return SDDG_ERR_VALIDATION;                      \
+    }                                                    \
+    std::lock_guard<std::mutex> _lk((ctx)->mu);          \
+    try {                                                \
+        ck(cudaSetDevice((ctx)->device), "cudaSetDevice");
+#define API_END(ctx)                                     \
+    }                                                    \
+    catch (const Fail& f) {                              \
+        return finish((ctx), f);                         \
+    }                                                    \
+    catch (const std::exception& e) {                    \
+        return finish((ctx), Fail{SDDG_ERR_INTERNAL, e.what()}); \
+    }                                                    \
+    (ctx)->err.clear();                                  \
+    return SDDG_OK;
+
+}  // namespace
+
+namespace sddg {
+
+bool walk_variant_supported(int dv, int precision) {
+    if (dv >= 32 && dv <= 34) return true;
+    return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18));
+}
+
+cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s) {
+    if (!walk_variant_supported(dv, precision)) return cudaErrorInvalidValue;
+    if (dv >= 32) return launch_walk_fast(dv, precision, a, grid, s);
+    return launch_walk_ref(dv, a, grid, s);
+}
+
+cudaError_t walk_occupancy(int dv, int precision, int* b) {
+    if (!walk_variant_supported(dv, precision)) return cudaErrorInvalidValue;
+    if (dv >= 32) return occupancy_walk_fast(dv, precision, b);
+    return occupancy_walk_ref(dv, b);
+}
+
+}  // namespace sddg
+
+extern "C" {
+
+const char* sddg_version(void) { return "sddg 0.1 (sm_100a)"; }
+int sddg_abi_version(void) { return SDDG_ABI_VERSION; }
+
+sddg_status sddg_device_count(int32_t* n) {
+    int k = 0;
+    const cudaError_t e = cudaGetDeviceCount(&k);
+    *n = e == cudaSuccess ? k : 0;
+    return e == cudaSuccess ? SDDG_OK : SDDG_ERR_CUDA;
+}
+
+sddg_status sddg_create(int32_t device, sddg_ctx** out) {
+    *out = nullptr;
+    try {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (device < 0 || device >= n) fail(SDDG_ERR_CUDA, "no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp p;
+        ck(cudaGetDeviceProperties(&p, device), "properties");
+        if (p.major != 10 || p.minor != 0)
+            fail(SDDG_ERR_CUDA, std::string("sddg is built for sm_100a (B200); device is ") + p.name);
+        auto* c = new sddg_ctx();
+        c->device = device;
+        c->sms = p.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        ck(cudaEventCreate(&c->ev0), "event");
+        ck(cudaEventCreate(&c->ev1), "event");
+        *out = c;
+    } catch (const Fail& f) {
+        g_free_err = f.msg;
+        return f.st;
+    }
+    return SDDG_OK;
+}
+
+void sddg_destroy(sddg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
+                      &c->counters, &c->dump, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->s_coef, &c->s_err})
+        b->release();
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* sddg_last_error(const sddg_ctx* c) { return c ? c->err.c_str() : g_free_err.c_str(); }
+
+sddg_status sddg_last_stats(const sddg_ctx* c, int64_t* steps, int64_t* launches, double* ms) {
+    if (!c) return SDDG_ERR_VALIDATION;
+    if (steps) *steps = c->last_steps;
+    if (launches) *launches = c->last_launches;
+    if (ms) *ms = c->last_ms;
+    return SDDG_OK;
+}
+
+sddg_status sddg_mc_estimate_batch(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                   const sddg_boundary* bd, const sddg_walk_config* cfg,
+                                   const double* px, const double* py, const uint64_t* pid,
+                                   int64_t n, sddg_estimate* out) {
+    API_BEGIN(ctx)
+    estimates_host(ctx, *dens, *dom, *bd, *cfg, px, py, pid, n, out);
+    API_END(ctx)
+}
+
+sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* dens,
+                                          const sddg_domain* dom, const sddg_boundary* bd,
+                                          const sddg_walk_config* cfg, const double* d_px,
+                                          const double* d_py, const uint64_t* d_pid, int64_t n,
+                                          sddg_estimate* d_out, void* stream) {
+    API_BEGIN(ctx)
+    validate_walk(*cfg);
+    check_domain(*dom);
+    check_boundary(*bd);
+    drift_variant(*dens, cfg->precision);
+    check_positivity(*dens, *dom);
+    if (n > 0) {
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        std::vector<double> hx(n), hy(n);
+        ck(cudaMemcpyAsync(hx.data(), d_px, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(hy.data(), d_py, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "sync");
+        check_points(*dom, hx.data(), hy.data(), n);
+        run_estimates(ctx, *dens, *dom, *bd, *cfg, d_px, d_py, d_pid, n, d_out, st);
+    }
+    API_END(ctx)
+}
+
+sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                           const sddg_boundary* bd, const sddg_walk_config* cfg, double px,
+                           double py, uint64_t pid, int64_t walk_lo, int64_t n, sddg_path* out) {
+    API_BEGIN(ctx)
+    validate_walk(*cfg);
+    check_domain(*dom);
+    check_boundary(*bd);
+    const int dv = drift_variant(*dens, cfg->precision);
+    check_positivity(*dens, *dom);
+    check_points(*dom, &px, &py, 1);
+    if (walk_lo < 0 || walk_lo + n > 0x100000000LL)
+        fail(SDDG_ERR_VALIDATION, "walk range must fit the 32-bit stream walk id");
+    if (n > 0) {
+        cudaStream_t st = ctx->stream;
+        const double* dtab = upload_tables(ctx, *bd);
+        char* nb = static_cast<char*>(ctx->nodes.ensure(3 * sizeof(double)));
+        double* dn = reinterpret_cast<double*>(nb);
+        unsigned char hv[3 * sizeof(double)];
+        std::memcpy(hv, &px, sizeof(double));
+        std::memcpy(hv + sizeof(double), &py, sizeof(double));
+        std::memcpy(hv + 2 * sizeof(double), &pid, sizeof(uint64_t));
+        ck(cudaMemcpyAsync(dn, hv, sizeof(hv), cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaStreamSynchronize(st), "sync");
+        Counters* cnt = static_cast<Counters*>(ctx->counters.ensure(sizeof(Counters)));
+        ck(cudaMemsetAsync(cnt, 0, sizeof(Counters), st), "memset");
+        sddg_path* dd = static_cast<sddg_path*>(ctx->dump.ensure(sizeof(sddg_path) * n));
+        WalkArgs a;
+        fill_args(a, *dens, *dom, *bd, *cfg, dtab);
+        a.px = dn;
+        a.py = dn + 1;
+        a.pid = reinterpret_cast<const uint64_t*>(dn + 2);
+        a.walks = n;
+        a.walk_lo = walk_lo;
+        a.total = static_cast<uint64_t>(n);
+        a.next = &cnt->next;
+        a.steps = &cnt->steps;
+        a.err_flag = &cnt->err_flag;
+        a.err_info = &cnt->err_info;
+        a.dump = dd;
+        const int grid = walk_grid(ctx, dv, cfg->precision, a.total);
+        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * kWalkBlock);
+        ck(cudaEventRecord(ctx->ev0, st), "event");
+        ck(launch_walk(dv, cfg->precision, a, grid, st), "walk kernel launch");
+        ck(cudaEventRecord(ctx->ev1, st), "event");
+        Counters hc;
+        ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaMemcpyAsync(out, dd, sizeof(sddg_path) * n, cudaMemcpyDeviceToHost, st), "d2h");
+        ck(cudaStreamSynchronize(st), "walk dump");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+        ctx->last_ms = ms;
+        ctx->last_steps = static_cast<int64_t>(hc.steps);
+        ctx->last_launches = 2;
+        raise_kernel_error(hc);
+    }
+    API_END(ctx)
+}
+
+sddg_status sddg_solve_dirichlet_batch(sddg_ctx* ctx, const double* w, int32_t gnx, int32_t gny,
+                                       double hx, double hy, int64_t n, const sddg_subdomain* subs,
+                                       const double* bc, const sddg_solver_config* sc, double* u,
+                                       sddg_solve_info* info) {
+    API_BEGIN(ctx)
+    solve_batch_host(ctx, w, gnx, gny, hx, hy, n, subs, bc, *sc, u, info);
+    API_END(ctx)
+}
+
+sddg_status sddg_make_boundary_data(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
+                                    int32_t ny, int32_t mode, double* tables8[8]) {
+    try {
+        check_domain(*dom);
+        if (nx < 3 || ny < 3) fail(SDDG_ERR_VALIDATION, "GridSpec: needs nx >= 3 and ny >= 3");
+        const auto t = boundary_tables(*dens, *dom, nx, ny, mode);
+        for (int k = 0; k < 8; ++k) std::memcpy(tables8[k], t[k].data(), sizeof(double) * t[k].size());
+    } catch (const Fail& f) {
+        return finish(nullptr, f);
+    } catch (const std::exception& e) {
+        return finish(nullptr, Fail{SDDG_ERR_EVALUATION, e.what()});
+    }
+    return SDDG_OK;
+}
+
+sddg_status sddg_plan_interface_points(const sddg_density* dens, const sddg_domain* dom,
+                                       int32_t nx, int32_t ny, int32_t sx, int32_t sy,
+                                       int32_t placement, int32_t k, int32_t* n_lines,
+                                       int32_t* vert, int32_t* fixed, int32_t* counts,
+                                       int32_t* nodes) {
+    try {
+        const Layout L = build_layout(*dom, nx, ny, sx, sy);
+        const auto pl = plan(*dens, L, placement, k);
+        *n_lines = static_cast<int32_t>(L.lines.size());
+        int off = 0;
+        for (size_t l = 0; l < L.lines.size(); ++l) {
+            vert[l] = L.lines[l].vertical ? 1 : 0;
+            fixed[l] = L.lines[l].fixed;
+            counts[l] = static_cast<int32_t>(pl[l].size());
+            for (int v : pl[l]) nodes[off++] = v;
+        }
+    } catch (const Fail& f) {
+        return finish(nullptr, f);
+    } catch (const std::exception& e) {
+        return finish(nullptr, Fail{SDDG_ERR_EVALUATION, e.what()});
+    }
+    return SDDG_OK;
+}
+
+sddg_status sddg_solve_interfaces(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                  int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t placement,
+                                  int32_t k, const sddg_boundary* bd, const sddg_walk_config* cfg,
+                                  double* xi, double* eta, double* sxi, double* seta,
+                                  sddg_sdd_stats* stats) {
+    API_BEGIN(ctx)
+    const double t0 = now_s();
+    const Layout L = build_layout(*dom, nx, ny, sx, sy);
+    const auto pl = plan(*dens, L, placement, k);
+    const IfcResult r = solve_interfaces(ctx, *dens, L, pl, *bd, *cfg);
+    size_t off = 0;
+    for (size_t l = 0; l < r.xi.size(); ++l) {
+        const size_t n = r.xi[l].size();
+        std::memcpy(xi + off, r.xi[l].data(), sizeof(double) * n);
+        std::memcpy(eta + off, r.eta[l].data(), sizeof(double) * n);
+        if (sxi) std::memcpy(sxi + off, r.sxi[l].data(), sizeof(double) * n);
+        if (seta) std::memcpy(seta + off, r.seta[l].data(), sizeof(double) * n);
+        off += n;
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->t_stoc = r.mc_points > 0 ? now_s() - t0 : 0.0;
+        stats->mc_points = r.mc_points;
+        stats->restarts = r.restarts;
+        stats->path_steps = r.path_steps;
+        stats->warnings = r.warnings;
+    }
+    API_END(ctx)
+}
+
+sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                           int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t placement,
+                           int32_t k, int32_t bc_mode, const sddg_walk_config* cfg,
+                           const sddg_solver_config* sc, double* xi, double* eta,
+                           sddg_sdd_stats* stats) {
+    API_BEGIN(ctx)
+    // solve_sdd (proj/src/decomposition.cpp:262-385)
+    const Layout L = build_layout(*dom, nx, ny, sx, sy);
+    const double tb0 = now_s();
+    const auto tabs = boundary_tables(*dens, *dom, nx, ny, bc_mode);
+    const double t_bd = now_s() - tb0;
+    const sddg_boundary bd = make_boundary_view(*dom, nx, ny, tabs);
+    const auto pl = plan(*dens, L, placement, k);
+    const double t0 = now_s();
+    const IfcResult ifc = solve_interfaces(ctx, *dens, L, pl, bd, *cfg);
+    const double t_stoc = ifc.mc_points > 0 ? now_s() - t0 : 0.0;
+    const int64_t steps = ifc.path_steps;
+
+    std::map<int, size_t> vline, hline;
+    for (size_t l = 0; l < L.lines.size(); ++l) {
+        if (L.lines[l].vertical) vline[L.lines[l].fixed] = l;
+        else hline[L.lines[l].fixed] = l;
+    }
+    const double ts0 = now_s();
+    // weight_values on the global grid (detsolver.cpp:219-224)
+    const HostDensity h = host_density(*dens);
+    std::vector<double> w(static_cast<size_t>(nx) * ny);
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i)
+            w[static_cast<size_t>(j) * nx + i] = 1.0 / h.rho(dom->xmin + i * L.hx(), dom->ymin + j * L.hy());
+    const int n_sub = sx * sy;
+    std::vector<sddg_subdomain> subs;
+    std::vector<double> bc;
+    for (int s = 0; s < n_sub; ++s) {
+        const int a = s % sx, b = s / sx;
+        const sddg_subdomain q{a * L.bx, b * L.by, L.bx + 1, L.by + 1};
+        for (int field = 0; field < 2; ++field) {
+            const bool fxi = field == 0;
+            auto edge = [&](int e) {
+                const bool horiz = e < 2;
+                const int len = horiz ? q.nx : q.ny, lo = horiz ? q.i0 : q.j0;
+                const std::vector<double>* src;
+                if (e == 0) src = q.j0 == 0 ? &tabs[fxi ? 0 : 4] : (fxi ? &ifc.xi[hline.at(q.j0)] : &ifc.eta[hline.at(q.j0)]);
+                else if (e == 1) {
+                    const int j1 = q.j0 + q.ny - 1;
+                    src = j1 == ny - 1 ? &tabs[fxi ? 1 : 5] : (fxi ? &ifc.xi[hline.at(j1)] : &ifc.eta[hline.at(j1)]);
+                } else if (e == 2) src = q.i0 == 0 ? &tabs[fxi ? 2 : 6] : (fxi ? &ifc.xi[vline.at(q.i0)] : &ifc.eta[vline.at(q.i0)]);
+                else {
+                    const int i1 = q.i0 + q.nx - 1;
+                    src = i1 == nx - 1 ? &tabs[fxi ? 3 : 7] : (fxi ? &ifc.xi[vline.at(i1)] : &ifc.eta[vline.at(i1)]);
+                }
+                bc.insert(bc.end(), src->begin() + lo, src->begin() + lo + len);
+            };
+            for (int e = 0; e < 4; ++e) edge(e);
+            subs.push_back(q);
+        }
+    }
+    std::vector<double> u(static_cast<size_t>(2 * n_sub) * (L.bx + 1) * (L.by + 1));
+    std::vector<sddg_solve_info> info(2 * n_sub);
+    solve_batch_host(ctx, w.data(), nx, ny, L.hx(), L.hy(), 2 * n_sub, subs.data(), bc.data(), *sc,
+                     u.data(), info.data());
+    int warns = ifc.warnings;
+    size_t off = 0;
+    for (int s = 0; s < 2 * n_sub; ++s) {
+        const sddg_subdomain& q = subs[s];
+        double* dst = (s % 2 == 0) ? xi : eta;
+        for (int j = 0; j < q.ny; ++j)
+            for (int i = 0; i < q.nx; ++i)
+                dst[static_cast<size_t>(q.j0 + j) * nx + (q.i0 + i)] = u[off + static_cast<size_t>(j) * q.nx + i];
+        off += static_cast<size_t>(q.nx) * q.ny;
+        if (!info[s].converged) ++warns;
+    }
+    if (stats) {
+        stats->t_bd = t_bd;
+        stats->t_stoc = t_stoc;
+        stats->t_sub = t_bd + (now_s() - ts0);
+        stats->t_smooth = 0.0;
+        stats->mc_points = ifc.mc_points;
+        stats->subdomain_solves = 2 * n_sub;
+        stats->restarts = ifc.restarts;
+        stats->path_steps = steps;
+        stats->warnings = warns;
+        stats->reserved = 0;
+    }
+    API_END(ctx)
+}
+
+}  // extern "C"

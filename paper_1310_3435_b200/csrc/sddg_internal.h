@@ -1,0 +1,79 @@
+// sddg_internal.h -- kernel argument blocks and launcher declarations shared
+// by the CUDA translation units and the host runtime.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/sddg.h"
+
+namespace sddg {
+
+constexpr int kWalkBlock = 128;   // threads per walk CTA
+constexpr int64_t kChunk = 256;   // reference mc_estimate chunk (proj/src/sde.cpp:201)
+
+struct WalkArgs {
+    // walk domain (sdd::RectDomain passed to mc_estimate)
+    double xmin, xmax, ymin, ymax;
+    // boundary tables (BoundaryData over the table grid)
+    double txmin, tymin, thx, thy;
+    int tnx, tny;
+    const double* tf[4];
+    const double* tg[4];
+    // density
+    double R, alpha, fd_h;
+    // walk config
+    int scheme, bridge;
+    double dt, sqrt2dt, lambda, nu2, bridge_thr;
+    uint64_t seed;
+    int64_t max_steps;
+    // batch: total = n_nodes * walks
+    const double* px;
+    const double* py;
+    const uint64_t* pid;
+    int64_t walks;
+    int64_t walk_lo;
+    uint64_t total;
+    unsigned long long* next;   // global walk counter (starts at the grid size)
+    unsigned long long* steps;  // executed path-steps
+    int* err_flag;              // 3 EvaluationError, 4 NumericalError
+    unsigned long long* err_info;
+    // outputs: per-walk records, or per-path dumps
+    double* rec_f;
+    double* rec_g;
+    uint32_t* rec_meta;  // edge | epochs_used << 2
+    sddg_path* dump;
+};
+
+// walk_ref.cu (fp64, -fmad=false) and walk_fast.cu (analytic drifts, fp64 + fp32)
+bool walk_variant_supported(int dv, int precision);
+cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
+cudaError_t walk_occupancy(int dv, int precision, int* blocks_per_sm);
+// the two TUs' own dispatchers
+cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s);
+cudaError_t occupancy_walk_ref(int dv, int* b);
+cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
+cudaError_t occupancy_walk_fast(int dv, int precision, int* b);
+
+// reduce.cu: K2 fixed chunk-order finalize, one CTA per node
+cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
+                          int64_t walks, int64_t n_nodes, sddg_estimate* out, cudaStream_t s);
+
+// solver.cu: K3 batched Dirichlet solves
+struct SolveJob {
+    int i0, j0, nx, ny;
+    int64_t bc_off;  // offset of bottom[nx] top[nx] left[ny] right[ny] in bc
+    int64_t u_off;   // offset of the nx*ny solution
+};
+// coef_in_smem: cE/cN/inv_den in shared memory (4*max_n doubles of smem),
+// else in coef_scratch (n_jobs * 3*max_n doubles).  max_interior <=
+// solver_max_points() for METHOD Jacobi.
+int solver_max_points();
+cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
+                               int64_t n_jobs, const SolveJob* jobs, const double* bc,
+                               double tol, int64_t max_iters_cfg, int init_blend, int method,
+                               double omega, double* u, sddg_solve_info* info, int* err,
+                               cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
+                               int coef_in_smem);
+
+}  // namespace sddg

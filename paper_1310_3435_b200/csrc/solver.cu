@@ -1,0 +1,262 @@
+// solver.cu -- K3: batched Dirichlet solves of the conservative five-point
+// generator stencil, one CTA per (subdomain, field), the solution resident in
+// shared memory for the whole solve.
+//
+// Reference: solve_dirichlet (proj/src/detsolver.cpp:72-209).
+//  * half-point weights cE = (w_i + w_{i+1})/2, cN (:88-102); inv_den (:107-111)
+//  * transfinite-blend initial guess clamped to [bmin, bmax] (:121-148)
+//  * iteration (:156-171) and stopping rule (:175-187)
+//  * maximum-principle check (:191-198)
+// METHOD 0 (Jacobi) performs the reference's iteration with the same
+// rounding sequence (this TU is built with -fmad=false; max is exact), so
+// iterates, iteration count and result are bit-identical to the reference.
+// METHOD 1 (red-black SOR) converges to the same discrete fixed point in
+// O(n) instead of O(n^2) sweeps.
+//
+// Shared memory: u (nx*ny fp64) always; the coefficient arrays cE, cN,
+// inv_den (stored with row stride nx) also in smem when they fit, else read
+// through L1/L2 from a global scratch laid out the same way.
+#include <cfloat>
+
+#include "sddg_internal.h"
+
+namespace sddg {
+
+namespace {
+
+constexpr int kSolveThreads = 512;
+
+struct BlockMax {
+    __device__ static double reduce(double v, double* red) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = v < u ? u : v;
+        }
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) red[wid] = v;
+        __syncthreads();
+        double m = red[0];
+        const int nw = (blockDim.x + 31) >> 5;
+        for (int k = 1; k < nw; ++k) m = m < red[k] ? red[k] : m;
+        __syncthreads();
+        return m;
+    }
+};
+
+template <int METHOD, int PTS>
+__global__ void __launch_bounds__(kSolveThreads)
+solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
+             const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
+             int64_t max_iters_cfg, int init_blend, double omega, double* __restrict__ uout,
+             sddg_solve_info* __restrict__ info, double* __restrict__ coef_scratch,
+             int64_t coef_stride, int coef_in_smem, int* err) {
+    extern __shared__ double smem[];
+    __shared__ double red[kSolveThreads / 32];
+    const SolveJob J = jobs[blockIdx.x];
+    const int nx = J.nx, ny = J.ny;
+    const int N = nx * ny;
+    double* u = smem;
+    double* cE;
+    double* cN;
+    double* inv;
+    if (coef_in_smem) {
+        cE = smem + N;
+        cN = cE + N;
+        inv = cN + N;
+    } else {
+        cE = coef_scratch + blockIdx.x * coef_stride;
+        cN = cE + N;
+        inv = cN + N;
+    }
+    const double* B = bc + J.bc_off;
+    const double* T = B + nx;
+    const double* L = T + nx;
+    const double* Rt = L + ny;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    // coefficients from the global weights (detsolver.cpp:88-111)
+    for (int c = tid; c < N; c += nt) {
+        const int i = c % nx, j = c / nx;
+        const double wc = wg[(int64_t)(J.j0 + j) * gnx + (J.i0 + i)];
+        cE[c] = i + 1 < nx ? 0.5 * (wc + wg[(int64_t)(J.j0 + j) * gnx + (J.i0 + i + 1)]) : 0.0;
+        cN[c] = j + 1 < ny ? 0.5 * (wc + wg[(int64_t)(J.j0 + j + 1) * gnx + (J.i0 + i)]) : 0.0;
+    }
+    __syncthreads();
+    for (int c = tid; c < N; c += nt) {
+        const int i = c % nx, j = c / nx;
+        inv[c] = (i > 0 && j > 0 && i + 1 < nx && j + 1 < ny)
+                     ? 1.0 / ((cE[c] + cE[c - 1]) * ihx2 + (cN[c] + cN[c - nx]) * ihy2)
+                     : 0.0;
+    }
+    // boundary range (exact min/max, order free)
+    double lmin = DBL_MAX, lmax = -DBL_MAX;
+    for (int k = tid; k < 2 * (nx + ny); k += nt) {
+        const double v = B[k];  // B, T, L, Rt are contiguous
+        lmin = v < lmin ? v : lmin;
+        lmax = lmax < v ? v : lmax;
+    }
+    const double bmax = BlockMax::reduce(lmax, red);
+    const double bmin = -BlockMax::reduce(-lmin, red);
+    // initial guess (detsolver.cpp:121-148)
+    for (int c = tid; c < N; c += nt) {
+        const int i = c % nx, j = c / nx;
+        double v;
+        if (init_blend) {
+            const double ty = static_cast<double>(j) / (ny - 1);
+            const double tx = static_cast<double>(i) / (nx - 1);
+            const double xb = (1.0 - tx) * L[j] + tx * Rt[j];
+            const double yb = (1.0 - ty) * B[i] + ty * T[i];
+            const double bil = ((1.0 - tx) * (1.0 - ty) * B[0] + tx * ty * T[nx - 1]) +
+                               (tx * (1.0 - ty) * B[nx - 1] + (1.0 - tx) * ty * T[0]);
+            v = xb + yb - bil;
+            v = v < bmin ? bmin : (bmax < v ? bmax : v);
+        } else {
+            v = 0.5 * (bmin + bmax);
+        }
+        if (j == 0) v = B[i];
+        if (j == ny - 1) v = T[i];
+        if (i == 0) v = L[j];
+        if (i == nx - 1) v = Rt[j];
+        u[c] = v;
+    }
+    __syncthreads();
+
+    const int mi = nx - 2, mj = ny - 2;
+    const int64_t max_iters =
+        max_iters_cfg > 0 ? max_iters_cfg : 200LL * (nx > ny ? nx : ny) * (nx > ny ? nx : ny);
+    int64_t iters = 0;
+    double upd = 0.0, prev = -1.0;
+    bool conv = false;
+    // colour passes: METHOD 0 one pass over all interior points; METHOD 1
+    // two passes (i+j even, then odd) updated in place.
+    const int half = (mi + 1) / 2;
+    while (iters < max_iters) {
+        ++iters;
+        double lupd = 0.0;
+        if (METHOD == 0) {
+            // two-phase in-place Jacobi: every thread reads the old iterate
+            // for its PTS points, barrier, then writes them
+            double nu[PTS];
+#pragma unroll
+            for (int k = 0; k < PTS; ++k) {
+                const int p = tid + k * nt;
+                if (p < mi * mj) {
+                    const int c = (p / mi + 1) * nx + (p % mi + 1);
+                    const double xp = (cE[c] * u[c + 1] + cE[c - 1] * u[c - 1]) * ihx2;
+                    const double yp = (cN[c] * u[c + nx] + cN[c - nx] * u[c - nx]) * ihy2;
+                    nu[k] = (xp + yp) * inv[c];
+                    const double du = fabs(nu[k] - u[c]);
+                    lupd = lupd < du ? du : lupd;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int k = 0; k < PTS; ++k) {
+                const int p = tid + k * nt;
+                if (p < mi * mj) u[(p / mi + 1) * nx + (p % mi + 1)] = nu[k];
+            }
+        } else {
+#pragma unroll 1
+            for (int colour = 0; colour < 2; ++colour) {
+                for (int p = tid; p < mj * half; p += nt) {
+                    const int j = p / half + 1;
+                    const int i = 2 * (p % half) + 1 + ((j + 1 + colour) & 1);
+                    if (i > mi) continue;
+                    const int c = j * nx + i;
+                    const double xp = (cE[c] * u[c + 1] + cE[c - 1] * u[c - 1]) * ihx2;
+                    const double yp = (cN[c] * u[c + nx] + cN[c - nx] * u[c - nx]) * ihy2;
+                    const double gs = (xp + yp) * inv[c];
+                    const double nv = u[c] + omega * (gs - u[c]);
+                    const double du = fabs(nv - u[c]);
+                    lupd = lupd < du ? du : lupd;
+                    u[c] = nv;
+                }
+                __syncthreads();
+            }
+        }
+        upd = BlockMax::reduce(lupd, red);  // includes the barrier publishing u
+        if (upd < tol) {
+            if (upd == 0.0 || upd < 1e-4 * tol) {
+                conv = true;
+                break;
+            }
+            if (prev > 0.0 && upd < prev) {
+                const double rho = upd / prev;
+                if (upd * rho / (1.0 - rho) < tol) {
+                    conv = true;
+                    break;
+                }
+            }
+        }
+        prev = upd;
+    }
+    __syncthreads();
+    // maximum principle (detsolver.cpp:191-198) and write-out
+    const double slack = 1e-12 * (1.0 + fabs(bmin) + fabs(bmax));
+    double* U = uout + J.u_off;
+    for (int c = tid; c < N; c += nt) {
+        const int i = c % nx, j = c / nx;
+        const double v = u[c];
+        if (i > 0 && j > 0 && i + 1 < nx && j + 1 < ny && (v < bmin - slack || v > bmax + slack))
+            atomicCAS(err, 0, 4);
+        U[c] = v;
+    }
+    if (tid == 0) {
+        sddg_solve_info r;
+        r.iterations = iters;
+        r.final_update = upd;
+        r.converged = conv ? 1 : 0;
+        r.reserved = 0;
+        info[blockIdx.x] = r;
+    }
+}
+
+template <int METHOD, int PTS>
+cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, const double* wg,
+                       int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
+                       double tol, int64_t mi, int init_blend, double omega, double* u,
+                       sddg_solve_info* info, double* scratch, int64_t cstride, int cin,
+                       int* err) {
+    auto k = solve_kernel<METHOD, PTS>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    k<<<grid, threads, smem, st>>>(wg, gnx, ihx2, ihy2, jobs, bc, tol, mi, init_blend, omega, u,
+                                   info, scratch, cstride, cin, err);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int solver_max_points() { return kSolveThreads * 32; }
+
+cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
+                               int64_t n_jobs, const SolveJob* jobs, const double* bc,
+                               double tol, int64_t max_iters_cfg, int init_blend, int method,
+                               double omega, double* u, sddg_solve_info* info, int* err,
+                               cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
+                               int coef_in_smem) {
+    if (n_jobs <= 0) return cudaSuccess;
+    const double ihx2 = 1.0 / (hx * hx);
+    const double ihy2 = 1.0 / (hy * hy);
+    const size_t smem = sizeof(double) * static_cast<size_t>(max_n) * (coef_in_smem ? 4 : 1);
+    const int64_t cstride = 3LL * max_n;
+    const int grid = static_cast<int>(n_jobs);
+    const int T = kSolveThreads;
+    if (method == SDDG_SOLVER_RBSOR)
+        return launch_one<1, 1>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
+                                max_iters_cfg, init_blend, omega, u, info, coef_scratch, cstride,
+                                coef_in_smem, err);
+    const int pts = (max_interior + T - 1) / T;
+#define SDDG_J(P)                                                                             \
+    if (pts <= P)                                                                             \
+        return launch_one<0, P>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,   \
+                                max_iters_cfg, init_blend, omega, u, info, coef_scratch,      \
+                                cstride, coef_in_smem, err);
+    SDDG_J(1) SDDG_J(2) SDDG_J(4) SDDG_J(8) SDDG_J(16) SDDG_J(32)
+#undef SDDG_J
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace sddg

@@ -1,0 +1,320 @@
+// walk_kernel.cuh -- K1: persistent first-exit walk kernel.
+//
+// One walk per lane at a time; a lane whose walk exits writes the walk's
+// record and immediately takes the next walk index from a global counter, so
+// the heavy-tailed walk lengths (SURVEY.md 7 "Divergence") never idle a lane
+// until the batch tail.  Walk g of the batch is walk (walk_lo + g % walks) of
+// node g / walks.  Records go to HBM by walk index; K2 (reduce.cu) then sums
+// them in the reference's fixed 256-walk chunk order, so results do not depend
+// on which lane ran which walk.
+//
+// Per step (reference: run_walk, proj/src/sde.cpp:151-183; Appendix A of
+// SURVEY.md): drift -> one Philox block -> Box-Muller -> Euler-Maruyama
+// update -> explicit exit (segment_exit, sde.cpp:31-65) -> bridge test
+// (edge_crossing_test, sde.cpp:72-121).  The bridge test only draws for edges
+// with d0 d1/dt <= 40; a conservative product pre-filter skips the exact
+// sorted test on steps where no edge can qualify (no draw is consumed there
+// in the reference either, sde.cpp:92).
+#pragma once
+#include <cstdint>
+
+#include "density.cuh"
+#include "philox.cuh"
+#include "sddg_internal.h"
+
+namespace sddg {
+
+template <typename Real>
+struct RealOps;
+
+template <>
+struct RealOps<double> {
+    __device__ static __forceinline__ double u_open(uint64_t u) { return u01_open_d(u); }
+    __device__ static __forceinline__ double u(uint64_t u) { return u01_d(u); }
+    __device__ static __forceinline__ void box_muller(uint64_t a, uint64_t b, double& z0,
+                                                      double& z1) {
+        // rng.hpp:66-73
+        const double u1 = u01_open_d(a);
+        const double u2 = u01_d(b);
+        const double r = sqrt(-2.0 * log(u1));
+        const double ang = 6.283185307179586476925286766559 * u2;
+        double s, c;
+        sincos(ang, &s, &c);
+        z0 = r * c;
+        z1 = r * s;
+    }
+    __device__ static __forceinline__ double ex(double v) { return exp(v); }
+    __device__ static __forceinline__ double lg(double v) { return log(v); }
+    __device__ static __forceinline__ double sq(double v) { return sqrt(v); }
+};
+
+template <>
+struct RealOps<float> {
+    __device__ static __forceinline__ float u_open(uint64_t u) { return u01_open_f(u); }
+    __device__ static __forceinline__ float u(uint64_t u) { return u01_f(u); }
+    __device__ static __forceinline__ void box_muller(uint64_t a, uint64_t b, float& z0,
+                                                      float& z1) {
+        const float u1 = u01_open_f(a);
+        const float u2 = u01_f(b);
+        const float r = sqrtf(-2.0f * logf(u1));
+        float s, c;
+        sincospif(2.0f * u2, &s, &c);
+        z0 = r * c;
+        z1 = r * s;
+    }
+    __device__ static __forceinline__ float ex(float v) { return __expf(v); }
+    __device__ static __forceinline__ float lg(float v) { return logf(v); }
+    __device__ static __forceinline__ float sq(float v) { return sqrtf(v); }
+};
+
+template <int DV, typename Real>
+__device__ __forceinline__ bool drift(const DensityParams& P, Real x, Real y, Real& bx, Real& by) {
+    if constexpr (DV >= DV_RING_AN) {
+        return drift_an(DV, x, y, bx, by);
+    } else {
+        static_assert(sizeof(Real) == 8, "reference drifts are fp64 only");
+        return drift_ref<DV>(P, x, y, bx, by);
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ Real clampr(Real v, Real lo, Real hi) {
+    return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
+}
+
+template <typename Real>
+struct Dom {
+    Real xmin, xmax, ymin, ymax;
+    __device__ __forceinline__ bool inside(Real x, Real y) const {
+        return x > xmin && x < xmax && y > ymin && y < ymax;  // geometry.hpp:38-40
+    }
+    // geometry.cpp:24-32
+    __device__ __forceinline__ Real dist(Real x, Real y, int e) const {
+        return e == 0 ? y - ymin : (e == 1 ? ymax - y : (e == 2 ? x - xmin : xmax - x));
+    }
+    __device__ __forceinline__ void project(int e, Real& hx, Real& hy) const {
+        if (e == 0) hy = ymin;
+        else if (e == 1) hy = ymax;
+        else if (e == 2) hx = xmin;
+        else hx = xmax;
+        hx = clampr(hx, xmin, xmax);
+        hy = clampr(hy, ymin, ymax);
+    }
+};
+
+// segment_exit (proj/src/sde.cpp:31-65)
+template <typename Real>
+__device__ __forceinline__ void segment_exit(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
+                                          Real& hx, Real& hy, int& edge) {
+    Real best_t = Real(2);
+    int best = 0;
+    auto consider = [&](int e, Real c0, Real c1, Real target) {
+        if (c1 == c0) return;
+        const Real t = (target - c0) / (c1 - c0);
+        if (t >= Real(0) && t <= Real(1) && t < best_t) {
+            best_t = t;
+            best = e;
+        }
+    };
+    if (y1 <= d.ymin) consider(0, y0, y1, d.ymin);
+    if (y1 >= d.ymax) consider(1, y0, y1, d.ymax);
+    if (x1 <= d.xmin) consider(2, x0, x1, d.xmin);
+    if (x1 >= d.xmax) consider(3, x0, x1, d.xmax);
+    if (best_t > Real(1)) {
+        best_t = Real(1);
+        if (y1 <= d.ymin) best = 0;
+        else if (y1 >= d.ymax) best = 1;
+        else if (x1 <= d.xmin) best = 2;
+        else best = 3;
+    }
+    hx = x0 + best_t * (x1 - x0);
+    hy = y0 + best_t * (y1 - y0);
+    d.project(best, hx, hy);
+    edge = best;
+}
+
+// edge_crossing_test (proj/src/sde.cpp:72-109): edges sorted by
+// (min(d0,d1), id); exponent > 40 skips without a draw; else fire if
+// u01 < exp(-ex).  scheme 0: ex = d0 d1 / dt; scheme 1: ex = nu2 min(d0,d1).
+template <typename Real>
+__device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
+                                           int scheme, Real par, LaneStream& rng, Real& hx,
+                                           Real& hy, int& edge) {
+    Real k0 = d.dist(x0, y0, 0), k1 = d.dist(x0, y0, 1), k2 = d.dist(x0, y0, 2),
+         k3 = d.dist(x0, y0, 3);
+    Real m0 = d.dist(x1, y1, 0), m1 = d.dist(x1, y1, 1), m2 = d.dist(x1, y1, 2),
+         m3 = d.dist(x1, y1, 3);
+    // std::min(a, b) = b < a ? b : a
+    Real s0 = m0 < k0 ? m0 : k0, s1 = m1 < k1 ? m1 : k1, s2 = m2 < k2 ? m2 : k2,
+         s3 = m3 < k3 ? m3 : k3;
+    int e0 = 0, e1 = 1, e2 = 2, e3 = 3;
+    auto cswap = [](Real& da, int& ea, Real& db, int& eb) {
+        const bool less = db != da ? db < da : eb < ea;
+        if (less) {
+            const Real t = da; da = db; db = t;
+            const int u = ea; ea = eb; eb = u;
+        }
+    };
+    cswap(s0, e0, s1, e1);
+    cswap(s2, e2, s3, e3);
+    cswap(s0, e0, s2, e2);
+    cswap(s1, e1, s3, e3);
+    cswap(s1, e1, s2, e2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int e = i == 0 ? e0 : (i == 1 ? e1 : (i == 2 ? e2 : e3));
+        const Real d0 = e == 0 ? k0 : (e == 1 ? k1 : (e == 2 ? k2 : k3));
+        const Real d1 = e == 0 ? m0 : (e == 1 ? m1 : (e == 2 ? m2 : m3));
+        const Real ex = scheme == 0 ? d0 * d1 / par : par * (d1 < d0 ? d1 : d0);
+        if (ex > Real(40)) continue;
+        const Real u = RealOps<Real>::u(rng.next_one());
+        if (u < RealOps<Real>::ex(-ex)) {
+            const Real sum = d0 + d1;
+            const Real s = sum > Real(0) ? d0 / sum : Real(0);
+            hx = x0 + s * (x1 - x0);
+            hy = y0 + s * (y1 - y0);
+            d.project(e, hx, hy);
+            edge = e;
+            return true;
+        }
+    }
+    return false;
+}
+
+// table_at / f_at / g_at (proj/src/boundary.cpp:10-42)
+__device__ __forceinline__ double table_at(const double* __restrict__ t, int n, double s) {
+    int k = static_cast<int>(floor(s));
+    k = k < 0 ? 0 : (k > n - 2 ? n - 2 : k);
+    double u = s - k;
+    u = u < 0.0 ? 0.0 : (1.0 < u ? 1.0 : u);
+    return (1.0 - u) * __ldg(t + k) + u * __ldg(t + k + 1);
+}
+
+template <int DV, typename Real>
+__global__ void __launch_bounds__(kWalkBlock) walk_kernel(const WalkArgs a) {
+    using Ops = RealOps<Real>;
+    const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax)};
+    const DensityParams P{a.R, a.alpha, a.fd_h};
+    const Real dt = Real(a.dt);
+    const Real sq2dt = Real(a.sqrt2dt);
+    const Real thr = Real(a.bridge_thr);
+
+    uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint64_t my_steps = 0;
+    if (g < a.total) {
+        // ---- walk setup (also re-entered for every new walk)
+        uint64_t node = g / static_cast<uint64_t>(a.walks);
+        uint32_t walk = static_cast<uint32_t>(a.walk_lo + (g - node * a.walks));
+        uint64_t pid = a.pid[node];
+        uint32_t epoch = 0;
+        Real x = Real(a.px[node]), y = Real(a.py[node]);
+        LaneStream rng;
+        rng.init(a.seed, pid, walk, epoch);
+        int64_t step = 0;
+        for (;;) {
+            // ---- one step
+            Real bx, by, nxp, nyp, z0, z1;
+            bool ok;
+            if (a.scheme == 0) {
+                ok = drift<DV, Real>(P, x, y, bx, by);
+                uint64_t ua, ub;
+                rng.next_pair(ua, ub);
+                Ops::box_muller(ua, ub, z0, z1);
+                nxp = x + bx * dt + sq2dt * z0;
+                nyp = y + by * dt + sq2dt * z1;
+            } else {
+                // step_exponential (sde.cpp:123-140): dt ~ Exp(lambda) first
+                const Real edt = -Ops::lg(Ops::u_open(rng.next_one())) / Real(a.lambda);
+                ok = drift<DV, Real>(P, x, y, bx, by);
+                uint64_t ua, ub;
+                rng.next_pair(ua, ub);
+                Ops::box_muller(ua, ub, z0, z1);
+                const Real s = Ops::sq(Real(2) * edt);
+                nxp = x + bx * edt + s * z0;
+                nyp = y + by * edt + s * z1;
+            }
+            ++step;
+            if (!ok) {
+                atomicCAS(a.err_flag, 0, 3);  // EvaluationError
+                atomicExch(a.err_info, static_cast<unsigned long long>(pid));
+                break;
+            }
+            bool exited = false;
+            Real hx = Real(0), hy = Real(0);
+            int edge = 0;
+            if (!dom.inside(nxp, nyp)) {
+                segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+                exited = true;
+            } else if (a.scheme == 0) {
+                if (a.bridge) {
+                    // pre-filter: an edge can draw only if d0*d1 <= 40 dt
+                    const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
+                    const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
+                    const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
+                    const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
+                    const Real pm = fmin(fmin(pB, pT), fmin(pL, pR));
+                    if (pm <= thr)
+                        exited = edge_crossing(dom, x, y, nxp, nyp, 0, dt, rng, hx, hy, edge);
+                }
+            } else {
+                exited = edge_crossing(dom, x, y, nxp, nyp, 1, Real(a.nu2), rng, hx, hy, edge);
+            }
+            if (!exited) {
+                x = nxp;
+                y = nyp;
+                if (step < a.max_steps) continue;
+                // max_steps reached: restart on the next epoch's stream
+                my_steps += static_cast<uint64_t>(step);
+                ++epoch;
+                if (epoch >= 1024u) {
+                    atomicCAS(a.err_flag, 0, 4);  // NumericalError
+                    atomicExch(a.err_info, static_cast<unsigned long long>(pid));
+                    break;
+                }
+                rng.init(a.seed, pid, walk, epoch);
+                x = Real(a.px[node]);
+                y = Real(a.py[node]);
+                step = 0;
+                continue;
+            }
+            // ---- exit: boundary values, record, next walk
+            const double dhx = static_cast<double>(hx), dhy = static_cast<double>(hy);
+            const bool horiz = edge < 2;
+            const double par = horiz ? (dhx - a.txmin) / a.thx : (dhy - a.tymin) / a.thy;
+            const int tn = horiz ? a.tnx : a.tny;
+            const double fv = table_at(a.tf[edge], tn, par);
+            const double gv = table_at(a.tg[edge], tn, par);
+            my_steps += static_cast<uint64_t>(step);
+            if (a.dump) {
+                sddg_path& r = a.dump[g];
+                r.f = fv;
+                r.g = gv;
+                r.ex = dhx;
+                r.ey = dhy;
+                r.steps = step;
+                r.epoch = static_cast<int32_t>(epoch);
+                r.edge = edge;
+            } else {
+                a.rec_f[g] = fv;
+                a.rec_g[g] = gv;
+                a.rec_meta[g] = static_cast<uint32_t>(edge) | (epoch << 2);
+            }
+            g = atomicAdd(a.next, 1ull);
+            if (g >= a.total) break;
+            node = g / static_cast<uint64_t>(a.walks);
+            walk = static_cast<uint32_t>(a.walk_lo + (g - node * a.walks));
+            pid = a.pid[node];
+            epoch = 0;
+            x = Real(a.px[node]);
+            y = Real(a.py[node]);
+            rng.init(a.seed, pid, walk, epoch);
+            step = 0;
+        }
+    }
+    // path-step count: warp sum, one atomic per warp
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_steps += __shfl_xor_sync(0xffffffffu, my_steps, o);
+    if ((threadIdx.x & 31) == 0 && my_steps) atomicAdd(a.steps, static_cast<unsigned long long>(my_steps));
+}
+
+}  // namespace sddg
