@@ -1,0 +1,60 @@
+// probe.cu -- measured non-tensor peaks of this B200 for the walk kernel's
+// roofline (MEASURED_PEAKS.json only carries HBM and bf16 tensor peaks).
+//   fp64: independent DFMA chains, 2 flops per DFMA
+//   fp32: independent FFMA chains, 2 flops per FFMA
+// Each thread runs 8 independent chains so the pipes, not latency, bind.
+#include "sddg_internal.h"
+
+namespace sddg {
+
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256) fma_probe(T* out, int iters, T a, T b) {
+    T c0 = T(threadIdx.x), c1 = c0 + T(1), c2 = c0 + T(2), c3 = c0 + T(3);
+    T c4 = c0 + T(4), c5 = c0 + T(5), c6 = c0 + T(6), c7 = c0 + T(7);
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            c0 = fma(c0, a, b); c1 = fma(c1, a, b); c2 = fma(c2, a, b); c3 = fma(c3, a, b);
+            c4 = fma(c4, a, b); c5 = fma(c5, a, b); c6 = fma(c6, a, b); c7 = fma(c7, a, b);
+        }
+    }
+    const T s = c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+    if (s == T(-12345)) out[threadIdx.x] = s;  // keep the chains live
+}
+
+}  // namespace
+
+cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops) {
+    void* buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, 1024 * sizeof(double));
+    if (e != cudaSuccess) return e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const int blocks = sms * 8, threads = 256, iters = precision == SDDG_FP64 ? 2048 : 8192;
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a, st);
+        if (precision == SDDG_FP64)
+            fma_probe<double><<<blocks, threads, 0, st>>>(static_cast<double*>(buf), iters, 0.999999, 1e-7);
+        else
+            fma_probe<float><<<blocks, threads, 0, st>>>(static_cast<float*>(buf), iters, 0.9999f, 1e-4f);
+        cudaEventRecord(b, st);
+        e = cudaEventSynchronize(b);
+        if (e != cudaSuccess) break;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        const double flops = 2.0 * 8 * 16 * double(iters) * blocks * threads;
+        if (rep > 0) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    *tflops = best;
+    return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+}  // namespace sddg

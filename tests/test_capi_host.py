@@ -1,0 +1,129 @@
+"""CPU-side checks of the C-ABI library (no compute calls need a GPU here).
+
+* libsddg.so loads and exports every function declared in include/sddg.h;
+* the host-side set-up entry points (boundary tables, layout + placement)
+  reproduce the reference's golden outputs bit for bit;
+* errors map onto the reference's exception classes;
+* without a GPU, creating a context fails loudly (no CPU fallback).
+"""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from cases import plan_from_flat
+from oracle import bindings as B
+from paper_1310_3435_b200 import sdd
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    text = open(os.path.join(ROOT, "include", "sddg.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sddg_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_functions()
+    assert len(names) >= 15
+    lib = sdd.lib()
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", sdd.library_path()], capture_output=True,
+                         text=True).stdout
+    exported = set(re.findall(r" T (sddg_\w+)", out))
+    assert set(names) <= exported
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", sdd.library_path()], capture_output=True,
+                         text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_abi_version():
+    assert sdd.lib().sddg_abi_version() == 1
+    assert b"sm_100a" in sdd.lib().sddg_version()
+
+
+@pytest.mark.parametrize("key,kind,dom", [
+    ("ring_65", sdd.RING_W, (0, 1, 0, 1)), ("shock_129", sdd.SHOCK_W, (0, 1, 0, 1)),
+    ("twobump_33", sdd.TWOBUMP_W, (0, 1, 0, 1)), ("running_29", sdd.RUNNING, (0, 1, 0, 1)),
+    ("five_ring_17", sdd.FIVE_RING, (-1, 1, -1, 1)), ("constant_33", sdd.CONSTANT, (0, 1, 0, 1)),
+    ("huang_sloan_33", sdd.HUANG_SLOAN, (0, 1, 0, 1)), ("mackenzie_33", sdd.MACKENZIE, (0, 1, 0, 1))])
+def test_make_boundary_data_matches_reference(golden, key, kind, dom):
+    n = int(key.rsplit("_", 1)[1])
+    m = {sdd.CONSTANT: sdd.MonitorFunction.constant(), sdd.RUNNING: sdd.MonitorFunction.running_example(),
+         sdd.HUANG_SLOAN: sdd.MonitorFunction.huang_sloan(), sdd.MACKENZIE: sdd.MonitorFunction.mackenzie(),
+         sdd.FIVE_RING: sdd.MonitorFunction.five_ring()}.get(kind) or sdd.MonitorFunction.weight(kind)
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(sdd.RectDomain(*dom), n, n))
+    got = np.concatenate(bd.f.arrays() + bd.g.arrays())
+    assert np.array_equal(got, golden[f"tables_{key}"])
+
+
+def test_identity_boundary_tables():
+    bd = sdd.make_boundary_data(sdd.MonitorFunction.ring(), sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), 65, 65),
+                                mode=sdd.BC_IDENTITY)
+    x = np.arange(65) / 64
+    assert np.allclose(bd.f.bottom, x, atol=1e-15) and np.allclose(bd.g.left, x, atol=1e-15)
+    assert (bd.f.left == 0).all() and (bd.f.right == 1).all()
+
+
+@pytest.mark.parametrize("name,m,n,sx,strategy,k", [
+    ("running29_all", sdd.MonitorFunction.running_example(), 29, 2, "all", 0),
+    ("running29_eq7", sdd.MonitorFunction.running_example(), 29, 2, "equispaced", 7),
+    ("running29_opt", sdd.MonitorFunction.running_example(), 29, 2, "optimal", 0),
+    ("constant29_opt", sdd.MonitorFunction.constant(), 29, 2, "optimal", 0),
+    ("ring65_eq31", sdd.MonitorFunction.ring(), 65, 2, "equispaced", 31),
+    ("twobump513_opt", sdd.MonitorFunction.two_bump(), 513, 4, "optimal", 0),
+    ("five157_opt", sdd.MonitorFunction.five_ring(), 157, 4, "optimal", 0),
+    ("shock129_eq40", sdd.MonitorFunction.shock(), 129, 4, "equispaced", 40)])
+def test_plans_match_reference(golden, name, m, n, sx, strategy, k):
+    spec = sdd.GridSpec(m.domain, n, n)
+    lay = sdd.build_layout(spec, sx, sx)
+    plan = sdd.plan_interface_points(strategy, k, m, lay)
+    want = plan_from_flat(golden[f"plan_{name}"])
+    assert [(ln.vertical, ln.fixed_index) for ln in lay.lines] == [(v, f) for v, f, _ in want]
+    assert plan.stochastic == [nodes for _, _, nodes in want]
+
+
+def test_layout_arithmetic():
+    # proj/tests/test_decomposition.cpp:28-62
+    unit = sdd.RectDomain(0, 1, 0, 1)
+    lay = sdd.build_layout(sdd.GridSpec(unit, 29, 29), 2, 2)
+    assert (lay.block_x, lay.block_y, len(lay.lines)) == (14, 14, 2)
+    assert lay.lines[0].vertical and not lay.lines[1].vertical
+    assert lay.subdomain(1, 0) == (14, 0, 15, 15)
+    lay = sdd.build_layout(sdd.GridSpec(unit, 157, 157), 4, 4)
+    assert lay.subdomain_count() == 16 and lay.block_x == 39 and len(lay.lines) == 6
+    assert sdd.build_layout(sdd.GridSpec(unit, 29, 29), 1, 1).lines == []
+    with pytest.raises(sdd.LayoutError, match="x axis"):
+        sdd.build_layout(sdd.GridSpec(unit, 29, 29), 3, 2)
+    with pytest.raises(sdd.LayoutError, match="y axis"):
+        sdd.build_layout(sdd.GridSpec(unit, 29, 29), 2, 5)
+
+
+def test_validation_errors_on_host_entry_points():
+    m = sdd.MonitorFunction.running_example()
+    lay = sdd.build_layout(sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), 29, 29), 2, 2)
+    with pytest.raises(sdd.ValidationError):
+        sdd.plan_interface_points("equispaced", 0, m, lay)
+    with pytest.raises(sdd.ValidationError):
+        sdd.plan_interface_points("equispaced", 28, m, lay)
+    with pytest.raises(sdd.ValidationError):
+        sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), 2, 5)
+    with pytest.raises(sdd.ValidationError):
+        sdd.RectDomain(1, 0, 0, 1)
+
+
+def test_no_gpu_means_loud_failure():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(sdd.CudaError):
+        sdd.Context(0)

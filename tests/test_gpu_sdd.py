@@ -1,0 +1,126 @@
+"""GPU end-to-end: solve_interfaces and solve_sdd through the C-ABI against
+the reference's golden outputs and the reference test_decomposition.cpp
+properties."""
+import numpy as np
+import pytest
+
+from oracle import bindings as B
+from paper_1310_3435_b200 import sdd
+
+pytestmark = pytest.mark.gpu
+UNIT = sdd.RectDomain(0, 1, 0, 1)
+
+
+def test_solve_interfaces_matches_reference(golden, ctx):
+    m = sdd.MonitorFunction.ring()
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    bd = sdd.make_boundary_data(m, spec)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("equispaced", 5, m, lay)
+    s = sdd.solve_interfaces(plan, m, bd, sdd.WalkConfig(scheme="linear", dt=1e-4, walks=200, seed=1),
+                             lay, ctx=ctx)
+    want = golden["ifc_ring33"]
+    got = [np.concatenate(v) for v in (s.xi, s.eta, s.se_xi, s.se_eta)]
+    for k in range(4):
+        assert np.max(np.abs(got[k] - want[k])) <= 1e-10
+    assert (s.mc_points, s.restarts) == tuple(int(v) for v in golden["ifc_ring33_meta"])
+
+
+def test_solve_sdd_matches_reference(golden, ctx):
+    m = sdd.MonitorFunction.running_example()
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("equispaced", 5, m, lay)
+    r = sdd.solve_sdd(m, lay, plan, sdd.WalkConfig(scheme="exponential", lambda_=1000.0, walks=200, seed=1),
+                      sdd.SolverConfig(tol=1e-12), ctx=ctx)
+    assert np.max(np.abs(r.xi - golden["sdd_running33_xi"])) <= 1e-10
+    assert np.max(np.abs(r.eta - golden["sdd_running33_eta"])) <= 1e-10
+    assert r.subdomain_solves == 8 and r.mc_points > 0 and r.path_steps > 0
+
+
+def test_one_by_one_layout_is_the_single_domain_solve(oracle, ctx):
+    # proj/tests/test_decomposition.cpp:164-179
+    m = sdd.MonitorFunction.running_example()
+    spec = sdd.GridSpec(UNIT, 29, 29)
+    lay = sdd.build_layout(spec, 1, 1)
+    plan = sdd.plan_interface_points("all", 0, m, lay)
+    r = sdd.solve_sdd(m, lay, plan, sdd.WalkConfig(walks=10, seed=1), sdd.SolverConfig(tol=1e-10), ctx=ctx)
+    odom = B.Domain(0, 1, 0, 1)
+    w = oracle.weight_values(B.density(B.RUNNING), odom, 29, 29)
+    t = oracle.make_boundary(B.density(B.RUNNING), odom, 29, 29)
+    u_xi, *_ = oracle.solve_dirichlet(w, 29, 29, 1 / 28, 1 / 28, *t.f, tol=1e-10)
+    u_eta, *_ = oracle.solve_dirichlet(w, 29, 29, 1 / 28, 1 / 28, *t.g, tol=1e-10)
+    assert np.array_equal(r.xi, u_xi) and np.array_equal(r.eta, u_eta)
+    assert r.mc_points == 0
+
+
+def test_uniform_weight_interface_is_xi_equals_x(ctx):
+    # proj/tests/test_decomposition.cpp:119-138
+    m = sdd.MonitorFunction.constant()
+    spec = sdd.GridSpec(UNIT, 17, 17)
+    lay = sdd.build_layout(spec, 2, 2)
+    bd = sdd.make_boundary_data(m, spec)
+    plan = sdd.plan_interface_points("all", 0, m, lay)
+    s = sdd.solve_interfaces(plan, m, bd, sdd.WalkConfig(scheme="exponential", lambda_=2000, walks=2000, seed=1),
+                             lay, ctx=ctx)
+    assert len(s.xi) == 2
+    for pos in range(1, 16):
+        assert abs(s.xi[0][pos] - 0.5) <= 4.0 * s.se_xi[0][pos] + 1e-6
+    assert s.xi[0][0] == bd.f.bottom[8] and s.xi[0][16] == bd.f.top[8]
+    assert s.eta[0][0] == 0.0 and s.eta[0][16] == 1.0
+    assert s.mc_points == 2 * 15 - 1
+
+
+def test_solve_sdd_deterministic(ctx):
+    # proj/tests/test_decomposition.cpp:181-195 (thread counts -> repeated launches)
+    m = sdd.MonitorFunction.running_example()
+    lay = sdd.build_layout(sdd.GridSpec(UNIT, 17, 17), 2, 2)
+    plan = sdd.plan_interface_points("optimal", 0, m, lay)
+    cfg = sdd.WalkConfig(scheme="exponential", lambda_=1000, walks=1500, seed=9)
+    a = sdd.solve_sdd(m, lay, plan, cfg, sdd.SolverConfig(), ctx=ctx)
+    b = sdd.solve_sdd(m, lay, plan, cfg, sdd.SolverConfig(), ctx=ctx)
+    assert np.array_equal(a.xi, b.xi) and np.array_equal(a.eta, b.eta)
+
+
+def test_interface_values_carried_into_subdomain_edges(ctx):
+    # proj/tests/test_decomposition.cpp:197-218: the assembled mesh carries
+    # the interface line values unchanged
+    m = sdd.MonitorFunction.ring()
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("equispaced", 7, m, lay)
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=300, seed=3)
+    r = sdd.solve_sdd(m, lay, plan, cfg, sdd.SolverConfig(tol=1e-12, method="rbsor"), ctx=ctx)
+    s = sdd.solve_interfaces(plan, m, sdd.make_boundary_data(m, spec), cfg, lay, ctx=ctx)
+    X = r.xi.reshape(33, 33)
+    assert np.array_equal(X[:, 16], s.xi[0])   # vertical line i = 16
+    assert np.array_equal(X[16, :], s.xi[1])   # horizontal line j = 16
+
+
+def test_sdd_close_to_single_domain(oracle, ctx):
+    # proj/tests/test_decomposition.cpp:140-162: uniform weight, within 0.02
+    m = sdd.MonitorFunction.constant()
+    spec = sdd.GridSpec(UNIT, 17, 17)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("all", 0, m, lay)
+    r = sdd.solve_sdd(m, lay, plan, sdd.WalkConfig(scheme="exponential", lambda_=2000, walks=2000, seed=1),
+                      sdd.SolverConfig(), ctx=ctx)
+    assert r.subdomain_solves == 8 and r.mc_points == 29
+    odom = B.Domain(0, 1, 0, 1)
+    w = oracle.weight_values(B.density(B.CONSTANT), odom, 17, 17)
+    t = oracle.make_boundary(B.density(B.CONSTANT), odom, 17, 17)
+    u_xi, *_ = oracle.solve_dirichlet(w, 17, 17, 1 / 16, 1 / 16, *t.f)
+    u_eta, *_ = oracle.solve_dirichlet(w, 17, 17, 1 / 16, 1 / 16, *t.g)
+    assert max(np.max(np.abs(r.xi - u_xi)), np.max(np.abs(r.eta - u_eta))) <= 0.02
+
+
+def test_identity_bc_mode(ctx):
+    m = sdd.MonitorFunction.ring(analytic=True)
+    spec = sdd.GridSpec(UNIT, 65, 65)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("equispaced", 31, m, lay)
+    r = sdd.solve_sdd(m, lay, plan, sdd.WalkConfig(scheme="linear", dt=1e-4, walks=500, seed=1),
+                      sdd.SolverConfig(tol=1e-10, method="rbsor"), bc_mode=sdd.BC_IDENTITY, ctx=ctx)
+    X = r.xi.reshape(65, 65)
+    assert np.allclose(X[0, :], np.arange(65) / 64, atol=1e-15)
+    assert (X >= 0).all() and (X <= 1).all()
