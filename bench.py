@@ -1,0 +1,362 @@
+"""Benchmark: SDE walk path-steps/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+unit square, 129x129 global grid split 4x4, every interior node of the six
+interface lines (753 unique Monte Carlo nodes), ring density w with the
+analytic drift grad(w)/w, Euler-Maruyama dt = 2e-5 with the reference's
+Brownian-bridge exit test, fp64.  One bench step = the walk phase of
+solve_interfaces over all 753 nodes at 10^4 paths per node (a tenth of the
+config's 10^5; the seed changes every step), i.e. ~6e10 path-steps.
+
+  value  : path-steps/s, device-resident inputs (sddg_mc_estimate_batch_device),
+           CUDA events on the launching stream, max over ranks, L2 flushed
+           (256 MiB write) before every timed step.
+  e2e    : the same metric through the public host-buffer API
+           (sdd.mc_estimate_batch -> sddg_mc_estimate_batch), pinned host
+           inputs copied in and estimates copied out every step, wall clock.
+  roofline: walk kernel (K1) FP64 pipe: algorithmic DP flops per path-step
+            x path-steps / K1 event time, against the
+           DFMA peak measured on this GPU by sddg_probe_fma_peak.
+  cpu_baseline: the reference's own mc_estimate (oracle/_ref, built from
+           /root/reference/proj/src) on all host threads over a fixed node
+           subsample of the same workload.
+
+--impl reference runs the reference CPU implementation alone (rank 0), each
+step a bounded sample of the workload, and prints the same metric.
+Multi-GPU (torchrun): weak scaling, every rank walks its own 753-node batch
+(seed offset by rank); no collective in the timed region except the timing
+max-reduction after it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GRID, SUBS, DT, WALKS_PER_STEP, CONFIG_WALKS = 129, 4, 2e-5, 10_000, 100_000
+# naive census of FP64 operations per interior path-step (transcendental = 1),
+# SURVEY.md 8(d) / DESIGN.md "Roofline"
+DP_FLOPS_PER_STEP = 57
+CPU_SAMPLE_STRIDE, CPU_SAMPLE_WALKS = 24, 2000  # every 24th node (32 nodes) x 2000 walks
+
+
+def config2_nodes():
+    """Unique interface nodes of the 129^2 4x4 layout in solve_interfaces order
+    (vertical lines first, proj/src/decomposition.cpp:44-51,156-169)."""
+    h = 1.0 / (GRID - 1)
+    seen, px, py, pid = set(), [], [], []
+    block = (GRID - 1) // SUBS
+    lines = [(True, a * block) for a in range(1, SUBS)] + [(False, b * block) for b in range(1, SUBS)]
+    for vertical, fixed in lines:
+        for p in range(1, GRID - 1):
+            i, j = (fixed, p) if vertical else (p, fixed)
+            g = j * GRID + i
+            if g in seen:
+                continue
+            seen.add(g)
+            px.append(0.0 + i * h)
+            py.append(0.0 + j * h)
+            pid.append(g)
+    return np.array(px), np.array(py), np.array(pid, np.uint64)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].lower() == "active"})
+        power = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(power) if power else None}
+
+
+def cpu_reference_sample(ref, B, threads, walks=CPU_SAMPLE_WALKS, seed=1):
+    """The reference's mc_estimate (FD ring drift -- its only route for a
+    user density) over the fixed node subsample; returns (path-steps, seconds)."""
+    px, py, pid = config2_nodes()
+    sel = slice(0, None, CPU_SAMPLE_STRIDE)
+    dom = B.Domain(0, 1, 0, 1)
+    d = B.density(B.RING_W)
+    tabs = ref.make_boundary(d, dom, GRID, GRID)
+    cfg = B.walk_cfg(dt=DT, walks=walks, seed=seed)
+    t0 = time.perf_counter()
+    ref.mc_estimate_batch(d, dom, tabs, cfg, px[sel], py[sel], pid[sel], threads=threads)
+    sec = time.perf_counter() - t0
+    # path-steps of the identical walks (same streams): counted by the C
+    # restatement, which is bit-identical to the reference (tests/test_oracle_pins.py)
+    return sec, (px[sel], py[sel], pid[sel], tabs, cfg)
+
+
+def count_steps(B, sample, threads):
+    px, py, pid, tabs, cfg = sample
+    orc = B.Oracle()
+    e = orc.mc_estimate_batch(B.density(B.RING_W), B.Domain(0, 1, 0, 1), tabs, cfg, px, py, pid,
+                              threads=threads)
+    return int(e["path_steps"].sum())
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import bindings as B
+    try:
+        B.ensure_built()
+        ref = B.Ref()
+    except Exception as exc:  # the reference library could not be loaded
+        print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref: {exc}"}))
+        return 0
+    threads = ref.hardware_threads()
+    walks = CPU_SAMPLE_WALKS // 2
+    times, sample = [], None
+    for k in range(args.warmup + args.steps):
+        # the same bounded sample every step (identical work per step)
+        sec, sample = cpu_reference_sample(ref, B, threads, walks=walks, seed=1)
+        if k >= args.warmup:
+            times.append(sec)
+    # path-steps of those walks, counted once by the bit-identical C restatement
+    steps = [count_steps(B, sample, threads)] * len(times)
+    value = float(sum(steps) / sum(times))
+    n_nodes = len(range(0, 753, CPU_SAMPLE_STRIDE))
+    sample_desc = (f"config-2 walk phase sample: every {CPU_SAMPLE_STRIDE}th of the 753 interface "
+                   f"nodes ({n_nodes} nodes) x {walks} paths, dt={DT}, ring density via the "
+                   f"reference's user_supplied FD drift")
+    print(json.dumps({
+        "impl": "reference", "metric": "SDE walk path-steps/s", "value": value,
+        "unit": "path-steps/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "BASELINE config 2 walk phase (129^2, 4x4, ring, dt=2e-5), bounded sample",
+                   "nodes": n_nodes, "paths_per_node": walks},
+        "cpu_baseline": {"value": value, "unit": "path-steps/s", "cores": threads,
+                         "kind": "reference", "sample": sample_desc},
+        "e2e": {"value": value, "unit": "path-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--drift", default="analytic", choices=["analytic", "reference"])
+    ap.add_argument("--walks", type=int, default=WALKS_PER_STEP)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1310_3435_b200 import sdd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = sdd.Context(local)
+    stream = torch.cuda.current_stream()
+
+    m = sdd.MonitorFunction.ring(analytic=args.drift == "analytic")
+    dom = sdd.RectDomain(0.0, 1.0, 0.0, 1.0)
+    spec = sdd.GridSpec(dom, GRID, GRID)
+    bd = sdd.make_boundary_data(m, spec)
+    px, py, pid = config2_nodes()
+    n = len(px)
+    d_px = torch.tensor(px, dtype=torch.float64, device="cuda")
+    d_py = torch.tensor(py, dtype=torch.float64, device="cuda")
+    d_pid = torch.tensor(pid.astype(np.int64), dtype=torch.int64, device="cuda")
+    d_out = torch.empty(n * sdd.ESTIMATE_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    def cfg_for(step):
+        return sdd.WalkConfig(scheme="linear", dt=DT, walks=args.walks,
+                              seed=1 + step + 1000 * rank, precision=args.precision)
+
+    def one_step(step):
+        sdd.mc_estimate_batch_device(d_px, d_py, d_pid, d_out, m, dom, bd, cfg_for(step), ctx=ctx,
+                                     stream=stream)
+        return ctx.last_stats()
+
+    for k in range(args.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+
+    peak_fp64 = ctx.probe_fma_peak("fp64")
+    peak_fp32 = ctx.probe_fma_peak("fp32")
+
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    total_steps, k1_ms, launches = 0, 0.0, 0
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        st = one_step(args.warmup + k)
+        ev[k][1].record(stream)
+        total_steps += st["path_steps"]
+        k1_ms += st["kernel_ms"]
+        launches += st["launches"]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([elapsed_ms, float(total_steps), k1_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        elapsed_ms, all_steps = float(tmax[0]), float(tsum[1])
+    else:
+        all_steps = float(total_steps)
+    value = all_steps / (elapsed_ms / 1e3)
+
+    # ---- e2e through the public host-buffer API (pinned inputs, D2H result)
+    e2e = None
+    if not args.no_e2e:
+        pts = torch.empty((n, 2), dtype=torch.float64, pin_memory=True)
+        pts[:, 0] = torch.from_numpy(px)
+        pts[:, 1] = torch.from_numpy(py)
+        hpid = torch.from_numpy(pid.astype(np.int64)).pin_memory()
+        sdd.mc_estimate_batch(pts.numpy(), hpid.numpy().view(np.uint64), m, dom, bd, cfg_for(0), ctx=ctx)
+        e_steps, e_sec = 0, 0.0
+        for k in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            sdd.mc_estimate_batch(pts.numpy(), hpid.numpy().view(np.uint64), m, dom, bd,
+                                  cfg_for(args.warmup + k), ctx=ctx)
+            e_sec += time.perf_counter() - t0
+            e_steps += ctx.last_stats()["path_steps"]
+        et = torch.tensor([e_sec, float(e_steps)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            emax = et.clone()
+            dist.all_reduce(emax, op=dist.ReduceOp.MAX)
+            esum = et.clone()
+            dist.all_reduce(esum, op=dist.ReduceOp.SUM)
+            e_sec, e_steps = float(emax[0]), float(esum[1])
+        tables_bytes = 8 * 4 * (GRID + GRID)
+        e2e = {"value": e_steps / e_sec, "unit": "path-steps/s",
+               "h2d_bytes_per_step": int(n * 24 + tables_bytes),
+               "d2h_bytes_per_step": int(n * sdd.ESTIMATE_DTYPE.itemsize),
+               "api": "sdd.mc_estimate_batch -> sddg_mc_estimate_batch (host buffers)"}
+
+    # ---- CPU baseline: the reference on this host, rank 0 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import bindings as B
+            ref = B.Ref()
+            threads = ref.hardware_threads()
+            sec, sample = cpu_reference_sample(ref, B, threads)
+            steps = count_steps(B, sample, threads)
+            cpu = {"value": steps / sec, "unit": "path-steps/s", "cores": threads, "kind": "reference",
+                   "sample": f"every {CPU_SAMPLE_STRIDE}th config-2 node ({len(sample[0])} nodes) x "
+                             f"{CPU_SAMPLE_WALKS} paths, dt={DT}, reference mc_estimate with its "
+                             f"user_supplied FD ring drift; {steps} path-steps in {sec:.2f} s"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "path-steps/s", "cores": None, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        k1_avg_s = k1_ms / 1e3 / args.steps
+        steps_per_launch = total_steps / args.steps
+        achieved = DP_FLOPS_PER_STEP * steps_per_launch / k1_avg_s / 1e12
+        prec_peak = peak_fp64 if args.precision == "fp64" else peak_fp32
+        line = {
+            "metric": "SDE walk path-steps/s", "value": value, "unit": "path-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic",
+            "config": {"workload": "BASELINE config 2 walk phase: 129^2 grid, 4x4 subdomains, all 753 "
+                                   "interface nodes, ring density (analytic grad w / w), linear EM "
+                                   "dt=2e-5 + bridge exit test",
+                       "paths_per_node_per_step": args.walks, "config_paths_per_node": CONFIG_WALKS,
+                       "nodes_per_rank": n, "drift": args.drift, "precision": args.precision,
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": f"weak x{world} (independent node batches per rank)"},
+            "roofline": {"bound": "fp64" if args.precision == "fp64" else "fp32",
+                         "achieved": achieved, "peak": prec_peak, "unit": "TFLOP/s",
+                         "frac": achieved / prec_peak if prec_peak else None, "traffic": None,
+                         "kernel": "walk_kernel (K1)",
+                         "algorithmic_flops_per_path_step": DP_FLOPS_PER_STEP,
+                         "k1_ms_per_launch": k1_avg_s * 1e3,
+                         "path_steps_per_launch": steps_per_launch,
+                         "peak_source": "measured on this GPU by sddg_probe_fma_peak (independent "
+                                        "FMA chains; MEASURED_PEAKS.json has no non-tensor peak)",
+                         "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value * world,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

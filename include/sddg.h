@@ -133,9 +133,15 @@ sddg_status sddg_device_count(int32_t* n);
 sddg_status sddg_create(int32_t device, sddg_ctx** out);
 void sddg_destroy(sddg_ctx* ctx);
 const char* sddg_last_error(const sddg_ctx* ctx);
-/* Path-steps executed and kernels launched by the last compute call. */
+/* Path-steps executed, kernels launched and summed walk-kernel (K1) device
+ * time of the last compute call (solver calls: the solve kernel's time). */
 sddg_status sddg_last_stats(const sddg_ctx* ctx, int64_t* path_steps, int64_t* launches,
                             double* kernel_ms);
+
+/* Measured non-tensor FMA peak of this device in TFLOP/s (independent
+ * DFMA / FFMA chains on every SM), the denominator of the walk kernel's
+ * pipe roofline. */
+sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops);
 
 /* ------------------------------------------------------------- walk seams */
 

@@ -28,6 +28,7 @@ UNITS = {
     "walk_fast.cu": ["-fmad=true"],
     "reduce.cu": ["-fmad=false"],
     "solver.cu": ["-fmad=false"],
+    "probe.cu": [],
     "runtime.cu": [],
 }
 HEADERS = ["density.cuh", "philox.cuh", "walk_kernel.cuh", "sddg_internal.h", "host_density.h"]

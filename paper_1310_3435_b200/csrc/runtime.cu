@@ -86,6 +86,7 @@ struct sddg_ctx {
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
     std::map<int, int> occ;  // (dv*2+prec) -> blocks per SM
+    std::vector<cudaEvent_t> bev;  // per-batch walk-kernel events
 };
 
 namespace {
@@ -275,8 +276,14 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     a.rec_g = rg;
     a.rec_meta = rm;
     int64_t launches = 0;
-    ck(cudaEventRecord(c->ev0, st), "event");
-    for (int64_t b = 0; b < n; b += npb) {
+    const size_t nbatch = static_cast<size_t>((n + npb - 1) / npb);
+    while (c->bev.size() < 2 * nbatch) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "event");
+        c->bev.push_back(e);
+    }
+    size_t bi = 0;
+    for (int64_t b = 0; b < n; b += npb, ++bi) {
         const int64_t nb = std::min(npb, n - b);
         a.px = d_px + b;
         a.py = d_py + b;
@@ -285,17 +292,22 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         const int grid = walk_grid(c, dv, cfg.precision, a.total);
         set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * kWalkBlock);
         ck(cudaGetLastError(), "set_next");
+        ck(cudaEventRecord(c->bev[2 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
+        ck(cudaEventRecord(c->bev[2 * bi + 1], st), "event");
         ck(launch_reduce(rf, rg, rm, W, nb, d_out + b, st), "reduce launch");
         launches += 3;
     }
-    ck(cudaEventRecord(c->ev1, st), "event");
     Counters hc;
     ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "read counters");
     ck(cudaStreamSynchronize(st), "walk kernels");
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
-    c->last_ms = ms;
+    double tot_ms = 0.0;
+    for (size_t k = 0; k < nbatch; ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->bev[2 * k], c->bev[2 * k + 1]);
+        tot_ms += ms;
+    }
+    c->last_ms = tot_ms;
     c->last_steps = static_cast<int64_t>(hc.steps);
     c->last_launches = launches;
     raise_kernel_error(hc);
@@ -770,6 +782,7 @@ void sddg_destroy(sddg_ctx* c) {
                       &c->counters, &c->dump, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err})
         b->release();
+    for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -784,6 +797,13 @@ sddg_status sddg_last_stats(const sddg_ctx* c, int64_t* steps, int64_t* launches
     if (launches) *launches = c->last_launches;
     if (ms) *ms = c->last_ms;
     return SDDG_OK;
+}
+
+sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops) {
+    API_BEGIN(ctx)
+    if (precision != SDDG_FP64 && precision != SDDG_FP32) fail(SDDG_ERR_VALIDATION, "precision");
+    ck(probe_fma_tflops(precision, ctx->sms, ctx->stream, tflops), "probe");
+    API_END(ctx)
 }
 
 sddg_status sddg_mc_estimate_batch(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,

@@ -76,4 +76,6 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
                                cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem);
 
+cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
+
 }  // namespace sddg

@@ -172,6 +172,13 @@ class Context:
         except Exception:
             pass
 
+    def probe_fma_peak(self, precision="fp64"):
+        """Measured non-tensor FMA peak (TFLOP/s) of this device."""
+        t = C.c_double()
+        _check(lib().sddg_probe_fma_peak(self._h, FP64 if precision == "fp64" else FP32, C.byref(t)),
+               self._h)
+        return t.value
+
     def last_stats(self):
         s, n, ms = C.c_int64(), C.c_int64(), C.c_double()
         _check(lib().sddg_last_stats(self._h, C.byref(s), C.byref(n), C.byref(ms)), self._h)
