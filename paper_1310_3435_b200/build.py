@@ -16,8 +16,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
-OBJ_DIR = os.path.join(OUT_DIR, "obj")
-LIB = os.path.join(OUT_DIR, "libsddg.so")
+# SDDG_BUILD_TAG / SDDG_EXTRA_NVCC: side-by-side variant builds for A/B timing
+_TAG = os.environ.get("SDDG_BUILD_TAG", "")
+OBJ_DIR = os.path.join(OUT_DIR, "obj" + (("_" + _TAG) if _TAG else ""))
+LIB = os.path.join(OUT_DIR, "libsddg" + (("_" + _TAG) if _TAG else "") + ".so")
+EXTRA = os.environ.get("SDDG_EXTRA_NVCC", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -44,7 +47,7 @@ def _compile(unit, flags, verbose):
     deps = [src] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "sddg.h")]
     if _mtime(obj) >= max(_mtime(d) for d in deps):
         return obj, False
-    cmd = [NVCC] + ARCH + COMMON + flags + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + COMMON + EXTRA + flags + ["-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

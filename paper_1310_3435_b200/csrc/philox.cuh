@@ -38,18 +38,49 @@ __device__ __forceinline__ uint64_t join64(uint32_t lo, uint32_t hi) {
     return (static_cast<uint64_t>(hi) << 32) | lo;
 }
 
-// Per-lane stream (one walk, one epoch).
+// Philox round keys of a seed: k0 + r*W0, k1 + r*W1 for r = 0..9.  Passed
+// as a kernel parameter so every LOP3 of the rounds reads its key straight
+// from the constant bank (no per-block key schedule in the step loop).
+struct RoundKeys {
+    uint32_t k[20];
+};
+
+__host__ __device__ inline RoundKeys make_round_keys(uint64_t seed) {
+    RoundKeys r;
+    uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+    for (int i = 0; i < 10; ++i) {
+        r.k[2 * i] = k0;
+        r.k[2 * i + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return r;
+}
+
+__device__ __forceinline__ PhiloxWords philox4x32_10(const RoundKeys& rk, uint32_t c0,
+                                                     uint32_t c1, uint32_t c2, uint32_t c3) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+        c0 = hi1 ^ c1 ^ rk.k[2 * r];
+        c1 = lo1;
+        c2 = hi0 ^ c3 ^ rk.k[2 * r + 1];
+        c3 = lo0;
+    }
+    return {c0, c1, c2, c3};
+}
+
+// Per-lane stream (one walk, one epoch); the seed lives in RoundKeys.
 struct LaneStream {
-    uint32_t k0, k1;   // seed
     uint32_t c1;       // walk
     uint32_t c2, c3;   // point id lo, point id hi16 | epoch << 16
     uint32_t n;        // u64s consumed this epoch
     uint32_t cw2, cw3; // words 2,3 of the last generated block
 
-    __device__ __forceinline__ void init(uint64_t seed, uint64_t pid, uint32_t walk,
-                                         uint32_t epoch) {
-        k0 = static_cast<uint32_t>(seed);
-        k1 = static_cast<uint32_t>(seed >> 32);
+    __device__ __forceinline__ void init(uint64_t pid, uint32_t walk, uint32_t epoch) {
         c1 = walk;
         c2 = static_cast<uint32_t>(pid);
         c3 = static_cast<uint32_t>((pid >> 32) & 0xFFFFu) | (epoch << 16);
@@ -59,27 +90,23 @@ struct LaneStream {
 
     // Two consecutive u64s (n, n+1): exactly one new block, index (n+1)>>1,
     // for either parity of n -- the per-step Philox call is warp-uniform.
-    __device__ __forceinline__ void next_pair(uint64_t& a, uint64_t& b) {
-        const PhiloxWords w = philox4x32_10(k0, k1, (n + 1) >> 1, c1, c2, c3);
-        if (n & 1u) {
-            a = join64(cw2, cw3);
-            b = join64(w.w0, w.w1);
-        } else {
-            a = join64(w.w0, w.w1);
-            b = join64(w.w2, w.w3);
-        }
+    __device__ __forceinline__ void next_pair(const RoundKeys& rk, uint64_t& a, uint64_t& b) {
+        const PhiloxWords w = philox4x32_10(rk, (n + 1) >> 1, c1, c2, c3);
+        const bool odd = n & 1u;
+        a = odd ? join64(cw2, cw3) : join64(w.w0, w.w1);
+        b = odd ? join64(w.w0, w.w1) : join64(w.w2, w.w3);
         cw2 = w.w2;
         cw3 = w.w3;
         n += 2;
     }
 
     // One u64 (bridge / exponential draws): a new block only when n is even.
-    __device__ __forceinline__ uint64_t next_one() {
+    __device__ __forceinline__ uint64_t next_one(const RoundKeys& rk) {
         uint64_t v;
         if (n & 1u) {
             v = join64(cw2, cw3);
         } else {
-            const PhiloxWords w = philox4x32_10(k0, k1, n >> 1, c1, c2, c3);
+            const PhiloxWords w = philox4x32_10(rk, n >> 1, c1, c2, c3);
             v = join64(w.w0, w.w1);
             cw2 = w.w2;
             cw3 = w.w3;

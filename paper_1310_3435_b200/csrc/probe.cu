@@ -58,3 +58,53 @@ cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tf
 }
 
 }  // namespace sddg
+
+// ---- accuracy self-test of fastmath.cuh against the CUDA library
+#include "fastmath.cuh"
+
+namespace sddg {
+namespace {
+
+__device__ unsigned long long ulp_diff(double a, double b) {
+    if (a == b) return 0;
+    long long ia = __double_as_longlong(a), ib = __double_as_longlong(b);
+    if (ia < 0) ia = 0x8000000000000000LL - ia;
+    if (ib < 0) ib = 0x8000000000000000LL - ib;
+    return static_cast<unsigned long long>(ia > ib ? ia - ib : ib - ia);
+}
+
+__global__ void fastmath_check(int64_t n, unsigned long long* maxulp) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double t = (static_cast<double>(i) + 0.5) / static_cast<double>(n);  // (0,1)
+    const double xe = -700.0 * t * t;
+    atomicMax(&maxulp[0], ulp_diff(fm::fexp_neg(xe), exp(xe)));
+    const double xe2 = -t * 40.0;
+    atomicMax(&maxulp[0], ulp_diff(fm::fexp_neg(xe2), exp(xe2)));
+    const double xl = exp2(-53.0 * t);
+    atomicMax(&maxulp[1], ulp_diff(fm::flog_unit(xl), log(xl)));
+    atomicMax(&maxulp[1], ulp_diff(fm::flog_unit(t), log(t)));
+    double s, c, s2, c2;
+    fm::fsincos_2pi(t, s, c);
+    sincospi(2.0 * t, &s2, &c2);
+    if (fabs(s2) > 1e-3) atomicMax(&maxulp[2], ulp_diff(s, s2));
+    if (fabs(c2) > 1e-3) atomicMax(&maxulp[2], ulp_diff(c, c2));
+    const double xs = 80.0 * t;
+    atomicMax(&maxulp[3], ulp_diff(fm::fsqrt_pos(xs), sqrt(xs)));
+    atomicMax(&maxulp[4], ulp_diff(fm::frcp(1.0 + xs), 1.0 / (1.0 + xs)));
+}
+
+}  // namespace
+
+cudaError_t fastmath_selftest(int64_t n, unsigned long long* host_maxulp5) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 5 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, 5 * sizeof(unsigned long long));
+    fastmath_check<<<static_cast<unsigned>((n + 255) / 256), 256>>>(n, d);
+    e = cudaMemcpy(host_maxulp5, d, 5 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
+
+}  // namespace sddg

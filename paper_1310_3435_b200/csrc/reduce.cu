@@ -15,7 +15,8 @@ constexpr int kReduceThreads = 256;
 
 __global__ void __launch_bounds__(kReduceThreads)
 reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
-              const uint32_t* __restrict__ meta, int64_t walks, sddg_estimate* out) {
+              const uint32_t* __restrict__ meta, int64_t walks, const uint32_t* __restrict__ perm,
+              sddg_estimate* out) {
     __shared__ double part[4][kReduceThreads];
     __shared__ unsigned long long icnt[5][kReduceThreads / 32];
     const int64_t node = blockIdx.x;
@@ -99,14 +100,16 @@ reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
         e.sum_ff = tff;
         e.sum_gg = tgg;
         e.path_steps = 0;  // filled by the host from the kernel counter
-        out[node] = e;
+        out[perm ? perm[node] : node] = e;
     }
 }
 
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
-                          int64_t walks, int64_t n_nodes, sddg_estimate* out, cudaStream_t s) {
+                          int64_t walks, int64_t n_nodes, const uint32_t* perm, sddg_estimate* out,
+                          cudaStream_t s) {
     if (n_nodes <= 0) return cudaSuccess;
-    reduce_kernel<<<static_cast<unsigned>(n_nodes), kReduceThreads, 0, s>>>(rf, rg, meta, walks, out);
+    reduce_kernel<<<static_cast<unsigned>(n_nodes), kReduceThreads, 0, s>>>(rf, rg, meta, walks, perm,
+                                                                            out);
     return cudaGetLastError();
 }
 

@@ -81,7 +81,7 @@ struct sddg_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::string err;
     std::mutex mu;
-    DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump;
+    DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm;
     DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err;
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
@@ -218,8 +218,33 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     a.lambda = cfg.lambda;
     a.nu2 = 2.0 * std::sqrt(cfg.lambda);  // step_exponential (sde.cpp:135)
     a.bridge_thr = 40.0 * cfg.dt * (1.0 + (cfg.precision == SDDG_FP32 ? 1e-5 : 1e-12));
+    // inner box: both endpoints farther than s >= sqrt(bridge_thr) from every
+    // edge => every d0*d1 > bridge_thr => no bridge draw possible
+    const double sbox = std::sqrt(a.bridge_thr) * (1.0 + 1e-6);
+    a.box[0] = dom.xmin + sbox;
+    a.box[1] = dom.xmax - sbox;
+    a.box[2] = dom.ymin + sbox;
+    a.box[3] = dom.ymax - sbox;
     a.seed = cfg.seed;
-    a.max_steps = cfg.max_steps;
+    a.rk = make_round_keys(cfg.seed);
+    a.max_steps32 = static_cast<uint32_t>(std::min<int64_t>(cfg.max_steps, 0xFFFFFFFFLL));
+}
+
+// Longest-expected-walk-first node order (LPT): a first-exit walk from p
+// takes time ~ the product of its distances to opposite edges, so sort by
+// that descending; the batch tail is then made of short walks.
+std::vector<uint32_t> lpt_order(const sddg_domain& dom, const double* px, const double* py,
+                                int64_t n) {
+    std::vector<uint32_t> perm(n);
+    std::vector<double> key(n);
+    for (int64_t k = 0; k < n; ++k) {
+        perm[k] = static_cast<uint32_t>(k);
+        const double kx = (px[k] - dom.xmin) * (dom.xmax - px[k]);
+        const double ky = (py[k] - dom.ymin) * (dom.ymax - py[k]);
+        key[k] = kx * ky / (kx + ky);
+    }
+    std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return key[a] > key[b]; });
+    return perm;
 }
 
 double* upload_tables(sddg_ctx* c, const sddg_boundary& bd) {
@@ -253,9 +278,13 @@ void raise_kernel_error(const Counters& hc) {
 void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
                    const sddg_boundary& bd, const sddg_walk_config& cfg, const double* d_px,
                    const double* d_py, const uint64_t* d_pid, int64_t n, sddg_estimate* d_out,
-                   cudaStream_t st) {
+                   cudaStream_t st, const double* hpx, const double* hpy) {
     const int dv = drift_variant(d, cfg.precision);
     const double* dtab = upload_tables(c, bd);
+    const std::vector<uint32_t> perm = lpt_order(dom, hpx, hpy, n);
+    uint32_t* dperm = static_cast<uint32_t*>(c->perm.ensure(sizeof(uint32_t) * n));
+    ck(cudaMemcpyAsync(dperm, perm.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st),
+       "h2d perm");
     Counters* cnt = static_cast<Counters*>(c->counters.ensure(sizeof(Counters)));
     ck(cudaMemsetAsync(cnt, 0, sizeof(Counters), st), "memset counters");
     const int64_t W = cfg.walks;
@@ -285,9 +314,10 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     size_t bi = 0;
     for (int64_t b = 0; b < n; b += npb, ++bi) {
         const int64_t nb = std::min(npb, n - b);
-        a.px = d_px + b;
-        a.py = d_py + b;
-        a.pid = d_pid + b;
+        a.px = d_px;
+        a.py = d_py;
+        a.pid = d_pid;
+        a.perm = dperm + b;
         a.total = static_cast<uint64_t>(nb) * W;
         const int grid = walk_grid(c, dv, cfg.precision, a.total);
         set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * kWalkBlock);
@@ -295,7 +325,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         ck(cudaEventRecord(c->bev[2 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
         ck(cudaEventRecord(c->bev[2 * bi + 1], st), "event");
-        ck(launch_reduce(rf, rg, rm, W, nb, d_out + b, st), "reduce launch");
+        ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, d_out, st), "reduce launch");
         launches += 3;
     }
     Counters hc;
@@ -337,7 +367,7 @@ void estimates_host(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     ck(cudaMemcpyAsync(dpy, py, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
     ck(cudaMemcpyAsync(dpid, pid, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
     sddg_estimate* dout = static_cast<sddg_estimate*>(c->est.ensure(sizeof(sddg_estimate) * n));
-    run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream);
+    run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream, px, py);
     ck(cudaMemcpyAsync(out, dout, sizeof(sddg_estimate) * n, cudaMemcpyDeviceToHost, c->stream),
        "d2h");
     ck(cudaStreamSynchronize(c->stream), "d2h sync");
@@ -779,7 +809,7 @@ void sddg_destroy(sddg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
@@ -803,6 +833,14 @@ sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops
     API_BEGIN(ctx)
     if (precision != SDDG_FP64 && precision != SDDG_FP32) fail(SDDG_ERR_VALIDATION, "precision");
     ck(probe_fma_tflops(precision, ctx->sms, ctx->stream, tflops), "probe");
+    API_END(ctx)
+}
+
+sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[5]) {
+    API_BEGIN(ctx)
+    unsigned long long m[5];
+    ck(fastmath_selftest(n, m), "fastmath self-test");
+    for (int k = 0; k < 5; ++k) max_ulp[k] = m[k];
     API_END(ctx)
 }
 
@@ -833,7 +871,8 @@ sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* den
         ck(cudaMemcpyAsync(hy.data(), d_py, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");
         check_points(*dom, hx.data(), hy.data(), n);
-        run_estimates(ctx, *dens, *dom, *bd, *cfg, d_px, d_py, d_pid, n, d_out, st);
+        run_estimates(ctx, *dens, *dom, *bd, *cfg, d_px, d_py, d_pid, n, d_out, st, hx.data(),
+                      hy.data());
     }
     API_END(ctx)
 }

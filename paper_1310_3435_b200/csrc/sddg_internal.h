@@ -6,10 +6,15 @@
 #include <cstdint>
 
 #include "../../include/sddg.h"
+#include "philox.cuh"
 
 namespace sddg {
 
 constexpr int kWalkBlock = 128;   // threads per walk CTA
+#ifndef SDDG_WALK_MIN_BLOCKS
+#define SDDG_WALK_MIN_BLOCKS 6
+#endif
+constexpr int kWalkMinBlocks = SDDG_WALK_MIN_BLOCKS;  // >= 6 CTAs (24 warps) per SM
 constexpr int64_t kChunk = 256;   // reference mc_estimate chunk (proj/src/sde.cpp:201)
 
 struct WalkArgs {
@@ -25,12 +30,15 @@ struct WalkArgs {
     // walk config
     int scheme, bridge;
     double dt, sqrt2dt, lambda, nu2, bridge_thr;
+    double box[4];  // inner box x0, x1, y0, y1 (edge distances > sqrt(bridge_thr))
     uint64_t seed;
-    int64_t max_steps;
+    RoundKeys rk;
+    uint32_t max_steps32;  // min(max_steps, 2^32-1)
     // batch: total = n_nodes * walks
     const double* px;
     const double* py;
     const uint64_t* pid;
+    const uint32_t* perm;  // batch slot -> node (longest expected walks first), or null
     int64_t walks;
     int64_t walk_lo;
     uint64_t total;
@@ -57,7 +65,8 @@ cudaError_t occupancy_walk_fast(int dv, int precision, int* b);
 
 // reduce.cu: K2 fixed chunk-order finalize, one CTA per node
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
-                          int64_t walks, int64_t n_nodes, sddg_estimate* out, cudaStream_t s);
+                          int64_t walks, int64_t n_nodes, const uint32_t* perm, sddg_estimate* out,
+                          cudaStream_t s);
 
 // solver.cu: K3 batched Dirichlet solves
 struct SolveJob {
@@ -77,5 +86,6 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
                                int coef_in_smem);
 
 cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
+cudaError_t fastmath_selftest(int64_t n, unsigned long long* host_maxulp5);
 
 }  // namespace sddg

@@ -4,54 +4,71 @@
 // record and immediately takes the next walk index from a global counter, so
 // the heavy-tailed walk lengths (SURVEY.md 7 "Divergence") never idle a lane
 // until the batch tail.  Walk g of the batch is walk (walk_lo + g % walks) of
-// node g / walks.  Records go to HBM by walk index; K2 (reduce.cu) then sums
-// them in the reference's fixed 256-walk chunk order, so results do not depend
-// on which lane ran which walk.
+// node perm[g / walks]; the host orders nodes longest-expected-walk first so
+// the batch tail is made of short walks.  Records go to HBM by walk index; K2
+// (reduce.cu) sums them in the reference's fixed 256-walk chunk order, so
+// results do not depend on which lane ran which walk.
 //
-// Per step (reference: run_walk, proj/src/sde.cpp:151-183; Appendix A of
-// SURVEY.md): drift -> one Philox block -> Box-Muller -> Euler-Maruyama
+// Per step (reference: run_walk, proj/src/sde.cpp:151-183; SURVEY.md
+// Appendix A): drift -> one Philox block -> Box-Muller -> Euler-Maruyama
 // update -> explicit exit (segment_exit, sde.cpp:31-65) -> bridge test
-// (edge_crossing_test, sde.cpp:72-121).  The bridge test only draws for edges
-// with d0 d1/dt <= 40; a conservative product pre-filter skips the exact
-// sorted test on steps where no edge can qualify (no draw is consumed there
-// in the reference either, sde.cpp:92).
+// (edge_crossing_test, sde.cpp:72-121).  The bridge test draws only for
+// edges with d0 d1/dt <= 40 (sde.cpp:92); a step whose old and new positions
+// both lie in the inner box (every edge distance > sqrt(40 dt)) cannot have
+// such an edge, so the exact sorted test runs only near the boundary.
+//
+// Template parameters: DV drift variant (density.cuh), Real (double/float),
+// SCHEME (0 linear, 1 exponential), BRIDGE (linear bridge test on/off).
 #pragma once
 #include <cstdint>
 
 #include "density.cuh"
+#include "fastmath.cuh"
 #include "philox.cuh"
 #include "sddg_internal.h"
 
 namespace sddg {
 
-template <typename Real>
+// Elementary functions per mode: FAST (analytic fp64) uses fastmath.cuh;
+// the reference-parity mode uses the CUDA library (closest to glibc).
+template <typename Real, bool FAST>
 struct RealOps;
 
-template <>
-struct RealOps<double> {
-    __device__ static __forceinline__ double u_open(uint64_t u) { return u01_open_d(u); }
+template <bool FAST>
+struct RealOps<double, FAST> {
     __device__ static __forceinline__ double u(uint64_t u) { return u01_d(u); }
+    __device__ static __forceinline__ double u_open(uint64_t u) { return u01_open_d(u); }
+    // rng.hpp:66-73: r = sqrt(-2 ln u1), a = 2 pi u2, z = (r cos a, r sin a)
     __device__ static __forceinline__ void box_muller(uint64_t a, uint64_t b, double& z0,
                                                       double& z1) {
-        // rng.hpp:66-73
         const double u1 = u01_open_d(a);
         const double u2 = u01_d(b);
-        const double r = sqrt(-2.0 * log(u1));
-        const double ang = 6.283185307179586476925286766559 * u2;
-        double s, c;
-        sincos(ang, &s, &c);
+        double s, c, r;
+        if constexpr (FAST) {
+            r = fm::fsqrt_pos(-2.0 * fm::flog_unit(u1));
+            fm::fsincos_2pi(u2, s, c);
+        } else {
+            r = sqrt(-2.0 * log(u1));
+            sincos(6.283185307179586476925286766559 * u2, &s, &c);
+        }
         z0 = r * c;
         z1 = r * s;
     }
-    __device__ static __forceinline__ double ex(double v) { return exp(v); }
-    __device__ static __forceinline__ double lg(double v) { return log(v); }
+    __device__ static __forceinline__ double ex(double v) {
+        if constexpr (FAST) return fm::fexp_neg(v);
+        else return exp(v);
+    }
+    __device__ static __forceinline__ double lg(double v) {
+        if constexpr (FAST) return fm::flog_unit(v);
+        else return log(v);
+    }
     __device__ static __forceinline__ double sq(double v) { return sqrt(v); }
 };
 
-template <>
-struct RealOps<float> {
-    __device__ static __forceinline__ float u_open(uint64_t u) { return u01_open_f(u); }
+template <bool FAST>
+struct RealOps<float, FAST> {
     __device__ static __forceinline__ float u(uint64_t u) { return u01_f(u); }
+    __device__ static __forceinline__ float u_open(uint64_t u) { return u01_open_f(u); }
     __device__ static __forceinline__ void box_muller(uint64_t a, uint64_t b, float& z0,
                                                       float& z1) {
         const float u1 = u01_open_f(a);
@@ -70,7 +87,7 @@ struct RealOps<float> {
 template <int DV, typename Real>
 __device__ __forceinline__ bool drift(const DensityParams& P, Real x, Real y, Real& bx, Real& by) {
     if constexpr (DV >= DV_RING_AN) {
-        return drift_an(DV, x, y, bx, by);
+        return drift_an<DV>(x, y, bx, by);
     } else {
         static_assert(sizeof(Real) == 8, "reference drifts are fp64 only");
         return drift_ref<DV>(P, x, y, bx, by);
@@ -85,8 +102,12 @@ __device__ __forceinline__ Real clampr(Real v, Real lo, Real hi) {
 template <typename Real>
 struct Dom {
     Real xmin, xmax, ymin, ymax;
+    Real bx0, bx1, by0, by1;  // inner box: every edge distance > sqrt(40 dt)
     __device__ __forceinline__ bool inside(Real x, Real y) const {
         return x > xmin && x < xmax && y > ymin && y < ymax;  // geometry.hpp:38-40
+    }
+    __device__ __forceinline__ bool in_box(Real x, Real y) const {
+        return x > bx0 && x < bx1 && y > by0 && y < by1;
     }
     // geometry.cpp:24-32
     __device__ __forceinline__ Real dist(Real x, Real y, int e) const {
@@ -104,8 +125,8 @@ struct Dom {
 
 // segment_exit (proj/src/sde.cpp:31-65)
 template <typename Real>
-__device__ __forceinline__ void segment_exit(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
-                                          Real& hx, Real& hy, int& edge) {
+__device__ __forceinline__ void segment_exit(const Dom<Real>& d, Real x0, Real y0, Real x1,
+                                             Real y1, Real& hx, Real& hy, int& edge) {
     Real best_t = Real(2);
     int best = 0;
     auto consider = [&](int e, Real c0, Real c1, Real target) {
@@ -135,15 +156,15 @@ __device__ __forceinline__ void segment_exit(const Dom<Real>& d, Real x0, Real y
 
 // edge_crossing_test (proj/src/sde.cpp:72-109): edges sorted by
 // (min(d0,d1), id); exponent > 40 skips without a draw; else fire if
-// u01 < exp(-ex).  scheme 0: ex = d0 d1 / dt; scheme 1: ex = nu2 min(d0,d1).
-template <typename Real>
-__device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
-                                           int scheme, Real par, LaneStream& rng, Real& hx,
-                                           Real& hy, int& edge) {
-    Real k0 = d.dist(x0, y0, 0), k1 = d.dist(x0, y0, 1), k2 = d.dist(x0, y0, 2),
-         k3 = d.dist(x0, y0, 3);
-    Real m0 = d.dist(x1, y1, 0), m1 = d.dist(x1, y1, 1), m2 = d.dist(x1, y1, 2),
-         m3 = d.dist(x1, y1, 3);
+// u01 < exp(-ex).  SCHEME 0: ex = d0 d1 / dt (bridge_exit_test); 1: nu2 min(d0,d1).
+template <typename Real, bool FAST, int SCHEME>
+__device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real y0, Real x1,
+                                              Real y1, Real par, const RoundKeys& rk,
+                                              LaneStream& rng, Real& hx, Real& hy, int& edge) {
+    const Real k0 = d.dist(x0, y0, 0), k1 = d.dist(x0, y0, 1), k2 = d.dist(x0, y0, 2),
+               k3 = d.dist(x0, y0, 3);
+    const Real m0 = d.dist(x1, y1, 0), m1 = d.dist(x1, y1, 1), m2 = d.dist(x1, y1, 2),
+               m3 = d.dist(x1, y1, 3);
     // std::min(a, b) = b < a ? b : a
     Real s0 = m0 < k0 ? m0 : k0, s1 = m1 < k1 ? m1 : k1, s2 = m2 < k2 ? m2 : k2,
          s3 = m3 < k3 ? m3 : k3;
@@ -165,10 +186,10 @@ __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real 
         const int e = i == 0 ? e0 : (i == 1 ? e1 : (i == 2 ? e2 : e3));
         const Real d0 = e == 0 ? k0 : (e == 1 ? k1 : (e == 2 ? k2 : k3));
         const Real d1 = e == 0 ? m0 : (e == 1 ? m1 : (e == 2 ? m2 : m3));
-        const Real ex = scheme == 0 ? d0 * d1 / par : par * (d1 < d0 ? d1 : d0);
+        const Real ex = SCHEME == 0 ? d0 * d1 / par : par * (d1 < d0 ? d1 : d0);
         if (ex > Real(40)) continue;
-        const Real u = RealOps<Real>::u(rng.next_one());
-        if (u < RealOps<Real>::ex(-ex)) {
+        const Real u = RealOps<Real, FAST>::u(rng.next_one(rk));
+        if (u < RealOps<Real, FAST>::ex(-ex)) {
             const Real sum = d0 + d1;
             const Real s = sum > Real(0) ? d0 / sum : Real(0);
             hx = x0 + s * (x1 - x0);
@@ -190,44 +211,51 @@ __device__ __forceinline__ double table_at(const double* __restrict__ t, int n, 
     return (1.0 - u) * __ldg(t + k) + u * __ldg(t + k + 1);
 }
 
-template <int DV, typename Real>
-__global__ void __launch_bounds__(kWalkBlock) walk_kernel(const WalkArgs a) {
-    using Ops = RealOps<Real>;
-    const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax)};
+template <int DV, typename Real, int SCHEME, bool BRIDGE>
+__global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING_AN) ? 5
+                                                                                   : kWalkMinBlocks)
+    walk_kernel(const __grid_constant__ WalkArgs a) {
+    constexpr bool FAST = DV >= DV_RING_AN;
+    using Ops = RealOps<Real, FAST>;
+    const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax),
+                        Real(a.box[0]), Real(a.box[1]), Real(a.box[2]), Real(a.box[3])};
     const DensityParams P{a.R, a.alpha, a.fd_h};
     const Real dt = Real(a.dt);
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);
+    const uint32_t max_steps = a.max_steps32;
 
     uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     uint64_t my_steps = 0;
     if (g < a.total) {
-        // ---- walk setup (also re-entered for every new walk)
-        uint64_t node = g / static_cast<uint64_t>(a.walks);
-        uint32_t walk = static_cast<uint32_t>(a.walk_lo + (g - node * a.walks));
+        // ---- walk setup (re-entered for every new walk)
+        uint64_t slot = g / static_cast<uint64_t>(a.walks);
+        uint32_t node = a.perm ? a.perm[slot] : static_cast<uint32_t>(slot);
+        uint32_t walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
         uint64_t pid = a.pid[node];
         uint32_t epoch = 0;
         Real x = Real(a.px[node]), y = Real(a.py[node]);
+        bool in_box = dom.in_box(x, y);
         LaneStream rng;
-        rng.init(a.seed, pid, walk, epoch);
-        int64_t step = 0;
+        rng.init(pid, walk, epoch);
+        uint32_t step = 0;
         for (;;) {
             // ---- one step
             Real bx, by, nxp, nyp, z0, z1;
             bool ok;
-            if (a.scheme == 0) {
+            if constexpr (SCHEME == 0) {
                 ok = drift<DV, Real>(P, x, y, bx, by);
                 uint64_t ua, ub;
-                rng.next_pair(ua, ub);
+                rng.next_pair(a.rk, ua, ub);
                 Ops::box_muller(ua, ub, z0, z1);
                 nxp = x + bx * dt + sq2dt * z0;
                 nyp = y + by * dt + sq2dt * z1;
             } else {
                 // step_exponential (sde.cpp:123-140): dt ~ Exp(lambda) first
-                const Real edt = -Ops::lg(Ops::u_open(rng.next_one())) / Real(a.lambda);
+                const Real edt = -Ops::lg(Ops::u_open(rng.next_one(a.rk))) / Real(a.lambda);
                 ok = drift<DV, Real>(P, x, y, bx, by);
                 uint64_t ua, ub;
-                rng.next_pair(ua, ub);
+                rng.next_pair(a.rk, ua, ub);
                 Ops::box_muller(ua, ub, z0, z1);
                 const Real s = Ops::sq(Real(2) * edt);
                 nxp = x + bx * edt + s * z0;
@@ -242,38 +270,45 @@ __global__ void __launch_bounds__(kWalkBlock) walk_kernel(const WalkArgs a) {
             bool exited = false;
             Real hx = Real(0), hy = Real(0);
             int edge = 0;
+            bool nb = true;
             if (!dom.inside(nxp, nyp)) {
                 segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
                 exited = true;
-            } else if (a.scheme == 0) {
-                if (a.bridge) {
-                    // pre-filter: an edge can draw only if d0*d1 <= 40 dt
-                    const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
-                    const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
-                    const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
-                    const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
-                    const Real pm = fmin(fmin(pB, pT), fmin(pL, pR));
-                    if (pm <= thr)
-                        exited = edge_crossing(dom, x, y, nxp, nyp, 0, dt, rng, hx, hy, edge);
+            } else if constexpr (SCHEME == 0) {
+                if constexpr (BRIDGE) {
+                    nb = dom.in_box(nxp, nyp);
+                    if (!(nb && in_box)) {
+                        // exact pre-filter: an edge draws only if d0*d1 <= 40 dt
+                        const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
+                        const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
+                        const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
+                        const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
+                        if (pB <= thr || pT <= thr || pL <= thr || pR <= thr)
+                            exited = edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk,
+                                                                  rng, hx, hy, edge);
+                    }
                 }
             } else {
-                exited = edge_crossing(dom, x, y, nxp, nyp, 1, Real(a.nu2), rng, hx, hy, edge);
+                exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, rng,
+                                                      hx, hy, edge);
             }
             if (!exited) {
                 x = nxp;
                 y = nyp;
-                if (step < a.max_steps) continue;
+                in_box = nb;
+                if (step < max_steps) continue;
                 // max_steps reached: restart on the next epoch's stream
-                my_steps += static_cast<uint64_t>(step);
+                my_steps += step;
                 ++epoch;
                 if (epoch >= 1024u) {
                     atomicCAS(a.err_flag, 0, 4);  // NumericalError
                     atomicExch(a.err_info, static_cast<unsigned long long>(pid));
                     break;
                 }
-                rng.init(a.seed, pid, walk, epoch);
+                rng.init(pid, walk, epoch);
                 x = Real(a.px[node]);
                 y = Real(a.py[node]);
+                in_box = dom.in_box(x, y);
                 step = 0;
                 continue;
             }
@@ -284,7 +319,7 @@ __global__ void __launch_bounds__(kWalkBlock) walk_kernel(const WalkArgs a) {
             const int tn = horiz ? a.tnx : a.tny;
             const double fv = table_at(a.tf[edge], tn, par);
             const double gv = table_at(a.tg[edge], tn, par);
-            my_steps += static_cast<uint64_t>(step);
+            my_steps += step;
             if (a.dump) {
                 sddg_path& r = a.dump[g];
                 r.f = fv;
@@ -301,20 +336,41 @@ __global__ void __launch_bounds__(kWalkBlock) walk_kernel(const WalkArgs a) {
             }
             g = atomicAdd(a.next, 1ull);
             if (g >= a.total) break;
-            node = g / static_cast<uint64_t>(a.walks);
-            walk = static_cast<uint32_t>(a.walk_lo + (g - node * a.walks));
+            slot = g / static_cast<uint64_t>(a.walks);
+            node = a.perm ? a.perm[slot] : static_cast<uint32_t>(slot);
+            walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
             pid = a.pid[node];
             epoch = 0;
             x = Real(a.px[node]);
             y = Real(a.py[node]);
-            rng.init(a.seed, pid, walk, epoch);
+            in_box = dom.in_box(x, y);
+            rng.init(pid, walk, epoch);
             step = 0;
         }
     }
     // path-step count: warp sum, one atomic per warp
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_steps += __shfl_xor_sync(0xffffffffu, my_steps, o);
-    if ((threadIdx.x & 31) == 0 && my_steps) atomicAdd(a.steps, static_cast<unsigned long long>(my_steps));
+    if ((threadIdx.x & 31) == 0 && my_steps)
+        atomicAdd(a.steps, static_cast<unsigned long long>(my_steps));
+}
+
+// All (SCHEME, BRIDGE) instantiations of one drift variant.
+template <int DV, typename Real>
+cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
+    if (a.scheme == SDDG_SCHEME_EXPONENTIAL)
+        walk_kernel<DV, Real, 1, false><<<grid, kWalkBlock, 0, s>>>(a);
+    else if (a.bridge)
+        walk_kernel<DV, Real, 0, true><<<grid, kWalkBlock, 0, s>>>(a);
+    else
+        walk_kernel<DV, Real, 0, false><<<grid, kWalkBlock, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int DV, typename Real>
+cudaError_t occupancy_variant(int* b) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, walk_kernel<DV, Real, 0, true>,
+                                                         kWalkBlock, 0);
 }
 
 }  // namespace sddg

@@ -13,7 +13,7 @@ namespace sddg {
 
 cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s) {
     switch (dv) {
-#define X(V) case V: walk_kernel<V, double><<<grid, kWalkBlock, 0, s>>>(a); return cudaGetLastError();
+#define X(V) case V: return launch_variant<V, double>(a, grid, s);
         SDDG_REF_VARIANTS(X)
 #undef X
     }
@@ -22,7 +22,7 @@ cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s)
 
 cudaError_t occupancy_walk_ref(int dv, int* b) {
     switch (dv) {
-#define X(V) case V: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, walk_kernel<V, double>, kWalkBlock, 0);
+#define X(V) case V: return occupancy_variant<V, double>(b);
         SDDG_REF_VARIANTS(X)
 #undef X
     }

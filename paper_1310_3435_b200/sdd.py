@@ -30,7 +30,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libsddg.so")
+_LIB_PATH = os.environ.get("SDDG_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libsddg.so")
 
 
 # --------------------------------------------------------------- errors

@@ -279,3 +279,12 @@ def test_config3_scale_properties_fp32(ctx):
     # xi increases with x along every horizontal line on average (boundary data 0 -> 1)
     x = np.array([p[0] for p in pts])
     assert np.corrcoef(x, e["xi"])[0, 1] > 0.9
+
+
+def test_fastmath_accuracy(ctx):
+    # performance-mode elementary functions (fastmath.cuh) vs the CUDA library
+    import ctypes as C
+    m = (C.c_uint64 * 5)()
+    sdd._check(sdd.lib().sddg_selftest_fastmath(ctx.handle, C.c_int64(1 << 22), m), ctx.handle)
+    exp_u, log_u, sc_u, sqrt_u, rcp_u = list(m)
+    assert exp_u <= 4 and log_u <= 4 and sc_u <= 4 and sqrt_u <= 2 and rcp_u <= 2, list(m)
