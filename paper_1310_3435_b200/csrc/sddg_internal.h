@@ -12,9 +12,9 @@ namespace sddg {
 
 constexpr int kWalkBlock = 128;   // threads per walk CTA
 #ifndef SDDG_WALK_MIN_BLOCKS
-#define SDDG_WALK_MIN_BLOCKS 6
+#define SDDG_WALK_MIN_BLOCKS 8
 #endif
-constexpr int kWalkMinBlocks = SDDG_WALK_MIN_BLOCKS;  // >= 6 CTAs (24 warps) per SM
+constexpr int kWalkMinBlocks = SDDG_WALK_MIN_BLOCKS;  // >= 8 CTAs (32 warps) per SM: A/B best
 constexpr int64_t kChunk = 256;   // reference mc_estimate chunk (proj/src/sde.cpp:201)
 
 struct WalkArgs {
