@@ -193,6 +193,7 @@ def main():
     ap.add_argument("--walks", type=int, default=WALKS_PER_STEP)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-mesh", action="store_true", help="skip the end-to-end mesh-gen timings")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -300,6 +301,23 @@ def main():
                "d2h_bytes_per_step": int(n * sdd.ESTIMATE_DTYPE.itemsize),
                "api": "sdd.mc_estimate_batch -> sddg_mc_estimate_batch (host buffers)"}
 
+    # ---- end-to-end mesh generation (T_stoc + T_sub, proj/src/cli.cpp:322):
+    # full BASELINE configs 1 and 2 through sdd.solve_sdd, once each
+    mesh = None
+    if rank == 0 and world == 1 and not args.no_mesh:
+        mesh = {}
+        for name, grid, subs_, place, k, walks, dt in (("config1", 65, 2, "equispaced", 31, 10_000, 1e-4),
+                                                       ("config2", 129, 4, "all", 0, 100_000, 2e-5)):
+            lay = sdd.build_layout(sdd.GridSpec(dom, grid, grid), subs_, subs_)
+            plan = sdd.plan_interface_points(place, k, m, lay)
+            wc = sdd.WalkConfig(scheme="linear", dt=dt, walks=walks, seed=1, precision=args.precision)
+            sc = sdd.SolverConfig(tol=1e-10, method="rbsor")
+            r = sdd.solve_sdd(m, lay, plan, wc, sc, ctx=ctx)
+            mesh[name] = {"t_stoc_s": r.t_stoc, "t_sub_s": r.t_sub, "t_total_s": r.t_stoc + r.t_sub,
+                          "mc_points": r.mc_points, "paths_per_node": walks,
+                          "path_steps": r.path_steps, "subdomain_solves": r.subdomain_solves,
+                          "solver": "rbsor tol 1e-10"}
+
     # ---- CPU baseline: the reference on this host, rank 0 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -349,6 +367,7 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "mesh_gen_seconds": mesh,
             "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value * world,
         }
         print(json.dumps(line))

@@ -261,6 +261,33 @@ sddg_status sddg_solve_interfaces(sddg_ctx* ctx, const sddg_density* dens, const
                                   double* eta_lines, double* se_xi_lines, double* se_eta_lines,
                                   sddg_sdd_stats* stats);
 
+/* Sharding seams of solve_interfaces / solve_sdd (multi-GPU: every rank
+ * walks a shard of the nodes, an all-gather of the sddg_estimate records
+ * joins them, every rank fills the lines, ranks solve disjoint subdomain
+ * ranges).
+ * Host: the unique Monte Carlo nodes of the plan in solve_interfaces order
+ * (proj/src/decomposition.cpp:156-169), point_id = j*nx + i. */
+sddg_status sddg_interface_nodes(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
+                                 int32_t ny, int32_t sx, int32_t sy, int32_t placement, int32_t k,
+                                 int64_t capacity, double* px, double* py, uint64_t* point_id,
+                                 int64_t* n);
+/* Host: interface lines from the n estimates of those nodes (in that order):
+ * linear fill and crossing reconciliation (decomposition.cpp:176-246). */
+sddg_status sddg_fill_interfaces(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
+                                 int32_t ny, int32_t sx, int32_t sy, int32_t placement, int32_t k,
+                                 const sddg_boundary* bd, const sddg_estimate* est, int64_t n,
+                                 double* xi_lines, double* eta_lines, double* se_xi_lines,
+                                 double* se_eta_lines);
+/* GPU: the subdomain phase of solve_sdd (decomposition.cpp:292-355) for
+ * subdomains [s_lo, s_hi) (index s = b*sx + a) given the interface lines;
+ * fields receives per subdomain its xi then its eta block ((n+1)^2 each,
+ * index j*nx_sub + i); info one record per (subdomain, field). */
+sddg_status sddg_solve_subdomains(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                  int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t bc_mode,
+                                  const double* xi_lines, const double* eta_lines,
+                                  const sddg_solver_config* scfg, int32_t s_lo, int32_t s_hi,
+                                  double* fields, sddg_solve_info* info);
+
 /* Replaces sdd::solve_sdd (proj/include/sdd/decomposition.hpp:91-94):
  * boundary data, interface walks, subdomain solves, assembly into the global
  * xi, eta (nx*ny, index j*nx+i). */

@@ -614,44 +614,44 @@ struct IfcResult {
     int warnings = 0;
 };
 
-// solve_interfaces (proj/src/decomposition.cpp:147-248), walks on the GPU.
-IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
-                           const std::vector<std::vector<int>>& pl, const sddg_boundary& bd,
-                           const sddg_walk_config& cfg) {
+// Unique Monte Carlo nodes of a plan, in line order (vertical lines first):
+// proj/src/decomposition.cpp:156-169.  point_id = global index j*nx + i.
+struct NodeSet {
     std::map<uint64_t, size_t> index_of;
     std::vector<double> px, py;
     std::vector<uint64_t> gid;
-    auto node_xy = [&](const Line& ln, int pos, double& x, double& y) {
-        const int i = ln.vertical ? ln.fixed : pos, j = ln.vertical ? pos : ln.fixed;
-        x = L.dom.xmin + i * L.hx();
-        y = L.dom.ymin + j * L.hy();
-    };
-    auto node_gid = [&](const Line& ln, int pos) -> uint64_t {
-        const uint64_t i = ln.vertical ? ln.fixed : pos, j = ln.vertical ? pos : ln.fixed;
-        return j * static_cast<uint64_t>(L.nx) + i;
-    };
+};
+
+uint64_t line_node_gid(const Layout& L, const Line& ln, int pos) {
+    const uint64_t i = ln.vertical ? ln.fixed : pos, j = ln.vertical ? pos : ln.fixed;
+    return j * static_cast<uint64_t>(L.nx) + i;
+}
+
+NodeSet interface_nodes(const Layout& L, const std::vector<std::vector<int>>& pl) {
+    NodeSet ns;
     for (size_t l = 0; l < L.lines.size(); ++l)
         for (int pos : pl[l]) {
-            const uint64_t g = node_gid(L.lines[l], pos);
-            if (index_of.emplace(g, px.size()).second) {
-                double x, y;
-                node_xy(L.lines[l], pos, x, y);
-                px.push_back(x);
-                py.push_back(y);
-                gid.push_back(g);
+            const Line& ln = L.lines[l];
+            const uint64_t g = line_node_gid(L, ln, pos);
+            if (ns.index_of.emplace(g, ns.px.size()).second) {
+                const int i = ln.vertical ? ln.fixed : pos, j = ln.vertical ? pos : ln.fixed;
+                ns.px.push_back(L.dom.xmin + i * L.hx());
+                ns.py.push_back(L.dom.ymin + j * L.hy());
+                ns.gid.push_back(g);
             }
         }
+    return ns;
+}
+
+// Linear fill between known nodes and crossing reconciliation
+// (proj/src/decomposition.cpp:176-246) from per-node estimates in NodeSet order.
+IfcResult fill_interfaces(const Layout& L, const NodeSet& ns, const sddg_boundary& bd,
+                          const sddg_estimate* est) {
     IfcResult out;
-    std::vector<sddg_estimate> est(px.size());
-    if (!px.empty()) {
-        estimates_host(c, d, L.dom, bd, cfg, px.data(), py.data(), gid.data(),
-                       static_cast<int64_t>(px.size()), est.data());
-        out.path_steps = c->last_steps;
-    }
-    out.mc_points = static_cast<int64_t>(px.size());
-    for (const auto& e : est) {
-        out.restarts += e.restarts;
-        if (e.warn) ++out.warnings;
+    out.mc_points = static_cast<int64_t>(ns.px.size());
+    for (size_t k = 0; k < ns.px.size(); ++k) {
+        out.restarts += est[k].restarts;
+        if (est[k].warn) ++out.warnings;
     }
     const size_t nl = L.lines.size();
     out.xi.resize(nl);
@@ -669,8 +669,8 @@ IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
         eta[n - 1] = ln.vertical ? bd.g[1][fi] : bd.g[3][fi];
         known[0] = known[n - 1] = 1;
         for (int pos = 1; pos + 1 < n; ++pos) {
-            auto it = index_of.find(node_gid(ln, pos));
-            if (it == index_of.end()) continue;
+            auto it = ns.index_of.find(line_node_gid(L, ln, pos));
+            if (it == ns.index_of.end()) continue;
             const sddg_estimate& e = est[it->second];
             xi[pos] = e.xi;
             eta[pos] = e.eta;
@@ -699,10 +699,93 @@ IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
             if (L.lines[lh].vertical) continue;
             const int iv = L.lines[lv].fixed, jh = L.lines[lh].fixed;
             const uint64_t g = static_cast<uint64_t>(jh) * L.nx + iv;
-            if (index_of.count(g)) continue;
+            if (ns.index_of.count(g)) continue;
             out.xi[lh][iv] = out.xi[lv][jh];
             out.eta[lh][iv] = out.eta[lv][jh];
         }
+    }
+    return out;
+}
+
+// solve_interfaces (proj/src/decomposition.cpp:147-248), walks on the GPU.
+IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
+                           const std::vector<std::vector<int>>& pl, const sddg_boundary& bd,
+                           const sddg_walk_config& cfg) {
+    const NodeSet ns = interface_nodes(L, pl);
+    std::vector<sddg_estimate> est(ns.px.size());
+    int64_t steps = 0;
+    if (!ns.px.empty()) {
+        estimates_host(c, d, L.dom, bd, cfg, ns.px.data(), ns.py.data(), ns.gid.data(),
+                       static_cast<int64_t>(ns.px.size()), est.data());
+        steps = c->last_steps;
+    }
+    IfcResult out = fill_interfaces(L, ns, bd, est.data());
+    out.path_steps = steps;
+    return out;
+}
+
+// Subdomain phase of solve_sdd (proj/src/decomposition.cpp:292-355) for
+// subdomains [s_lo, s_hi): global weights, per-(subdomain, field) edge data
+// from the boundary tables or the interface lines, one batched K3 launch.
+// u receives, per subdomain, the xi field then the eta field (nx*ny each).
+void solve_subdomains(sddg_ctx* c, const sddg_density& d, const Layout& L,
+                      const std::vector<std::vector<double>>& tabs,
+                      const std::vector<std::vector<double>>& ixi,
+                      const std::vector<std::vector<double>>& ieta, const sddg_solver_config& sc,
+                      int s_lo, int s_hi, std::vector<double>& u,
+                      std::vector<sddg_solve_info>& info) {
+    std::map<int, size_t> vline, hline;
+    for (size_t l = 0; l < L.lines.size(); ++l) {
+        if (L.lines[l].vertical) vline[L.lines[l].fixed] = l;
+        else hline[L.lines[l].fixed] = l;
+    }
+    const int nx = L.nx, ny = L.ny;
+    // weight_values on the global grid (detsolver.cpp:219-224)
+    const HostDensity h = host_density(d);
+    std::vector<double> w(static_cast<size_t>(nx) * ny);
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i)
+            w[static_cast<size_t>(j) * nx + i] =
+                1.0 / h.rho(L.dom.xmin + i * L.hx(), L.dom.ymin + j * L.hy());
+    std::vector<sddg_subdomain> subs;
+    std::vector<double> bc;
+    for (int s = s_lo; s < s_hi; ++s) {
+        const int a = s % L.sx, b = s / L.sx;
+        const sddg_subdomain q{a * L.bx, b * L.by, L.bx + 1, L.by + 1};
+        for (int field = 0; field < 2; ++field) {
+            const bool fxi = field == 0;
+            const auto& lines = fxi ? ixi : ieta;
+            for (int e = 0; e < 4; ++e) {
+                const bool horiz = e < 2;
+                const int len = horiz ? q.nx : q.ny, lo = horiz ? q.i0 : q.j0;
+                const std::vector<double>* src;
+                if (e == 0) src = q.j0 == 0 ? &tabs[fxi ? 0 : 4] : &lines[hline.at(q.j0)];
+                else if (e == 1) {
+                    const int j1 = q.j0 + q.ny - 1;
+                    src = j1 == ny - 1 ? &tabs[fxi ? 1 : 5] : &lines[hline.at(j1)];
+                } else if (e == 2) src = q.i0 == 0 ? &tabs[fxi ? 2 : 6] : &lines[vline.at(q.i0)];
+                else {
+                    const int i1 = q.i0 + q.nx - 1;
+                    src = i1 == nx - 1 ? &tabs[fxi ? 3 : 7] : &lines[vline.at(i1)];
+                }
+                bc.insert(bc.end(), src->begin() + lo, src->begin() + lo + len);
+            }
+            subs.push_back(q);
+        }
+    }
+    const int64_t nj = static_cast<int64_t>(subs.size());
+    u.assign(static_cast<size_t>(nj) * (L.bx + 1) * (L.by + 1), 0.0);
+    info.assign(nj, sddg_solve_info{});
+    solve_batch_host(c, w.data(), nx, ny, L.hx(), L.hy(), nj, subs.data(), bc.data(), sc, u.data(),
+                     info.data());
+}
+
+std::vector<std::vector<double>> split_lines(const Layout& L, const double* flat) {
+    std::vector<std::vector<double>> out;
+    size_t off = 0;
+    for (const Line& ln : L.lines) {
+        out.emplace_back(flat + off, flat + off + ln.length);
+        off += ln.length;
     }
     return out;
 }
@@ -1031,49 +1114,15 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
     const double t_stoc = ifc.mc_points > 0 ? now_s() - t0 : 0.0;
     const int64_t steps = ifc.path_steps;
 
-    std::map<int, size_t> vline, hline;
-    for (size_t l = 0; l < L.lines.size(); ++l) {
-        if (L.lines[l].vertical) vline[L.lines[l].fixed] = l;
-        else hline[L.lines[l].fixed] = l;
-    }
     const double ts0 = now_s();
-    // weight_values on the global grid (detsolver.cpp:219-224)
-    const HostDensity h = host_density(*dens);
-    std::vector<double> w(static_cast<size_t>(nx) * ny);
-    for (int j = 0; j < ny; ++j)
-        for (int i = 0; i < nx; ++i)
-            w[static_cast<size_t>(j) * nx + i] = 1.0 / h.rho(dom->xmin + i * L.hx(), dom->ymin + j * L.hy());
     const int n_sub = sx * sy;
+    std::vector<double> u;
+    std::vector<sddg_solve_info> info;
+    solve_subdomains(ctx, *dens, L, tabs, ifc.xi, ifc.eta, *sc, 0, n_sub, u, info);
     std::vector<sddg_subdomain> subs;
-    std::vector<double> bc;
-    for (int s = 0; s < n_sub; ++s) {
-        const int a = s % sx, b = s / sx;
-        const sddg_subdomain q{a * L.bx, b * L.by, L.bx + 1, L.by + 1};
-        for (int field = 0; field < 2; ++field) {
-            const bool fxi = field == 0;
-            auto edge = [&](int e) {
-                const bool horiz = e < 2;
-                const int len = horiz ? q.nx : q.ny, lo = horiz ? q.i0 : q.j0;
-                const std::vector<double>* src;
-                if (e == 0) src = q.j0 == 0 ? &tabs[fxi ? 0 : 4] : (fxi ? &ifc.xi[hline.at(q.j0)] : &ifc.eta[hline.at(q.j0)]);
-                else if (e == 1) {
-                    const int j1 = q.j0 + q.ny - 1;
-                    src = j1 == ny - 1 ? &tabs[fxi ? 1 : 5] : (fxi ? &ifc.xi[hline.at(j1)] : &ifc.eta[hline.at(j1)]);
-                } else if (e == 2) src = q.i0 == 0 ? &tabs[fxi ? 2 : 6] : (fxi ? &ifc.xi[vline.at(q.i0)] : &ifc.eta[vline.at(q.i0)]);
-                else {
-                    const int i1 = q.i0 + q.nx - 1;
-                    src = i1 == nx - 1 ? &tabs[fxi ? 3 : 7] : (fxi ? &ifc.xi[vline.at(i1)] : &ifc.eta[vline.at(i1)]);
-                }
-                bc.insert(bc.end(), src->begin() + lo, src->begin() + lo + len);
-            };
-            for (int e = 0; e < 4; ++e) edge(e);
-            subs.push_back(q);
-        }
-    }
-    std::vector<double> u(static_cast<size_t>(2 * n_sub) * (L.bx + 1) * (L.by + 1));
-    std::vector<sddg_solve_info> info(2 * n_sub);
-    solve_batch_host(ctx, w.data(), nx, ny, L.hx(), L.hy(), 2 * n_sub, subs.data(), bc.data(), *sc,
-                     u.data(), info.data());
+    for (int s = 0; s < n_sub; ++s)
+        for (int f = 0; f < 2; ++f)
+            subs.push_back(sddg_subdomain{(s % sx) * L.bx, (s / sx) * L.by, L.bx + 1, L.by + 1});
     int warns = ifc.warnings;
     size_t off = 0;
     for (int s = 0; s < 2 * n_sub; ++s) {
@@ -1097,6 +1146,74 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         stats->warnings = warns;
         stats->reserved = 0;
     }
+    API_END(ctx)
+}
+
+sddg_status sddg_interface_nodes(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
+                                 int32_t ny, int32_t sx, int32_t sy, int32_t placement, int32_t k,
+                                 int64_t cap, double* px, double* py, uint64_t* pid, int64_t* n) {
+    try {
+        const Layout L = build_layout(*dom, nx, ny, sx, sy);
+        const NodeSet ns = interface_nodes(L, plan(*dens, L, placement, k));
+        *n = static_cast<int64_t>(ns.px.size());
+        if (*n > cap) fail(SDDG_ERR_VALIDATION, "interface_nodes: capacity too small");
+        for (int64_t q = 0; q < *n; ++q) {
+            px[q] = ns.px[q];
+            py[q] = ns.py[q];
+            pid[q] = ns.gid[q];
+        }
+    } catch (const Fail& f) {
+        return finish(nullptr, f);
+    } catch (const std::exception& e) {
+        return finish(nullptr, Fail{SDDG_ERR_EVALUATION, e.what()});
+    }
+    return SDDG_OK;
+}
+
+sddg_status sddg_fill_interfaces(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
+                                 int32_t ny, int32_t sx, int32_t sy, int32_t placement, int32_t k,
+                                 const sddg_boundary* bd, const sddg_estimate* est, int64_t n,
+                                 double* xi, double* eta, double* sxi, double* seta) {
+    try {
+        const Layout L = build_layout(*dom, nx, ny, sx, sy);
+        const NodeSet ns = interface_nodes(L, plan(*dens, L, placement, k));
+        if (static_cast<int64_t>(ns.px.size()) != n)
+            fail(SDDG_ERR_VALIDATION, "fill_interfaces: estimate count does not match the plan");
+        check_boundary(*bd);
+        const IfcResult r = fill_interfaces(L, ns, *bd, est);
+        size_t off = 0;
+        for (size_t l = 0; l < r.xi.size(); ++l) {
+            const size_t m = r.xi[l].size();
+            std::memcpy(xi + off, r.xi[l].data(), sizeof(double) * m);
+            std::memcpy(eta + off, r.eta[l].data(), sizeof(double) * m);
+            if (sxi) std::memcpy(sxi + off, r.sxi[l].data(), sizeof(double) * m);
+            if (seta) std::memcpy(seta + off, r.seta[l].data(), sizeof(double) * m);
+            off += m;
+        }
+    } catch (const Fail& f) {
+        return finish(nullptr, f);
+    } catch (const std::exception& e) {
+        return finish(nullptr, Fail{SDDG_ERR_EVALUATION, e.what()});
+    }
+    return SDDG_OK;
+}
+
+sddg_status sddg_solve_subdomains(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                  int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t bc_mode,
+                                  const double* xi_lines, const double* eta_lines,
+                                  const sddg_solver_config* sc, int32_t s_lo, int32_t s_hi,
+                                  double* fields, sddg_solve_info* info) {
+    API_BEGIN(ctx)
+    const Layout L = build_layout(*dom, nx, ny, sx, sy);
+    if (s_lo < 0 || s_hi > sx * sy || s_lo > s_hi)
+        fail(SDDG_ERR_VALIDATION, "solve_subdomains: subdomain range out of the layout");
+    const auto tabs = boundary_tables(*dens, *dom, nx, ny, bc_mode);
+    const auto ixi = split_lines(L, xi_lines), ieta = split_lines(L, eta_lines);
+    std::vector<double> u;
+    std::vector<sddg_solve_info> inf;
+    solve_subdomains(ctx, *dens, L, tabs, ixi, ieta, *sc, s_lo, s_hi, u, inf);
+    std::memcpy(fields, u.data(), sizeof(double) * u.size());
+    if (info) std::memcpy(info, inf.data(), sizeof(sddg_solve_info) * inf.size());
     API_END(ctx)
 }
 

@@ -633,3 +633,71 @@ def solve_sdd(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan, 
                                 C.byref(st)), ctx.handle)
     return SddResult(xi, eta, st.t_stoc, st.t_sub, st.t_smooth, st.mc_points, st.subdomain_solves,
                      st.restarts, st.path_steps, st.warnings)
+
+
+# --------------------------------------------------------------- sharding seams
+def interface_nodes(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan):
+    """Unique Monte Carlo nodes of the plan in solve_interfaces order
+    (sddg_interface_nodes): (px, py, point_id)."""
+    g = layout.global_
+    cap = max(1, sum(len(p) for p in plan.stochastic))
+    px, py = np.zeros(cap), np.zeros(cap)
+    pid = np.zeros(cap, np.uint64)
+    n = C.c_int64()
+    d, dom = m.c(), g.domain.c()
+    _check(lib().sddg_interface_nodes(C.byref(d), C.byref(dom), g.nx, g.ny, layout.n_sub_x,
+                                      layout.n_sub_y, PLACE.get(plan.strategy, 99), int(plan.k),
+                                      C.c_int64(cap), _dp(px), _dp(py),
+                                      pid.ctypes.data_as(C.c_void_p), C.byref(n)))
+    k = n.value
+    return px[:k].copy(), py[:k].copy(), pid[:k].copy()
+
+
+def fill_interfaces(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan,
+                    bd: BoundaryData, est: np.ndarray) -> InterfaceSolution:
+    """Interface lines from per-node estimates (sddg_fill_interfaces)."""
+    g = layout.global_
+    lens = [ln.length for ln in layout.lines]
+    tot = sum(lens)
+    xi, eta, sx, se = (np.zeros(tot) for _ in range(4))
+    est = np.ascontiguousarray(est, dtype=ESTIMATE_DTYPE)
+    d, dom, b = m.c(), g.domain.c(), bd.c()
+    _check(lib().sddg_fill_interfaces(C.byref(d), C.byref(dom), g.nx, g.ny, layout.n_sub_x,
+                                      layout.n_sub_y, PLACE.get(plan.strategy, 99), int(plan.k),
+                                      C.byref(b), est.ctypes.data_as(C.c_void_p),
+                                      C.c_int64(len(est)), _dp(xi), _dp(eta), _dp(sx), _dp(se)))
+    split = lambda a: [a[o:o + n].copy() for o, n in zip(np.cumsum([0] + lens[:-1]), lens)]
+    return InterfaceSolution(split(xi), split(eta), split(sx), split(se), len(est),
+                             int(est["restarts"].sum()), int(est["warn"].sum()), 0)
+
+
+def solve_subdomains(m: MonitorFunction, layout: SubdomainLayout, xi_lines, eta_lines,
+                     scfg: SolverConfig, s_lo: int, s_hi: int, bc_mode=BC_REFERENCE, ctx=None):
+    """Subdomain phase of solve_sdd for subdomains [s_lo, s_hi)
+    (sddg_solve_subdomains): array (s_hi-s_lo, 2, ny_sub, nx_sub), field 0 = xi."""
+    ctx = ctx or default_context()
+    g = layout.global_
+    bx, by = layout.block_x + 1, layout.block_y + 1
+    ns = s_hi - s_lo
+    fields = np.zeros(max(ns, 0) * 2 * bx * by)
+    info = np.zeros(max(ns, 0) * 2, SOLVE_INFO_DTYPE)
+    xl = _f64(np.concatenate(xi_lines)) if len(xi_lines) else np.zeros(0)
+    el = _f64(np.concatenate(eta_lines)) if len(eta_lines) else np.zeros(0)
+    d, dom, sc = m.c(), g.domain.c(), scfg.c()
+    _check(lib().sddg_solve_subdomains(ctx.handle, C.byref(d), C.byref(dom), g.nx, g.ny,
+                                       layout.n_sub_x, layout.n_sub_y, int(bc_mode), _dp(xl), _dp(el),
+                                       C.byref(sc), int(s_lo), int(s_hi), _dp(fields),
+                                       info.ctypes.data_as(C.c_void_p)), ctx.handle)
+    return fields.reshape(ns, 2, by, bx), info
+
+
+def assemble(layout: SubdomainLayout, fields: np.ndarray):
+    """Global xi, eta from all subdomain blocks (solve_sdd assembly,
+    proj/src/decomposition.cpp:357-377)."""
+    g = layout.global_
+    xi, eta = np.zeros((g.ny, g.nx)), np.zeros((g.ny, g.nx))
+    for s in range(layout.subdomain_count()):
+        i0, j0, nx, ny = layout.subdomain(s % layout.n_sub_x, s // layout.n_sub_x)
+        xi[j0:j0 + ny, i0:i0 + nx] = fields[s, 0]
+        eta[j0:j0 + ny, i0:i0 + nx] = fields[s, 1]
+    return xi.ravel(), eta.ravel()

@@ -124,3 +124,29 @@ def test_identity_bc_mode(ctx):
     X = r.xi.reshape(65, 65)
     assert np.allclose(X[0, :], np.arange(65) / 64, atol=1e-15)
     assert (X >= 0).all() and (X <= 1).all()
+
+
+def test_distributed_solve_sdd_world1_matches_solve_sdd(ctx):
+    # the sharded driver (paper_1310_3435_b200.parallel) over NCCL at world
+    # size 1 reproduces solve_sdd bit for bit
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1310_3435_b200 import parallel
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, init_method=f"tcp://127.0.0.1:{port}")
+    try:
+        m = sdd.MonitorFunction.ring(analytic=True)
+        lay = sdd.build_layout(sdd.GridSpec(UNIT, 65, 65), 4, 4)
+        plan = sdd.plan_interface_points("all", 0, m, lay)
+        wcfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=400, seed=3)
+        scfg = sdd.SolverConfig(tol=1e-11, method="rbsor")
+        xi, eta, ifc, est = parallel.solve_sdd_distributed(m, lay, plan, wcfg, scfg, ctx=ctx)
+        r = sdd.solve_sdd(m, lay, plan, wcfg, scfg, ctx=ctx)
+        assert np.array_equal(xi, r.xi) and np.array_equal(eta, r.eta)
+        assert len(est) == r.mc_points
+    finally:
+        dist.destroy_process_group()
