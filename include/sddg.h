@@ -34,7 +34,9 @@ typedef enum {
     SDDG_ERR_NUMERICAL = 4,     /* sdd::NumericalError   */
     SDDG_ERR_LAYOUT = 5,        /* sdd::LayoutError      */
     SDDG_ERR_CUDA = 6,          /* no B200 / CUDA failure (no fallback) */
-    SDDG_ERR_INTERNAL = 7
+    SDDG_ERR_INTERNAL = 7,
+    SDDG_ERR_INVERSION = 8,     /* sdd::InversionError   */
+    SDDG_ERR_TANGLING = 9       /* sdd::TanglingError    */
 } sddg_status;
 
 /* Density descriptor.  A GPU cannot call the reference's std::function
@@ -296,6 +298,30 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
                            int32_t k, int32_t bc_mode, const sddg_walk_config* cfg,
                            const sddg_solver_config* scfg, double* xi, double* eta,
                            sddg_sdd_stats* stats);
+
+/* ------------------------------------------------- post-processing seams */
+
+/* Replaces sdd::invert_mesh (proj/include/sdd/invert.hpp:14): the physical
+ * mesh x, y (m_xi*m_eta, index b*m_xi + a) of the uniform computational grid
+ * from the solution xi, eta on the nx x ny grid over dom.  Bit-identical to
+ * the reference (same walk/scan point location, same rounding sequence). */
+sddg_status sddg_invert_mesh(sddg_ctx* ctx, const double* xi, const double* eta, int32_t nx,
+                             int32_t ny, const sddg_domain* dom, int32_t m_xi, int32_t m_eta,
+                             double* x, double* y);
+
+/* sdd::QualityReport (proj/include/sdd/quality.hpp:10-14). */
+typedef struct {
+    double q_max, q_mean;
+    double r_max, r_mean; /* valid when has_reference */
+    double l_inf;         /* valid when has_l_inf */
+    int32_t has_reference, has_l_inf;
+} sddg_quality;
+
+/* Replaces sdd::quality_report (proj/src/quality.cpp:35-80); ref_x/ref_y
+ * (reference mesh) and dens (for l_inf) may be NULL. */
+sddg_status sddg_quality_report(sddg_ctx* ctx, const double* x, const double* y, int32_t m_xi,
+                                int32_t m_eta, const double* ref_x, const double* ref_y,
+                                const sddg_density* dens, sddg_quality* out);
 
 #ifdef __cplusplus
 }

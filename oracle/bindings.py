@@ -255,6 +255,30 @@ class Ref(_Lib):
             off += lens[l]
         return out, mc.value, rs.value
 
+    def invert_mesh(self, xi, eta, nx, ny, dom, m_xi, m_eta, threads=1):
+        xi, eta = _f64(xi), _f64(eta)
+        x, y = np.zeros(m_xi * m_eta), np.zeros(m_xi * m_eta)
+        self._check(self.L.ref_invert_mesh(_dp(xi), _dp(eta), nx, ny, C.byref(dom), m_xi, m_eta,
+                                           threads, _dp(x), _dp(y)))
+        return x, y
+
+    def quality(self, x, y, m_xi, m_eta, dom, ref_x=None, ref_y=None, dens=None):
+        x, y = _f64(x), _f64(y)
+        out = np.zeros(5)
+        rx = _dp(_f64(ref_x)) if ref_x is not None else None
+        ry = _dp(_f64(ref_y)) if ref_y is not None else None
+        keep = (ref_x, ref_y)
+        self._check(self.L.ref_quality(_dp(x), _dp(y), m_xi, m_eta, C.byref(dom), rx, ry,
+                                       C.byref(dens) if dens is not None else None, _dp(out)))
+        del keep
+        return out
+
+    def solve_single_domain(self, dens, dom, nx, ny, tol=1e-8):
+        xi, eta = np.zeros(nx * ny), np.zeros(nx * ny)
+        self._check(self.L.ref_solve_single_domain(C.byref(dens), C.byref(dom), nx, ny,
+                                                   C.c_double(tol), _dp(xi), _dp(eta)))
+        return xi, eta
+
     def solve_sdd(self, dens, dom, nx, ny, sx, sy, strategy, k, cfg, tol=1e-8, max_iters=0,
                   threads=0):
         xi, eta, t = np.zeros(nx * ny), np.zeros(nx * ny), np.zeros(3)

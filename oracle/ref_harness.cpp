@@ -16,11 +16,14 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <optional>
 #include <string>
 #include <vector>
 
 #include "sdd/boundary.hpp"
 #include "sdd/decomposition.hpp"
+#include "sdd/invert.hpp"
+#include "sdd/quality.hpp"
 #include "sdd/detsolver.hpp"
 #include "sdd/monitor.hpp"
 #include "sdd/parallel.hpp"
@@ -375,6 +378,59 @@ int ref_solve_sdd(const Density* d, const Domain* dom, int nx, int ny, int sx, i
     times_out[0] = r.t_stoc;
     times_out[1] = r.t_sub;
     times_out[2] = r.t_smooth;
+    GUARD_END
+}
+
+// invert_mesh (proj/src/invert.cpp:140-196) of a solution on the nx x ny grid over dom.
+int ref_invert_mesh(const double* xi, const double* eta, int nx, int ny, const Domain* dom,
+                    int m_xi, int m_eta, int threads, double* x_out, double* y_out) {
+    GUARD_BEGIN
+    const GridSpec g(RectDomain(dom->xmin, dom->xmax, dom->ymin, dom->ymax), nx, ny);
+    const MeshSolution sol(ScalarField(g, std::vector<double>(xi, xi + g.size())),
+                           ScalarField(g, std::vector<double>(eta, eta + g.size())));
+    const PhysicalMesh mesh = invert_mesh(sol, m_xi, m_eta, threads);
+    std::memcpy(x_out, mesh.x.data(), sizeof(double) * mesh.x.size());
+    std::memcpy(y_out, mesh.y.data(), sizeof(double) * mesh.y.size());
+    GUARD_END
+}
+
+// quality_report (proj/src/quality.cpp:35-80); ref_x/ref_y and d may be null.
+// out = {q_max, q_mean, r_max, r_mean, l_inf}
+int ref_quality(const double* x, const double* y, int m_xi, int m_eta, const Domain* dom,
+                const double* ref_x, const double* ref_y, const Density* d, double* out) {
+    GUARD_BEGIN
+    const RectDomain rd(dom->xmin, dom->xmax, dom->ymin, dom->ymax);
+    PhysicalMesh mesh(m_xi, m_eta, rd);
+    const std::size_t n = static_cast<std::size_t>(m_xi) * m_eta;
+    mesh.x.assign(x, x + n);
+    mesh.y.assign(y, y + n);
+    PhysicalMesh ref(m_xi, m_eta, rd);
+    if (ref_x) {
+        ref.x.assign(ref_x, ref_x + n);
+        ref.y.assign(ref_y, ref_y + n);
+    }
+    std::optional<MonitorFunction> m;
+    if (d) m.emplace(make_monitor(*d, *dom));
+    const QualityReport q = quality_report(mesh, ref_x ? &ref : nullptr, m ? &*m : nullptr);
+    out[0] = q.q_max;
+    out[1] = q.q_mean;
+    out[2] = q.r_max.value_or(0.0);
+    out[3] = q.r_mean.value_or(0.0);
+    out[4] = q.l_inf.value_or(0.0);
+    GUARD_END
+}
+
+// solve_single_domain (proj/src/detsolver.cpp:226-246)
+int ref_solve_single_domain(const Density* d, const Domain* dom, int nx, int ny, double tol,
+                            double* xi, double* eta) {
+    GUARD_BEGIN
+    const MonitorFunction m = make_monitor(*d, *dom);
+    SolverConfig sc;
+    sc.tol = tol;
+    const MeshSolveResult r = solve_single_domain(
+        m, GridSpec(RectDomain(dom->xmin, dom->xmax, dom->ymin, dom->ymax), nx, ny), sc);
+    std::memcpy(xi, r.sol.xi.values.data(), sizeof(double) * r.sol.xi.values.size());
+    std::memcpy(eta, r.sol.eta.values.data(), sizeof(double) * r.sol.eta.values.size());
     GUARD_END
 }
 

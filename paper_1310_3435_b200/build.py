@@ -31,6 +31,7 @@ UNITS = {
     "walk_fast.cu": ["-fmad=true"],
     "reduce.cu": ["-fmad=false"],
     "solver.cu": ["-fmad=false"],
+    "mesh.cu": ["-fmad=false"],
     "probe.cu": [],
     "runtime.cu": [],
 }

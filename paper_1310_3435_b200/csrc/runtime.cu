@@ -83,6 +83,7 @@ struct sddg_ctx {
     std::mutex mu;
     DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm;
     DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err;
+    DevBuf m_in, m_out, m_q, m_misc;
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
     std::map<int, int> occ;  // (dv*2+prec) -> blocks per SM
@@ -893,7 +894,7 @@ void sddg_destroy(sddg_ctx* c) {
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
                       &c->counters, &c->dump, &c->perm, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
-                      &c->s_coef, &c->s_err})
+                      &c->s_coef, &c->s_err, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1214,6 +1215,110 @@ sddg_status sddg_solve_subdomains(sddg_ctx* ctx, const sddg_density* dens, const
     solve_subdomains(ctx, *dens, L, tabs, ixi, ieta, *sc, s_lo, s_hi, u, inf);
     std::memcpy(fields, u.data(), sizeof(double) * u.size());
     if (info) std::memcpy(info, inf.data(), sizeof(sddg_solve_info) * inf.size());
+    API_END(ctx)
+}
+
+sddg_status sddg_invert_mesh(sddg_ctx* ctx, const double* xi, const double* eta, int32_t nx,
+                             int32_t ny, const sddg_domain* dom, int32_t m_xi, int32_t m_eta,
+                             double* x, double* y) {
+    API_BEGIN(ctx)
+    // invert_mesh (proj/src/invert.cpp:140-150)
+    if (m_xi < 2 || m_eta < 2)
+        fail(SDDG_ERR_VALIDATION, "invert_mesh: needs at least 2 target nodes per axis");
+    check_domain(*dom);
+    if (nx < 3 || ny < 3) fail(SDDG_ERR_VALIDATION, "GridSpec: needs nx >= 3 and ny >= 3");
+    const size_t N = static_cast<size_t>(nx) * ny, M = static_cast<size_t>(m_xi) * m_eta;
+    for (size_t k = 0; k < N; ++k)
+        if (!std::isfinite(xi[k]) || !std::isfinite(eta[k]))
+            fail(SDDG_ERR_EVALUATION, "ScalarField: non-finite value");
+    cudaStream_t st = ctx->stream;
+    double* din = static_cast<double*>(ctx->m_in.ensure(2 * N * sizeof(double)));
+    double* dout = static_cast<double*>(ctx->m_out.ensure(2 * M * sizeof(double)));
+    int* derr = static_cast<int*>(ctx->m_misc.ensure(64));
+    ck(cudaMemcpyAsync(din, xi, N * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    ck(cudaMemcpyAsync(din + N, eta, N * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    ck(cudaMemsetAsync(derr, 0, 2 * sizeof(int), st), "memset");
+    const double ghx = (dom->xmax - dom->xmin) / (nx - 1), ghy = (dom->ymax - dom->ymin) / (ny - 1);
+    ck(cudaEventRecord(ctx->ev0, st), "event");
+    ck(launch_invert(din, din + N, nx, ny, dom->xmin, dom->ymin, ghx, ghy, m_xi, m_eta, dout,
+                     dout + M, derr, derr + 1, st),
+       "invert launch");
+    ck(cudaEventRecord(ctx->ev1, st), "event");
+    int herr[2] = {0, 0};
+    ck(cudaMemcpyAsync(herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(x, dout, M * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(y, dout + M, M * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "invert");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+    ctx->last_ms = ms;
+    ctx->last_launches = 1;
+    ctx->last_steps = 0;
+    if (herr[0] == 8)
+        fail(SDDG_ERR_INVERSION, "invert_mesh: a target in row " + std::to_string(herr[1]) +
+                                     " is not covered by the forward tessellation");
+    API_END(ctx)
+}
+
+sddg_status sddg_quality_report(sddg_ctx* ctx, const double* x, const double* y, int32_t m_xi,
+                                int32_t m_eta, const double* ref_x, const double* ref_y,
+                                const sddg_density* dens, sddg_quality* out) {
+    API_BEGIN(ctx)
+    if (m_xi < 2 || m_eta < 2) fail(SDDG_ERR_VALIDATION, "PhysicalMesh: needs at least 2 nodes per axis");
+    if ((ref_x == nullptr) != (ref_y == nullptr))
+        fail(SDDG_ERR_VALIDATION, "quality_report: reference mesh needs both x and y");
+    const size_t M = static_cast<size_t>(m_xi) * m_eta;
+    const long long cells = static_cast<long long>(m_xi - 1) * (m_eta - 1);
+    cudaStream_t st = ctx->stream;
+    double* dm = static_cast<double*>(ctx->m_in.ensure(4 * M * sizeof(double)));
+    double* dq = static_cast<double*>(ctx->m_q.ensure(cells * sizeof(double)));
+    char* misc = static_cast<char*>(ctx->m_misc.ensure(256));
+    int* derr = reinterpret_cast<int*>(misc);
+    double* dres = reinterpret_cast<double*>(misc + 64);
+    unsigned long long* dl = reinterpret_cast<unsigned long long*>(misc + 128);
+    ck(cudaMemcpyAsync(dm, x, M * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    ck(cudaMemcpyAsync(dm + M, y, M * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    if (ref_x) {
+        ck(cudaMemcpyAsync(dm + 2 * M, ref_x, M * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+        ck(cudaMemcpyAsync(dm + 3 * M, ref_y, M * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    }
+    ck(cudaMemsetAsync(misc, 0, 256, st), "memset");
+    ck(launch_quality(dm, dm + M, m_xi, m_eta, dq, dres, derr, st), "quality launch");
+    int launches = 2;
+    if (ref_x) {
+        ck(launch_quality(dm + 2 * M, dm + 3 * M, m_xi, m_eta, dq, dres + 2, derr, st), "quality launch");
+        launches += 2;
+        if (dens) {
+            drift_variant(*dens, SDDG_FP64);  // validates the kind
+            ck(launch_linf(dm, dm + M, dm + 2 * M, dm + 3 * M, static_cast<long long>(M), dens->kind,
+                           dens->R, dens->alpha, dl, st),
+               "linf launch");
+            launches += 1;
+        }
+    }
+    int herr = 0;
+    double res[4] = {0, 0, 0, 0};
+    unsigned long long lbits = 0;
+    ck(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(res, dres, sizeof(res), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(&lbits, dl, sizeof(lbits), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "quality");
+    ctx->last_launches = launches;
+    if (herr == 9) fail(SDDG_ERR_TANGLING, "cell_quality: a cell is folded or degenerate (det J <= 0)");
+    std::memset(out, 0, sizeof(*out));
+    out->q_max = res[0];
+    out->q_mean = res[1];
+    if (ref_x) {
+        out->has_reference = 1;
+        out->r_max = res[2] / res[0];   // quality.cpp:64-65
+        out->r_mean = res[3] / res[1];
+        if (dens) {
+            out->has_l_inf = 1;
+            double l;
+            std::memcpy(&l, &lbits, sizeof(l));
+            out->l_inf = l;
+        }
+    }
     API_END(ctx)
 }
 

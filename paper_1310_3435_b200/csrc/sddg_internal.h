@@ -85,6 +85,16 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
                                cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem);
 
+// mesh.cu: K4 inversion, K5 quality
+cudaError_t launch_invert(const double* xi, const double* eta, int nx, int ny, double gx0,
+                          double gy0, double ghx, double ghy, int m_xi, int m_eta, double* X,
+                          double* Y, int* err, int* err_row, cudaStream_t s);
+cudaError_t launch_quality(const double* X, const double* Y, int m_xi, int m_eta, double* qbuf,
+                           double* out2, int* err, cudaStream_t s);
+cudaError_t launch_linf(const double* X, const double* Y, const double* RX, const double* RY,
+                        long long n, int kind, double R, double al, unsigned long long* out_bits,
+                        cudaStream_t s);
+
 cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
 cudaError_t fastmath_selftest(int64_t n, unsigned long long* host_maxulp5);
 

@@ -45,10 +45,12 @@ class EvaluationError(Error): ...
 class NumericalError(Error): ...
 class LayoutError(Error): ...
 class CudaError(Error): ...
+class InversionError(Error): ...
+class TanglingError(Error): ...
 
 
 _ERR = {1: ValidationError, 2: OutOfDomainError, 3: EvaluationError, 4: NumericalError,
-        5: LayoutError, 6: CudaError, 7: Error}
+        5: LayoutError, 6: CudaError, 7: Error, 8: InversionError, 9: TanglingError}
 
 # --------------------------------------------------------------- C structs
 CONSTANT, RUNNING, HUANG_SLOAN, MACKENZIE, FIVE_RING = 0, 1, 2, 3, 4
@@ -701,3 +703,62 @@ def assemble(layout: SubdomainLayout, fields: np.ndarray):
         xi[j0:j0 + ny, i0:i0 + nx] = fields[s, 0]
         eta[j0:j0 + ny, i0:i0 + nx] = fields[s, 1]
     return xi.ravel(), eta.ravel()
+
+
+# --------------------------------------------------------------- post-processing
+class _Quality(C.Structure):
+    _fields_ = [("q_max", C.c_double), ("q_mean", C.c_double), ("r_max", C.c_double),
+                ("r_mean", C.c_double), ("l_inf", C.c_double), ("has_reference", C.c_int32),
+                ("has_l_inf", C.c_int32)]
+
+
+@dataclass
+class PhysicalMesh:
+    """sdd::PhysicalMesh (field.hpp:36-51): x, y indexed b*m_xi + a."""
+    m_xi: int
+    m_eta: int
+    domain: RectDomain
+    x: np.ndarray
+    y: np.ndarray
+
+
+@dataclass
+class QualityReport:
+    """sdd::QualityReport (quality.hpp:10-14)."""
+    q_max: float
+    q_mean: float
+    r_max: float | None = None
+    r_mean: float | None = None
+    l_inf: float | None = None
+
+
+def invert_mesh(xi, eta, spec: GridSpec, m_xi: int, m_eta: int, ctx=None) -> PhysicalMesh:
+    """sdd::invert_mesh (proj/include/sdd/invert.hpp:14) on the GPU."""
+    ctx = ctx or default_context()
+    xi, eta = _f64(xi), _f64(eta)
+    if xi.size != spec.nx * spec.ny or eta.size != spec.nx * spec.ny:
+        raise ValidationError("invert_mesh: field size does not match the grid")
+    x, y = np.zeros(m_xi * m_eta), np.zeros(m_xi * m_eta)
+    dom = spec.domain.c()
+    _check(lib().sddg_invert_mesh(ctx.handle, _dp(xi), _dp(eta), spec.nx, spec.ny, C.byref(dom),
+                                  int(m_xi), int(m_eta), _dp(x), _dp(y)), ctx.handle)
+    return PhysicalMesh(m_xi, m_eta, spec.domain, x, y)
+
+
+def quality_report(mesh: PhysicalMesh, reference: PhysicalMesh | None = None,
+                   m: MonitorFunction | None = None, ctx=None) -> QualityReport:
+    """sdd::quality_report (proj/src/quality.cpp:35-80) on the GPU."""
+    ctx = ctx or default_context()
+    if reference is not None and (reference.m_xi, reference.m_eta) != (mesh.m_xi, mesh.m_eta):
+        raise ValidationError("quality_report: meshes have different node counts")
+    q = _Quality()
+    x, y = _f64(mesh.x), _f64(mesh.y)
+    rx = _f64(reference.x) if reference is not None else None
+    ry = _f64(reference.y) if reference is not None else None
+    d = m.c() if (m is not None and reference is not None) else None
+    _check(lib().sddg_quality_report(ctx.handle, _dp(x), _dp(y), mesh.m_xi, mesh.m_eta,
+                                     _dp(rx) if rx is not None else None,
+                                     _dp(ry) if ry is not None else None,
+                                     C.byref(d) if d is not None else None, C.byref(q)), ctx.handle)
+    return QualityReport(q.q_max, q.q_mean, q.r_max if q.has_reference else None,
+                         q.r_mean if q.has_reference else None, q.l_inf if q.has_l_inf else None)

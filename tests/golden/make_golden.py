@@ -148,6 +148,22 @@ def main():
                                tol=1e-12, threads=4)
     G["sdd_running33_xi"] = xi
     G["sdd_running33_eta"] = eta
+    # -- invert_mesh + quality_report (proj/src/invert.cpp, proj/src/quality.cpp)
+    sx_, se_ = ref.solve_single_domain(B.density(B.RUNNING), UNIT, 33, 33, tol=1e-10)
+    G["single_running33_xi"], G["single_running33_eta"] = sx_, se_
+    X0, Y0 = ref.invert_mesh(sx_, se_, 33, 33, UNIT, 33, 33, threads=4)
+    G["invert_single_running33"] = np.stack([X0, Y0])
+    X1, Y1 = ref.invert_mesh(xi, eta, 33, 33, UNIT, 33, 33, threads=4)  # the SDD mesh above
+    G["invert_sdd_running33"] = np.stack([X1, Y1])
+    G["quality_sdd_running33"] = ref.quality(X1, Y1, 33, 33, UNIT, X0, Y0, B.density(B.RUNNING))
+    X2, Y2 = ref.invert_mesh(sx_, se_, 33, 33, UNIT, 57, 41, threads=4)  # non-square target grid
+    G["invert_single_running33_57x41"] = np.stack([X2, Y2])
+    G["quality_single_running33_57x41"] = ref.quality(X2, Y2, 57, 41, UNIT)
+    fx, fe = ref.solve_single_domain(B.density(B.FIVE_RING), FIVE, 41, 41, tol=1e-10)
+    X3, Y3 = ref.invert_mesh(fx, fe, 41, 41, FIVE, 41, 41, threads=4)
+    G["single_five41_xi"], G["single_five41_eta"] = fx, fe
+    G["invert_single_five41"] = np.stack([X3, Y3])
+    G["quality_single_five41"] = ref.quality(X3, Y3, 41, 41, FIVE)
     np.savez_compressed(OUT, **G)
     print(f"wrote {OUT}: {len(G)} arrays, {os.path.getsize(OUT) / 1024:.0f} KiB")
 

@@ -1,0 +1,90 @@
+"""GPU inversion (K4) and quality statistics (K5) against the reference's
+invert_mesh / quality_report outputs (tests/golden, made by the reference).
+BASELINE.json: mesh-quality statistics must match within 1e-6; the kernels
+keep the reference's operation order, so they match bit for bit."""
+import numpy as np
+import pytest
+
+from paper_1310_3435_b200 import sdd
+
+pytestmark = pytest.mark.gpu
+UNIT = sdd.RectDomain(0, 1, 0, 1)
+FIVE = sdd.RectDomain(-1, 1, -1, 1)
+
+
+def test_invert_single_domain_bit_identical(golden, ctx):
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    mesh = sdd.invert_mesh(golden["single_running33_xi"], golden["single_running33_eta"], spec, 33, 33, ctx=ctx)
+    want = golden["invert_single_running33"]
+    assert np.array_equal(mesh.x, want[0]) and np.array_equal(mesh.y, want[1])
+
+
+def test_invert_non_square_targets_and_quality(golden, ctx):
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    mesh = sdd.invert_mesh(golden["single_running33_xi"], golden["single_running33_eta"], spec, 57, 41, ctx=ctx)
+    want = golden["invert_single_running33_57x41"]
+    assert np.array_equal(mesh.x, want[0]) and np.array_equal(mesh.y, want[1])
+    q = sdd.quality_report(mesh, ctx=ctx)
+    wq = golden["quality_single_running33_57x41"]
+    assert abs(q.q_max - wq[0]) <= 1e-12 and abs(q.q_mean - wq[1]) <= 1e-12
+    assert q.r_max is None and q.l_inf is None
+
+
+def test_sdd_mesh_quality_against_single_domain_reference(golden, ctx):
+    # the reference's SDD pipeline output vs its single-domain mesh: q, r, l_inf
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    ref_mesh = sdd.invert_mesh(golden["single_running33_xi"], golden["single_running33_eta"], spec, 33, 33, ctx=ctx)
+    mesh = sdd.invert_mesh(golden["sdd_running33_xi"], golden["sdd_running33_eta"], spec, 33, 33, ctx=ctx)
+    want = golden["invert_sdd_running33"]
+    assert np.array_equal(mesh.x, want[0]) and np.array_equal(mesh.y, want[1])
+    q = sdd.quality_report(mesh, ref_mesh, sdd.MonitorFunction.running_example(), ctx=ctx)
+    wq = golden["quality_sdd_running33"]
+    got = np.array([q.q_max, q.q_mean, q.r_max, q.r_mean, q.l_inf])
+    assert np.max(np.abs(got - wq)) <= 1e-6   # BASELINE bar
+    assert np.max(np.abs(got[:4] - wq[:4])) <= 1e-13
+
+
+def test_five_ring_domain(golden, ctx):
+    spec = sdd.GridSpec(FIVE, 41, 41)
+    mesh = sdd.invert_mesh(golden["single_five41_xi"], golden["single_five41_eta"], spec, 41, 41, ctx=ctx)
+    want = golden["invert_single_five41"]
+    assert np.array_equal(mesh.x, want[0]) and np.array_equal(mesh.y, want[1])
+    q = sdd.quality_report(mesh, ctx=ctx)
+    wq = golden["quality_single_five41"]
+    assert abs(q.q_max - wq[0]) <= 1e-12 and abs(q.q_mean - wq[1]) <= 1e-12
+
+
+def test_gpu_pipeline_quality_end_to_end(golden, ctx):
+    # GPU solve_sdd -> GPU inversion -> GPU quality matches the reference's
+    # numbers for the same configuration within the BASELINE 1e-6 bar
+    m = sdd.MonitorFunction.running_example()
+    spec = sdd.GridSpec(UNIT, 33, 33)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("equispaced", 5, m, lay)
+    r = sdd.solve_sdd(m, lay, plan, sdd.WalkConfig(scheme="exponential", lambda_=1000.0, walks=200, seed=1),
+                      sdd.SolverConfig(tol=1e-12), ctx=ctx)
+    ref_mesh = sdd.invert_mesh(golden["single_running33_xi"], golden["single_running33_eta"], spec, 33, 33, ctx=ctx)
+    mesh = sdd.invert_mesh(r.xi, r.eta, spec, 33, 33, ctx=ctx)
+    q = sdd.quality_report(mesh, ref_mesh, m, ctx=ctx)
+    wq = golden["quality_sdd_running33"]
+    assert np.max(np.abs(np.array([q.q_max, q.q_mean, q.r_max, q.r_mean, q.l_inf]) - wq)) <= 1e-6
+
+
+def test_tangled_mesh_raises(ctx):
+    m = 5
+    X, Y = np.meshgrid(np.linspace(0, 1, m), np.linspace(0, 1, m))
+    X = X.copy()
+    X[2, 2], X[2, 3] = X[2, 3], X[2, 2]   # fold one cell pair
+    mesh = sdd.PhysicalMesh(m, m, UNIT, X.ravel(), Y.ravel())
+    with pytest.raises(sdd.TanglingError):
+        sdd.quality_report(mesh, ctx=ctx)
+
+
+def test_invert_validation(ctx):
+    spec = sdd.GridSpec(UNIT, 9, 9)
+    with pytest.raises(sdd.ValidationError):
+        sdd.invert_mesh(np.zeros(81), np.zeros(81), spec, 1, 9, ctx=ctx)
+    bad = np.zeros(81)
+    bad[3] = np.nan
+    with pytest.raises(sdd.EvaluationError):
+        sdd.invert_mesh(bad, np.zeros(81), spec, 9, 9, ctx=ctx)
