@@ -290,14 +290,21 @@ sddg_status sddg_solve_subdomains(sddg_ctx* ctx, const sddg_density* dens, const
                                   const sddg_solver_config* scfg, int32_t s_lo, int32_t s_hi,
                                   double* fields, sddg_solve_info* info);
 
+/* sdd::SddOptions (proj/include/sdd/decomposition.hpp:74-77). */
+typedef struct {
+    int32_t smooth_interface; /* loess pre-smoothing of the interface lines */
+    int32_t smooth_span;      /* odd window, reference default 5 */
+} sddg_sdd_options;
+
 /* Replaces sdd::solve_sdd (proj/include/sdd/decomposition.hpp:91-94):
- * boundary data, interface walks, subdomain solves, assembly into the global
- * xi, eta (nx*ny, index j*nx+i). */
+ * boundary data, interface walks, optional interface smoothing, subdomain
+ * solves, assembly into the global xi, eta (nx*ny, index j*nx+i).  opts may
+ * be NULL (reference defaults: no interface smoothing). */
 sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                            int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t placement,
                            int32_t k, int32_t bc_mode, const sddg_walk_config* cfg,
-                           const sddg_solver_config* scfg, double* xi, double* eta,
-                           sddg_sdd_stats* stats);
+                           const sddg_solver_config* scfg, const sddg_sdd_options* opts,
+                           double* xi, double* eta, sddg_sdd_stats* stats);
 
 /* ------------------------------------------------- post-processing seams */
 
@@ -322,6 +329,29 @@ typedef struct {
 sddg_status sddg_quality_report(sddg_ctx* ctx, const double* x, const double* y, int32_t m_xi,
                                 int32_t m_eta, const double* ref_x, const double* ref_y,
                                 const sddg_density* dens, sddg_quality* out);
+
+/* sdd::SmoothConfig (proj/include/sdd/smoothing.hpp:15-22). */
+typedef enum { SDDG_SMOOTH_GLOBAL = 0, SDDG_SMOOTH_PER_SUBDOMAIN = 1 } sddg_smooth_scope;
+typedef struct {
+    double k;      /* edge-stopping parameter, c = exp(-|grad u|^2 / k^2) */
+    double dt;
+    int32_t steps;
+    int32_t scope; /* sddg_smooth_scope */
+} sddg_smooth_config;
+
+/* Replaces sdd::perona_malik (proj/include/sdd/smoothing.hpp:34-35): FTCS
+ * Perona-Malik steps on xi and eta in place (nx*ny each over dom); sx, sy is
+ * the subdomain layout for the per-subdomain scope (ignored for global).
+ * *stability_warning (nullable) = 1 when dt > hx*hy/4 (stability_warning,
+ * smoothing.cpp:18-26).  NumericalError when the update grows > 10x. */
+sddg_status sddg_perona_malik(sddg_ctx* ctx, double* xi, double* eta, int32_t nx, int32_t ny,
+                              const sddg_domain* dom, const sddg_smooth_config* cfg, int32_t sx,
+                              int32_t sy, int32_t* stability_warning);
+
+/* Replaces sdd::smooth_interface (smoothing.hpp:41): tricube-weighted local
+ * quadratic regression over an odd `span` window; endpoints kept. */
+sddg_status sddg_smooth_interface(sddg_ctx* ctx, const double* values, int32_t n, int32_t span,
+                                  double* out);
 
 #ifdef __cplusplus
 }

@@ -273,6 +273,24 @@ class Ref(_Lib):
         del keep
         return out
 
+    def perona_malik(self, xi, eta, nx, ny, dom, k, dt, steps, scope=0, sx=1, sy=1):
+        xi, eta = _f64(xi).copy(), _f64(eta).copy()
+        self._check(self.L.ref_perona_malik(_dp(xi), _dp(eta), nx, ny, C.byref(dom), C.c_double(k),
+                                            C.c_double(dt), steps, scope, sx, sy))
+        return xi, eta
+
+    def smooth_interface(self, v, span):
+        v = _f64(v)
+        out = np.zeros_like(v)
+        self._check(self.L.ref_smooth_interface(_dp(v), len(v), span, _dp(out)))
+        return out
+
+    def solve_sdd_smoothed(self, dens, dom, nx, ny, sx, sy, strategy, k, cfg, tol, span):
+        xi, eta = np.zeros(nx * ny), np.zeros(nx * ny)
+        self._check(self.L.ref_solve_sdd_smoothed(C.byref(dens), C.byref(dom), nx, ny, sx, sy, strategy,
+                                                  k, C.byref(cfg), C.c_double(tol), span, _dp(xi), _dp(eta)))
+        return xi, eta
+
     def solve_single_domain(self, dens, dom, nx, ny, tol=1e-8):
         xi, eta = np.zeros(nx * ny), np.zeros(nx * ny)
         self._check(self.L.ref_solve_single_domain(C.byref(dens), C.byref(dom), nx, ny,

@@ -24,6 +24,7 @@
 #include "sdd/decomposition.hpp"
 #include "sdd/invert.hpp"
 #include "sdd/quality.hpp"
+#include "sdd/smoothing.hpp"
 #include "sdd/detsolver.hpp"
 #include "sdd/monitor.hpp"
 #include "sdd/parallel.hpp"
@@ -431,6 +432,56 @@ int ref_solve_single_domain(const Density* d, const Domain* dom, int nx, int ny,
         m, GridSpec(RectDomain(dom->xmin, dom->xmax, dom->ymin, dom->ymax), nx, ny), sc);
     std::memcpy(xi, r.sol.xi.values.data(), sizeof(double) * r.sol.xi.values.size());
     std::memcpy(eta, r.sol.eta.values.data(), sizeof(double) * r.sol.eta.values.size());
+    GUARD_END
+}
+
+// perona_malik (proj/src/smoothing.cpp:127-138) in place; scope 0 global, 1 per-subdomain
+int ref_perona_malik(double* xi, double* eta, int nx, int ny, const Domain* dom, double k,
+                     double dt, int steps, int scope, int sx, int sy) {
+    GUARD_BEGIN
+    const GridSpec g(RectDomain(dom->xmin, dom->xmax, dom->ymin, dom->ymax), nx, ny);
+    const MeshSolution sol(ScalarField(g, std::vector<double>(xi, xi + g.size())),
+                           ScalarField(g, std::vector<double>(eta, eta + g.size())));
+    SmoothConfig c;
+    c.k = k;
+    c.dt = dt;
+    c.steps = steps;
+    c.scope = scope == 1 ? SmoothScope::per_subdomain : SmoothScope::global;
+    std::optional<SubdomainLayout> lay;
+    if (scope == 1) lay.emplace(build_layout(g, sx, sy));
+    const MeshSolution out = perona_malik(sol, c, lay ? &*lay : nullptr);
+    std::memcpy(xi, out.xi.values.data(), sizeof(double) * g.size());
+    std::memcpy(eta, out.eta.values.data(), sizeof(double) * g.size());
+    GUARD_END
+}
+
+int ref_smooth_interface(const double* v, int n, int span, double* out) {
+    GUARD_BEGIN
+    const std::vector<double> r = smooth_interface(std::vector<double>(v, v + n), span);
+    std::memcpy(out, r.data(), sizeof(double) * n);
+    GUARD_END
+}
+
+// solve_sdd with SddOptions{smooth_interface=true, span}
+int ref_solve_sdd_smoothed(const Density* d, const Domain* dom, int nx, int ny, int sx, int sy,
+                           int strategy, int k, const WalkCfgC* wc, double tol, int span,
+                           double* xi_out, double* eta_out) {
+    GUARD_BEGIN
+    const MonitorFunction m = make_monitor(*d, *dom);
+    const SubdomainLayout lay = build_layout(
+        GridSpec(RectDomain(dom->xmin, dom->xmax, dom->ymin, dom->ymax), nx, ny), sx, sy);
+    const PlacementStrategy ps = strategy == 0   ? PlacementStrategy::all
+                                 : strategy == 1 ? PlacementStrategy::equispaced
+                                                 : PlacementStrategy::optimal;
+    const InterfacePlan plan = plan_interface_points(ps, k, m, lay);
+    SolverConfig sc;
+    sc.tol = tol;
+    SddOptions o;
+    o.smooth_interface = true;
+    o.smooth_span = span;
+    const SddResult r = solve_sdd(m, lay, plan, make_walk(*wc), sc, o, 4);
+    std::memcpy(xi_out, r.sol.xi.values.data(), sizeof(double) * r.sol.xi.values.size());
+    std::memcpy(eta_out, r.sol.eta.values.data(), sizeof(double) * r.sol.eta.values.size());
     GUARD_END
 }
 

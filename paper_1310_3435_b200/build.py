@@ -32,6 +32,7 @@ UNITS = {
     "reduce.cu": ["-fmad=false"],
     "solver.cu": ["-fmad=false"],
     "mesh.cu": ["-fmad=false"],
+    "smooth.cu": ["-fmad=false"],
     "probe.cu": [],
     "runtime.cu": [],
 }

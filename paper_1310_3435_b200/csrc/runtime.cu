@@ -781,6 +781,26 @@ void solve_subdomains(sddg_ctx* c, const sddg_density& d, const Layout& L,
                      info.data());
 }
 
+// smooth_interface on the GPU (K7, smoothing.cpp:140-183)
+std::vector<double> smooth_line(sddg_ctx* c, const std::vector<double>& v, int span) {
+    const int n = static_cast<int>(v.size());
+    if (span < 3 || span % 2 == 0 || span > n)
+        fail(SDDG_ERR_VALIDATION, "smooth_interface: span must be odd and in [3, length]");
+    cudaStream_t st = c->stream;
+    double* d = static_cast<double*>(c->m_q.ensure(sizeof(double) * 2 * n + 64));
+    int* derr = reinterpret_cast<int*>(d + 2 * n);
+    ck(cudaMemcpyAsync(d, v.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st), "h2d");
+    ck(cudaMemsetAsync(derr, 0, sizeof(int), st), "memset");
+    ck(loess_run(d, d + n, n, span, derr, st), "loess launch");
+    std::vector<double> out(n);
+    int herr = 0;
+    ck(cudaMemcpyAsync(out.data(), d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "loess");
+    if (herr) fail(SDDG_ERR_NUMERICAL, "smooth_interface: singular local fit");
+    return out;
+}
+
 std::vector<std::vector<double>> split_lines(const Layout& L, const double* flat) {
     std::vector<std::vector<double>> out;
     size_t off = 0;
@@ -818,6 +838,11 @@ sddg_status finish(sddg_ctx* c, const Fail& f) {
     std::lock_guard<std::mutex> _lk((ctx)->mu);          \
     try {                                                \
         ck(cudaSetDevice((ctx)->device), "cudaSetDevice");
+#define API_RETURN_OK(ctx) \
+    do {                   \
+        (ctx)->err.clear(); \
+        return SDDG_OK;    \
+    } while (0)
 #define API_END(ctx)                                     \
     }                                                    \
     catch (const Fail& f) {                              \
@@ -1100,8 +1125,8 @@ sddg_status sddg_solve_interfaces(sddg_ctx* ctx, const sddg_density* dens, const
 sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                            int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t placement,
                            int32_t k, int32_t bc_mode, const sddg_walk_config* cfg,
-                           const sddg_solver_config* sc, double* xi, double* eta,
-                           sddg_sdd_stats* stats) {
+                           const sddg_solver_config* sc, const sddg_sdd_options* opts, double* xi,
+                           double* eta, sddg_sdd_stats* stats) {
     API_BEGIN(ctx)
     // solve_sdd (proj/src/decomposition.cpp:262-385)
     const Layout L = build_layout(*dom, nx, ny, sx, sy);
@@ -1111,8 +1136,18 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
     const sddg_boundary bd = make_boundary_view(*dom, nx, ny, tabs);
     const auto pl = plan(*dens, L, placement, k);
     const double t0 = now_s();
-    const IfcResult ifc = solve_interfaces(ctx, *dens, L, pl, bd, *cfg);
+    IfcResult ifc = solve_interfaces(ctx, *dens, L, pl, bd, *cfg);
     const double t_stoc = ifc.mc_points > 0 ? now_s() - t0 : 0.0;
+    // optional interface pre-smoothing (decomposition.cpp:274-282)
+    double t_smooth = 0.0;
+    if (opts && opts->smooth_interface) {
+        const double ts = now_s();
+        for (size_t l = 0; l < ifc.xi.size(); ++l) {
+            ifc.xi[l] = smooth_line(ctx, ifc.xi[l], opts->smooth_span);
+            ifc.eta[l] = smooth_line(ctx, ifc.eta[l], opts->smooth_span);
+        }
+        t_smooth = now_s() - ts;
+    }
     const int64_t steps = ifc.path_steps;
 
     const double ts0 = now_s();
@@ -1139,7 +1174,7 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         stats->t_bd = t_bd;
         stats->t_stoc = t_stoc;
         stats->t_sub = t_bd + (now_s() - ts0);
-        stats->t_smooth = 0.0;
+        stats->t_smooth = t_smooth;
         stats->mc_points = ifc.mc_points;
         stats->subdomain_solves = 2 * n_sub;
         stats->restarts = ifc.restarts;
@@ -1319,6 +1354,69 @@ sddg_status sddg_quality_report(sddg_ctx* ctx, const double* x, const double* y,
             out->l_inf = l;
         }
     }
+    API_END(ctx)
+}
+
+sddg_status sddg_smooth_interface(sddg_ctx* ctx, const double* values, int32_t n, int32_t span,
+                                  double* out) {
+    API_BEGIN(ctx)
+    const std::vector<double> r = smooth_line(ctx, std::vector<double>(values, values + n), span);
+    std::memcpy(out, r.data(), sizeof(double) * n);
+    API_END(ctx)
+}
+
+sddg_status sddg_perona_malik(sddg_ctx* ctx, double* xi, double* eta, int32_t nx, int32_t ny,
+                              const sddg_domain* dom, const sddg_smooth_config* cfg, int32_t sx,
+                              int32_t sy, int32_t* stability_warning) {
+    API_BEGIN(ctx)
+    // SmoothConfig::validate (smoothing.cpp:12-16)
+    if (!(cfg->k > 0.0)) fail(SDDG_ERR_VALIDATION, "SmoothConfig: k must be > 0");
+    if (!(cfg->dt > 0.0)) fail(SDDG_ERR_VALIDATION, "SmoothConfig: dt must be > 0");
+    if (cfg->steps < 0) fail(SDDG_ERR_VALIDATION, "SmoothConfig: steps must be >= 0");
+    check_domain(*dom);
+    if (nx < 3 || ny < 3) fail(SDDG_ERR_VALIDATION, "GridSpec: needs nx >= 3 and ny >= 3");
+    const double hx = (dom->xmax - dom->xmin) / (nx - 1), hy = (dom->ymax - dom->ymin) / (ny - 1);
+    if (stability_warning) *stability_warning = cfg->dt > hx * hy / 4.0 ? 1 : 0;
+    std::vector<int> blocks;
+    if (cfg->scope == SDDG_SMOOTH_PER_SUBDOMAIN) {
+        const Layout L = build_layout(*dom, nx, ny, sx, sy);
+        for (int b = 0; b < sy; ++b)
+            for (int a = 0; a < sx; ++a)
+                blocks.insert(blocks.end(), {a * L.bx, b * L.by, L.bx + 1, L.by + 1});
+    } else if (cfg->scope == SDDG_SMOOTH_GLOBAL) {
+        blocks = {0, 0, nx, ny};
+    } else {
+        fail(SDDG_ERR_VALIDATION, "SmoothConfig: unknown scope");
+    }
+    if (cfg->steps == 0) API_RETURN_OK(ctx);
+    const int nb = static_cast<int>(blocks.size() / 4);
+    const size_t N = static_cast<size_t>(nx) * ny;
+    cudaStream_t st = ctx->stream;
+    double* du = static_cast<double*>(ctx->m_in.ensure(4 * N * sizeof(double)));
+    const size_t scr = pm_scratch_doubles(blocks.data(), nb);
+    double* dscr = static_cast<double*>(ctx->m_q.ensure(scr * sizeof(double)));
+    unsigned long long* dupd = static_cast<unsigned long long*>(
+        ctx->m_misc.ensure(sizeof(unsigned long long) * 2 * cfg->steps + 64));
+    ck(cudaMemcpyAsync(du, xi, N * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    ck(cudaMemcpyAsync(du + N, eta, N * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    std::vector<double> upd(2 * cfg->steps);
+    ck(pm_run(du, du + N, du + 2 * N, du + 3 * N, nx, ny, blocks.data(), nb, hx, hy, cfg->k, cfg->dt,
+              cfg->steps, dscr, dupd, upd.data(), st),
+       "perona-malik");
+    // FTCS instability rule per field (smoothing.cpp:111-121)
+    for (int f = 0; f < 2; ++f) {
+        double prev = -1.0;
+        for (int q = 0; q < cfg->steps; ++q) {
+            const double u = upd[2 * q + f];
+            if (prev >= 0.0 && u > 10.0 * prev && u > 1e-14)
+                fail(SDDG_ERR_NUMERICAL, "perona_malik: FTCS unstable at dt=" + std::to_string(cfg->dt));
+            prev = u;
+        }
+    }
+    ck(cudaMemcpyAsync(xi, du, N * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(eta, du + N, N * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaStreamSynchronize(st), "d2h");
+    ctx->last_launches = 2 * cfg->steps;
     API_END(ctx)
 }
 

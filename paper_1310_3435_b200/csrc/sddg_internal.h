@@ -3,7 +3,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
+#include <vector>
 
 #include "../../include/sddg.h"
 #include "philox.cuh"
@@ -84,6 +87,14 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
                                double omega, double* u, sddg_solve_info* info, int* err,
                                cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem);
+
+// smooth.cu: K6 Perona-Malik FTCS, K7 interface loess
+cudaError_t pm_run(double* u0, double* u1, double* v0, double* v1, int nx, int ny,
+                   const int* blocks_host, int nblocks, double hx, double hy, double k, double dt,
+                   int steps, double* scratch, unsigned long long* dev_upd, double* upd_host,
+                   cudaStream_t s);
+size_t pm_scratch_doubles(const int* blocks_host, int nblocks);
+cudaError_t loess_run(const double* d_in, double* d_out, int n, int span, int* d_err, cudaStream_t s);
 
 // mesh.cu: K4 inversion, K5 quality
 cudaError_t launch_invert(const double* xi, const double* eta, int nx, int ny, double gx0,

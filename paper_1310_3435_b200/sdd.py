@@ -621,17 +621,30 @@ class SddResult:
     warnings: int
 
 
+class _SddOptions(C.Structure):
+    _fields_ = [("smooth_interface", C.c_int32), ("smooth_span", C.c_int32)]
+
+
+@dataclass
+class SddOptions:
+    """sdd::SddOptions (proj/include/sdd/decomposition.hpp:74-77)."""
+    smooth_interface: bool = False
+    smooth_span: int = 5
+
+
 def solve_sdd(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan, wcfg: WalkConfig,
-              scfg: SolverConfig, bc_mode=BC_REFERENCE, ctx=None) -> SddResult:
+              scfg: SolverConfig, bc_mode=BC_REFERENCE, ctx=None,
+              opts: SddOptions | None = None) -> SddResult:
     """sdd::solve_sdd (proj/include/sdd/decomposition.hpp:91-94)."""
     ctx = ctx or default_context()
     g = layout.global_
     xi, eta = np.zeros(g.nx * g.ny), np.zeros(g.nx * g.ny)
     st = _SddStats()
     d, dom, c, sc = m.c(), g.domain.c(), wcfg.c(), scfg.c()
+    o = _SddOptions(1 if (opts and opts.smooth_interface) else 0, opts.smooth_span if opts else 5)
     _check(lib().sddg_solve_sdd(ctx.handle, C.byref(d), C.byref(dom), g.nx, g.ny, layout.n_sub_x,
                                 layout.n_sub_y, PLACE.get(plan.strategy, 99), int(plan.k),
-                                int(bc_mode), C.byref(c), C.byref(sc), _dp(xi), _dp(eta),
+                                int(bc_mode), C.byref(c), C.byref(sc), C.byref(o), _dp(xi), _dp(eta),
                                 C.byref(st)), ctx.handle)
     return SddResult(xi, eta, st.t_stoc, st.t_sub, st.t_smooth, st.mc_points, st.subdomain_solves,
                      st.restarts, st.path_steps, st.warnings)
@@ -762,3 +775,45 @@ def quality_report(mesh: PhysicalMesh, reference: PhysicalMesh | None = None,
                                      C.byref(d) if d is not None else None, C.byref(q)), ctx.handle)
     return QualityReport(q.q_max, q.q_mean, q.r_max if q.has_reference else None,
                          q.r_mean if q.has_reference else None, q.l_inf if q.has_l_inf else None)
+
+
+# --------------------------------------------------------------- smoothing
+class _SmoothCfg(C.Structure):
+    _fields_ = [("k", C.c_double), ("dt", C.c_double), ("steps", C.c_int32), ("scope", C.c_int32)]
+
+
+@dataclass
+class SmoothConfig:
+    """sdd::SmoothConfig (proj/include/sdd/smoothing.hpp:15-22); scope
+    "global" or "per_subdomain"."""
+    k: float = 1000.0
+    dt: float = 1e-4
+    steps: int = 5
+    scope: str = "global"
+
+
+def perona_malik(xi, eta, spec: GridSpec, cfg: SmoothConfig, layout: SubdomainLayout | None = None,
+                 ctx=None):
+    """sdd::perona_malik (smoothing.hpp:34-35) on the GPU: returns (xi, eta,
+    stability_warning)."""
+    ctx = ctx or default_context()
+    xi, eta = _f64(xi).copy(), _f64(eta).copy()
+    scope = {"global": 0, "per_subdomain": 1}.get(cfg.scope, 99)
+    if scope == 1 and layout is None:
+        raise ValidationError("perona_malik: per-subdomain scope needs a layout")
+    sx, sy = (layout.n_sub_x, layout.n_sub_y) if layout is not None else (1, 1)
+    c = _SmoothCfg(cfg.k, cfg.dt, int(cfg.steps), scope)
+    warn = C.c_int32()
+    dom = spec.domain.c()
+    _check(lib().sddg_perona_malik(ctx.handle, _dp(xi), _dp(eta), spec.nx, spec.ny, C.byref(dom),
+                                   C.byref(c), sx, sy, C.byref(warn)), ctx.handle)
+    return xi, eta, bool(warn.value)
+
+
+def smooth_interface(values, span: int, ctx=None):
+    """sdd::smooth_interface (smoothing.hpp:41) on the GPU."""
+    ctx = ctx or default_context()
+    v = _f64(values)
+    out = np.zeros_like(v)
+    _check(lib().sddg_smooth_interface(ctx.handle, _dp(v), len(v), int(span), _dp(out)), ctx.handle)
+    return out

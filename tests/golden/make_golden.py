@@ -164,6 +164,23 @@ def main():
     G["single_five41_xi"], G["single_five41_eta"] = fx, fe
     G["invert_single_five41"] = np.stack([X3, Y3])
     G["quality_single_five41"] = ref.quality(X3, Y3, 41, 41, FIVE)
+    # -- perona_malik + smooth_interface (proj/src/smoothing.cpp)
+    hx = 1.0 / 32
+    dt_ok = 0.9 * hx * hx / 4.0
+    for name, k, steps, scope in (("global", 1000.0, 5, 0), ("subdomain", 1000.0, 4, 1),
+                                  ("edgestop", 0.5, 6, 0)):
+        a, b = ref.perona_malik(xi, eta, 33, 33, UNIT, k, dt_ok, steps, scope, 2, 2)
+        G[f"pm_{name}"] = np.stack([a, b])
+    G["pm_dt"] = np.array([dt_ok])
+    line = lines[0][0]  # a noisy interface line from solve_interfaces above
+    G["loess_in"] = line
+    for span in (3, 5, 9):
+        G[f"loess_{span}"] = ref.smooth_interface(line, span)
+    # 2x1: with crossing lines the reference's per-line smoothing breaks corner
+    # agreement and solve_dirichlet raises ValidationError (mirrored in the tests)
+    sxi, seta = ref.solve_sdd_smoothed(B.density(B.RUNNING), UNIT, 33, 33, 2, 1, 0, 0,
+                                       B.walk_cfg(scheme="exp", lam=1000.0, seed=2, walks=300), 1e-12, 5)
+    G["sdd_smoothed_running33"] = np.stack([sxi, seta])
     np.savez_compressed(OUT, **G)
     print(f"wrote {OUT}: {len(G)} arrays, {os.path.getsize(OUT) / 1024:.0f} KiB")
 
