@@ -146,9 +146,9 @@ sddg_status sddg_last_stats(const sddg_ctx* ctx, int64_t* path_steps, int64_t* l
 sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops);
 
 /* Diagnostics: max ulp error over n sample points of the performance-mode
- * elementary functions (exp, log, sincos(2 pi u), sqrt, rcp) against the
- * CUDA library. */
-sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[5]);
+ * elementary functions (exp, log on (0, 0.9], sincos(2 pi u), sqrt, rcp)
+ * against the CUDA library; slot 5: max ulp error of log on (0.9, 1). */
+sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[6]);
 
 /* ------------------------------------------------------------- walk seams */
 

@@ -149,3 +149,89 @@ __device__ __forceinline__ void fsincos_2pi(double u, double& sn, double& cs) {
 
 }  // namespace fm
 }  // namespace sddg
+
+// ---------------------------------------------------------------------------
+// Table-driven variants (glibc-style reductions) used by the walk kernel:
+// a small table in shared memory replaces most polynomial terms, cutting the
+// step's elementary-function cost from ~150 to ~90 instructions.  Tables are
+// built on the host in 80-bit long double and rounded once (runtime.cu
+// make_fm_tables); each CTA copies them to shared memory at start.
+namespace sddg {
+namespace fm {
+
+struct FmTables {
+    double sc[256][2];   // sin, cos of 2 pi j / 256
+    double lg[128][3];   // 1/c_j, log(c_j) (hi, lo) [or log(c_j / 2) for c_j >= sqrt 2]
+    double e2[64];       // 2^(j/64)
+};
+static_assert(sizeof(FmTables) == 7680, "FmTables layout");
+
+constexpr double k64Ln2 = 92.33248261689366;       // 64 / ln 2
+constexpr double kLn2_64Hi = 0.010830424696249145;  // ln 2 / 64
+constexpr double kLn2_64Lo = 3.623510646634843e-19;
+
+// exp(x), x in [-700, 0]: x = (64 e + j) ln2/64 + r, |r| <= ln2/128
+__device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
+    x = fmax(x, -700.0);
+    const double t = fma(x, k64Ln2, kRound);
+    const double n = t - kRound;
+    double r = fma(n, -kLn2_64Hi, x);
+    r = fma(n, -kLn2_64Lo, r);
+    // e^r - 1 = r + r^2/2 + ... + r^6/720  (next term ~3e-20)
+    double p = fma(r, 0.001388888888888889, 0.008333333333333333);
+    p = fma(p, r, 0.041666666666666664);
+    p = fma(p, r, 0.16666666666666666);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = p * r;
+    const int ni = __double2loint(t);
+    const double s = T.e2[ni & 63];
+    const double v = fma(s, p, s);  // 2^(j/64) e^r
+    return __hiloint2double(__double2hiint(v) + ((ni >> 6) << 20), __double2loint(v));
+}
+
+// log(u), u in (2^-54, 1]: u = 2^k m, m in [1,2); c_j = 1 + (j+1/2)/128 of m's
+// top 7 mantissa bits; r = m / c_j - 1 (|r| <= 1/256);  log u = (k + a) ln2 +
+// log(c_j / 2^a) + log1p(r), a = [c_j >= sqrt 2] (no cancellation near u = 1).
+__device__ __forceinline__ double flog_tab(const FmTables& T, double u) {
+    const int hi = __double2hiint(u);
+    const int lo = __double2loint(u);
+    const int j = (hi >> 13) & 127;
+    const int k = ((hi >> 20) - 1023) + (j >= 53 ? 1 : 0);  // c_53 = 1.4180 >= sqrt 2
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+    const double* e = T.lg[j];
+    const double r = fma(m, e[0], -1.0);
+    // log1p(r) = r - r^2/2 + ... + r^7/7  (next term ~3e-20)
+    double p = fma(r, 0.14285714285714285, -0.16666666666666666);
+    p = fma(p, r, 0.2);
+    p = fma(p, r, -0.25);
+    p = fma(p, r, 0.3333333333333333);
+    p = fma(p, r, -0.5);
+    p = p * r;
+    const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - 4503601774854144.0;
+    const double h = fma(dk, kLn2Hi, e[1]);
+    return h + (fma(p, r, r) + fma(dk, kLn2Lo, e[2]));
+}
+
+// sin, cos of 2 pi u, u in [0, 1): 2 pi u = 2 pi j/256 + d, |d| <= pi/256
+__device__ __forceinline__ void fsincos_2pi_tab(const FmTables& T, double u, double& sn,
+                                                double& cs) {
+    const double t = fma(256.0, u, kRound);
+    const double q = t - kRound;                       // rint(256 u)
+    const double d = 6.283185307179586 * fma(-0.00390625, q, u);  // exact f, |f| <= 1/512
+    const double d2 = d * d;
+    // sin d = d (1 - d^2/6 + d^4/120 - d^6/5040), cos d - 1 = d^2 (-1/2 + d^2/24 - d^4/720)
+    double ps = fma(d2, -0.0001984126984126984, 0.008333333333333333);
+    ps = fma(ps, d2, -0.16666666666666666);
+    const double sd = fma(ps * d2, d, d);
+    double pc = fma(d2, -0.001388888888888889, 0.041666666666666664);
+    pc = fma(pc, d2, -0.5);
+    const double cm1 = pc * d2;
+    const double* e = T.sc[__double2loint(t) & 255];
+    const double s0 = e[0], c0 = e[1];
+    sn = s0 + fma(c0, sd, s0 * cm1);
+    cs = c0 + fma(-s0, sd, c0 * cm1);
+}
+
+}  // namespace fm
+}  // namespace sddg

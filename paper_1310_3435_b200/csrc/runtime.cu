@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "fastmath.cuh"
 #include "host_density.h"
 #include "sddg_internal.h"
 
@@ -88,6 +89,7 @@ struct sddg_ctx {
     double last_ms = 0.0;
     std::map<int, int> occ;  // (dv*2+prec) -> blocks per SM
     std::vector<cudaEvent_t> bev;  // per-batch walk-kernel events
+    DevBuf fm_tables;              // fastmath.cuh FmTables (performance mode)
 };
 
 namespace {
@@ -296,6 +298,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     uint32_t* rm = static_cast<uint32_t*>(c->rec_meta.ensure(sizeof(uint32_t) * cap));
     WalkArgs a;
     fill_args(a, d, dom, bd, cfg, dtab);
+    a.fm_tables = c->fm_tables.p;
     a.walks = W;
     a.walk_lo = 0;
     a.next = &cnt->next;
@@ -858,6 +861,27 @@ sddg_status finish(sddg_ctx* c, const Fail& f) {
 
 namespace sddg {
 
+// Tables of fastmath.cuh, in 80-bit long double, rounded once to double.
+void make_fm_tables(void* out) {
+    fm::FmTables& t = *static_cast<fm::FmTables*>(out);
+    const long double pi = acosl(-1.0L), ln2 = logl(2.0L);
+    for (int j = 0; j < 256; ++j) {
+        const long double a = 2.0L * pi * j / 256.0L;
+        t.sc[j][0] = static_cast<double>(sinl(a));
+        t.sc[j][1] = static_cast<double>(cosl(a));
+    }
+    for (int j = 0; j < 128; ++j) {
+        const double c = 1.0 + (j + 0.5) / 128.0;
+        const double rc = static_cast<double>(1.0L / c);
+        long double L = -logl(static_cast<long double>(rc));  // log(1/rc), consistent with r
+        if (j >= 53) L -= ln2;                               // log(c/2) branch
+        t.lg[j][0] = rc;
+        t.lg[j][1] = static_cast<double>(L);
+        t.lg[j][2] = static_cast<double>(L - static_cast<long double>(t.lg[j][1]));
+    }
+    for (int j = 0; j < 64; ++j) t.e2[j] = static_cast<double>(exp2l(j / 64.0L));
+}
+
 bool walk_variant_supported(int dv, int precision) {
     if (dv >= 32 && dv <= 34) return true;
     return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18));
@@ -906,6 +930,12 @@ sddg_status sddg_create(int32_t device, sddg_ctx** out) {
         ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
         ck(cudaEventCreate(&c->ev0), "event");
         ck(cudaEventCreate(&c->ev1), "event");
+        {
+            fm::FmTables t;
+            make_fm_tables(&t);
+            void* d = c->fm_tables.ensure(sizeof(t));
+            ck(cudaMemcpy(d, &t, sizeof(t), cudaMemcpyHostToDevice), "fm tables");
+        }
         *out = c;
     } catch (const Fail& f) {
         g_free_err = f.msg;
@@ -918,7 +948,7 @@ void sddg_destroy(sddg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->perm, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
@@ -945,11 +975,11 @@ sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops
     API_END(ctx)
 }
 
-sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[5]) {
+sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[6]) {
     API_BEGIN(ctx)
-    unsigned long long m[5];
-    ck(fastmath_selftest(n, m), "fastmath self-test");
-    for (int k = 0; k < 5; ++k) max_ulp[k] = m[k];
+    unsigned long long m[6];
+    ck(fastmath_selftest(n, ctx->fm_tables.p, m), "fastmath self-test");
+    for (int k = 0; k < 6; ++k) max_ulp[k] = m[k];
     API_END(ctx)
 }
 
@@ -1014,6 +1044,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         sddg_path* dd = static_cast<sddg_path*>(ctx->dump.ensure(sizeof(sddg_path) * n));
         WalkArgs a;
         fill_args(a, *dens, *dom, *bd, *cfg, dtab);
+        a.fm_tables = ctx->fm_tables.p;
         a.px = dn;
         a.py = dn + 1;
         a.pid = reinterpret_cast<const uint64_t*>(dn + 2);

@@ -54,7 +54,11 @@ struct WalkArgs {
     double* rec_g;
     uint32_t* rec_meta;  // edge | epochs_used << 2
     sddg_path* dump;
+    const void* fm_tables;  // fastmath.cuh FmTables in global memory (performance mode)
 };
+
+// fastmath tables (host-built in long double, uploaded once per context)
+void make_fm_tables(void* host_tables7680);
 
 // walk_ref.cu (fp64, -fmad=false) and walk_fast.cu (analytic drifts, fp64 + fp32)
 bool walk_variant_supported(int dv, int precision);
@@ -107,6 +111,6 @@ cudaError_t launch_linf(const double* X, const double* Y, const double* RX, cons
                         cudaStream_t s);
 
 cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
-cudaError_t fastmath_selftest(int64_t n, unsigned long long* host_maxulp5);
+cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long* host_maxulp5);
 
 }  // namespace sddg

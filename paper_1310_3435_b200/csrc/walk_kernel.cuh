@@ -39,14 +39,14 @@ struct RealOps<double, FAST> {
     __device__ static __forceinline__ double u(uint64_t u) { return u01_d(u); }
     __device__ static __forceinline__ double u_open(uint64_t u) { return u01_open_d(u); }
     // rng.hpp:66-73: r = sqrt(-2 ln u1), a = 2 pi u2, z = (r cos a, r sin a)
-    __device__ static __forceinline__ void box_muller(uint64_t a, uint64_t b, double& z0,
-                                                      double& z1) {
+    __device__ static __forceinline__ void box_muller(const fm::FmTables& T, uint64_t a,
+                                                      uint64_t b, double& z0, double& z1) {
         const double u1 = u01_open_d(a);
         const double u2 = u01_d(b);
         double s, c, r;
         if constexpr (FAST) {
-            r = fm::fsqrt_pos(-2.0 * fm::flog_unit(u1));
-            fm::fsincos_2pi(u2, s, c);
+            r = fm::fsqrt_pos(-2.0 * fm::flog_tab(T, u1));
+            fm::fsincos_2pi_tab(T, u2, s, c);
         } else {
             r = sqrt(-2.0 * log(u1));
             sincos(6.283185307179586476925286766559 * u2, &s, &c);
@@ -54,12 +54,12 @@ struct RealOps<double, FAST> {
         z0 = r * c;
         z1 = r * s;
     }
-    __device__ static __forceinline__ double ex(double v) {
-        if constexpr (FAST) return fm::fexp_neg(v);
+    __device__ static __forceinline__ double ex(const fm::FmTables& T, double v) {
+        if constexpr (FAST) return fm::fexp_tab(T, v);
         else return exp(v);
     }
-    __device__ static __forceinline__ double lg(double v) {
-        if constexpr (FAST) return fm::flog_unit(v);
+    __device__ static __forceinline__ double lg(const fm::FmTables& T, double v) {
+        if constexpr (FAST) return fm::flog_tab(T, v);
         else return log(v);
     }
     __device__ static __forceinline__ double sq(double v) { return sqrt(v); }
@@ -69,8 +69,8 @@ template <bool FAST>
 struct RealOps<float, FAST> {
     __device__ static __forceinline__ float u(uint64_t u) { return u01_f(u); }
     __device__ static __forceinline__ float u_open(uint64_t u) { return u01_open_f(u); }
-    __device__ static __forceinline__ void box_muller(uint64_t a, uint64_t b, float& z0,
-                                                      float& z1) {
+    __device__ static __forceinline__ void box_muller(const fm::FmTables&, uint64_t a, uint64_t b,
+                                                      float& z0, float& z1) {
         const float u1 = u01_open_f(a);
         const float u2 = u01_f(b);
         const float r = sqrtf(-2.0f * logf(u1));
@@ -79,15 +79,16 @@ struct RealOps<float, FAST> {
         z0 = r * c;
         z1 = r * s;
     }
-    __device__ static __forceinline__ float ex(float v) { return __expf(v); }
-    __device__ static __forceinline__ float lg(float v) { return logf(v); }
+    __device__ static __forceinline__ float ex(const fm::FmTables&, float v) { return __expf(v); }
+    __device__ static __forceinline__ float lg(const fm::FmTables&, float v) { return logf(v); }
     __device__ static __forceinline__ float sq(float v) { return sqrtf(v); }
 };
 
 template <int DV, typename Real>
-__device__ __forceinline__ bool drift(const DensityParams& P, Real x, Real y, Real& bx, Real& by) {
+__device__ __forceinline__ bool drift(const DensityParams& P, const fm::FmTables& T, Real x, Real y,
+                                      Real& bx, Real& by) {
     if constexpr (DV >= DV_RING_AN) {
-        return drift_an<DV>(x, y, bx, by);
+        return drift_an<DV>(T, x, y, bx, by);
     } else {
         static_assert(sizeof(Real) == 8, "reference drifts are fp64 only");
         return drift_ref<DV>(P, x, y, bx, by);
@@ -160,7 +161,8 @@ __device__ __forceinline__ void segment_exit(const Dom<Real>& d, Real x0, Real y
 template <typename Real, bool FAST, int SCHEME>
 __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real y0, Real x1,
                                               Real y1, Real par, const RoundKeys& rk,
-                                              LaneStream& rng, Real& hx, Real& hy, int& edge) {
+                                              const fm::FmTables& T, LaneStream& rng, Real& hx,
+                                              Real& hy, int& edge) {
     const Real k0 = d.dist(x0, y0, 0), k1 = d.dist(x0, y0, 1), k2 = d.dist(x0, y0, 2),
                k3 = d.dist(x0, y0, 3);
     const Real m0 = d.dist(x1, y1, 0), m1 = d.dist(x1, y1, 1), m2 = d.dist(x1, y1, 2),
@@ -189,7 +191,7 @@ __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real 
         const Real ex = SCHEME == 0 ? d0 * d1 / par : par * (d1 < d0 ? d1 : d0);
         if (ex > Real(40)) continue;
         const Real u = RealOps<Real, FAST>::u(rng.next_one(rk));
-        if (u < RealOps<Real, FAST>::ex(-ex)) {
+        if (u < RealOps<Real, FAST>::ex(T, -ex)) {
             const Real sum = d0 + d1;
             const Real s = sum > Real(0) ? d0 / sum : Real(0);
             hx = x0 + s * (x1 - x0);
@@ -224,6 +226,15 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);
     const uint32_t max_steps = a.max_steps32;
+    // performance mode: elementary-function tables in shared memory
+    extern __shared__ double dyn_smem[];
+    fm::FmTables& T = *reinterpret_cast<fm::FmTables*>(dyn_smem);
+    if constexpr (FAST && sizeof(Real) == 8) {
+        const double* src = reinterpret_cast<const double*>(a.fm_tables);
+        for (int k = threadIdx.x; k < static_cast<int>(sizeof(fm::FmTables) / 8); k += blockDim.x)
+            dyn_smem[k] = src[k];
+        __syncthreads();
+    }
 
     uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     uint64_t my_steps = 0;
@@ -244,19 +255,19 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
             Real bx, by, nxp, nyp, z0, z1;
             bool ok;
             if constexpr (SCHEME == 0) {
-                ok = drift<DV, Real>(P, x, y, bx, by);
+                ok = drift<DV, Real>(P, T, x, y, bx, by);
                 uint64_t ua, ub;
                 rng.next_pair(a.rk, ua, ub);
-                Ops::box_muller(ua, ub, z0, z1);
+                Ops::box_muller(T, ua, ub, z0, z1);
                 nxp = x + bx * dt + sq2dt * z0;
                 nyp = y + by * dt + sq2dt * z1;
             } else {
                 // step_exponential (sde.cpp:123-140): dt ~ Exp(lambda) first
-                const Real edt = -Ops::lg(Ops::u_open(rng.next_one(a.rk))) / Real(a.lambda);
-                ok = drift<DV, Real>(P, x, y, bx, by);
+                const Real edt = -Ops::lg(T, Ops::u_open(rng.next_one(a.rk))) / Real(a.lambda);
+                ok = drift<DV, Real>(P, T, x, y, bx, by);
                 uint64_t ua, ub;
                 rng.next_pair(a.rk, ua, ub);
-                Ops::box_muller(ua, ub, z0, z1);
+                Ops::box_muller(T, ua, ub, z0, z1);
                 const Real s = Ops::sq(Real(2) * edt);
                 nxp = x + bx * edt + s * z0;
                 nyp = y + by * edt + s * z1;
@@ -284,13 +295,13 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
                         const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
                         const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
                         if (pB <= thr || pT <= thr || pL <= thr || pR <= thr)
-                            exited = edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk,
+                            exited = edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T,
                                                                   rng, hx, hy, edge);
                     }
                 }
             } else {
-                exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, rng,
-                                                      hx, hy, edge);
+                exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T,
+                                                      rng, hx, hy, edge);
             }
             if (!exited) {
                 x = nxp;
@@ -357,20 +368,26 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
 
 // All (SCHEME, BRIDGE) instantiations of one drift variant.
 template <int DV, typename Real>
+constexpr size_t walk_smem() {
+    return (DV >= DV_RING_AN && sizeof(Real) == 8) ? sizeof(fm::FmTables) : 0;
+}
+
+template <int DV, typename Real>
 cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
+    constexpr size_t sm = walk_smem<DV, Real>();
     if (a.scheme == SDDG_SCHEME_EXPONENTIAL)
-        walk_kernel<DV, Real, 1, false><<<grid, kWalkBlock, 0, s>>>(a);
+        walk_kernel<DV, Real, 1, false><<<grid, kWalkBlock, sm, s>>>(a);
     else if (a.bridge)
-        walk_kernel<DV, Real, 0, true><<<grid, kWalkBlock, 0, s>>>(a);
+        walk_kernel<DV, Real, 0, true><<<grid, kWalkBlock, sm, s>>>(a);
     else
-        walk_kernel<DV, Real, 0, false><<<grid, kWalkBlock, 0, s>>>(a);
+        walk_kernel<DV, Real, 0, false><<<grid, kWalkBlock, sm, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int DV, typename Real>
 cudaError_t occupancy_variant(int* b) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, walk_kernel<DV, Real, 0, true>,
-                                                         kWalkBlock, 0);
+                                                         kWalkBlock, walk_smem<DV, Real>());
 }
 
 }  // namespace sddg

@@ -284,7 +284,9 @@ def test_config3_scale_properties_fp32(ctx):
 def test_fastmath_accuracy(ctx):
     # performance-mode elementary functions (fastmath.cuh) vs the CUDA library
     import ctypes as C
-    m = (C.c_uint64 * 5)()
+    m = (C.c_uint64 * 6)()
     sdd._check(sdd.lib().sddg_selftest_fastmath(ctx.handle, C.c_int64(1 << 22), m), ctx.handle)
-    exp_u, log_u, sc_u, sqrt_u, rcp_u = list(m)
+    exp_u, log_u, sc_u, sqrt_u, rcp_u, log_abs_near1 = list(m)
     assert exp_u <= 4 and log_u <= 4 and sc_u <= 4 and sqrt_u <= 2 and rcp_u <= 2, list(m)
+    print("fastmath max ulp (exp, log, sincos, sqrt, rcp, log near 1):", list(m))
+    assert log_abs_near1 <= 4096, list(m)  # cancellation near u = 1: <= 1e-12 relative
