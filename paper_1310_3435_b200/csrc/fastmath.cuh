@@ -163,8 +163,25 @@ struct FmTables {
     double sc[256][2];   // sin, cos of 2 pi j / 256
     double lg[128][3];   // 1/c_j, log(c_j) (hi, lo) [or log(c_j / 2) for c_j >= sqrt 2]
     double e2[64];       // 2^(j/64)
+    double k[24];        // polynomial / reduction constants (FmK), read with LDS so the
+                         // step loop does not rematerialise 64-bit immediates (2 UMOV each)
 };
-static_assert(sizeof(FmTables) == 7680, "FmTables layout");
+static_assert(sizeof(FmTables) == 7872, "FmTables layout");
+
+// indices into FmTables::k (pairs adjacent in use order -> LDS.128)
+enum FmK {
+    K_E6 = 0, K_E5, K_E4, K_E3,            // 1/720, 1/120, 1/24, 1/6
+    K_64LN2, K_LN2_64HI, K_LN2_64LO, K_PAD0, // 64/ln2, ln2/64 hi, lo
+    K_L7, K_L6, K_L5, K_L3,                // 1/7, -1/6, 1/5, 1/3
+    K_LN2HI, K_LN2LO, K_I2D, K_TWOPI,      // ln2 hi, lo, 2^52+2^31, 2 pi
+    K_S7, K_S5, K_S3, K_C6,                // -1/5040, 1/120, -1/6, -1/720
+    K_C4, K_PAD1, K_PAD2, K_PAD3           // 1/24
+};
+#ifdef SDDG_FM_IMMEDIATES
+#define FMK(i, v) (v)
+#else
+#define FMK(i, v) (T.k[i])
+#endif
 
 constexpr double k64Ln2 = 92.33248261689366;       // 64 / ln 2
 constexpr double kLn2_64Hi = 0.010830424696249145;  // ln 2 / 64
@@ -173,14 +190,14 @@ constexpr double kLn2_64Lo = 3.623510646634843e-19;
 // exp(x), x in [-700, 0]: x = (64 e + j) ln2/64 + r, |r| <= ln2/128
 __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
     x = fmax(x, -700.0);
-    const double t = fma(x, k64Ln2, kRound);
+    const double t = fma(x, FMK(K_64LN2, k64Ln2), kRound);
     const double n = t - kRound;
-    double r = fma(n, -kLn2_64Hi, x);
-    r = fma(n, -kLn2_64Lo, r);
+    double r = fma(n, -FMK(K_LN2_64HI, kLn2_64Hi), x);
+    r = fma(n, -FMK(K_LN2_64LO, kLn2_64Lo), r);
     // e^r - 1 = r + r^2/2 + ... + r^6/720  (next term ~3e-20)
-    double p = fma(r, 0.001388888888888889, 0.008333333333333333);
-    p = fma(p, r, 0.041666666666666664);
-    p = fma(p, r, 0.16666666666666666);
+    double p = fma(r, FMK(K_E6, 0.001388888888888889), FMK(K_E5, 0.008333333333333333));
+    p = fma(p, r, FMK(K_E4, 0.041666666666666664));
+    p = fma(p, r, FMK(K_E3, 0.16666666666666666));
     p = fma(p, r, 0.5);
     p = fma(p, r, 1.0);
     p = p * r;
@@ -202,15 +219,15 @@ __device__ __forceinline__ double flog_tab(const FmTables& T, double u) {
     const double* e = T.lg[j];
     const double r = fma(m, e[0], -1.0);
     // log1p(r) = r - r^2/2 + ... + r^7/7  (next term ~3e-20)
-    double p = fma(r, 0.14285714285714285, -0.16666666666666666);
-    p = fma(p, r, 0.2);
+    double p = fma(r, FMK(K_L7, 0.14285714285714285), FMK(K_L6, -0.16666666666666666));
+    p = fma(p, r, FMK(K_L5, 0.2));
     p = fma(p, r, -0.25);
-    p = fma(p, r, 0.3333333333333333);
+    p = fma(p, r, FMK(K_L3, 0.3333333333333333));
     p = fma(p, r, -0.5);
     p = p * r;
-    const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - 4503601774854144.0;
-    const double h = fma(dk, kLn2Hi, e[1]);
-    return h + (fma(p, r, r) + fma(dk, kLn2Lo, e[2]));
+    const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - FMK(K_I2D, 4503601774854144.0);
+    const double h = fma(dk, FMK(K_LN2HI, kLn2Hi), e[1]);
+    return h + (fma(p, r, r) + fma(dk, FMK(K_LN2LO, kLn2Lo), e[2]));
 }
 
 // sin, cos of 2 pi u, u in [0, 1): 2 pi u = 2 pi j/256 + d, |d| <= pi/256
@@ -218,13 +235,13 @@ __device__ __forceinline__ void fsincos_2pi_tab(const FmTables& T, double u, dou
                                                 double& cs) {
     const double t = fma(256.0, u, kRound);
     const double q = t - kRound;                       // rint(256 u)
-    const double d = 6.283185307179586 * fma(-0.00390625, q, u);  // exact f, |f| <= 1/512
+    const double d = FMK(K_TWOPI, 6.283185307179586) * fma(-0.00390625, q, u);  // exact f, |f| <= 1/512
     const double d2 = d * d;
     // sin d = d (1 - d^2/6 + d^4/120 - d^6/5040), cos d - 1 = d^2 (-1/2 + d^2/24 - d^4/720)
-    double ps = fma(d2, -0.0001984126984126984, 0.008333333333333333);
-    ps = fma(ps, d2, -0.16666666666666666);
+    double ps = fma(d2, FMK(K_S7, -0.0001984126984126984), FMK(K_S5, 0.008333333333333333));
+    ps = fma(ps, d2, FMK(K_S3, -0.16666666666666666));
     const double sd = fma(ps * d2, d, d);
-    double pc = fma(d2, -0.001388888888888889, 0.041666666666666664);
+    double pc = fma(d2, FMK(K_C6, -0.001388888888888889), FMK(K_C4, 0.041666666666666664));
     pc = fma(pc, d2, -0.5);
     const double cm1 = pc * d2;
     const double* e = T.sc[__double2loint(t) & 255];

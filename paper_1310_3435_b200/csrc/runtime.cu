@@ -880,6 +880,28 @@ void make_fm_tables(void* out) {
         t.lg[j][2] = static_cast<double>(L - static_cast<long double>(t.lg[j][1]));
     }
     for (int j = 0; j < 64; ++j) t.e2[j] = static_cast<double>(exp2l(j / 64.0L));
+    using namespace fm;
+    for (double& v : t.k) v = 0.0;
+    t.k[K_E6] = 1.0 / 720.0;
+    t.k[K_E5] = 1.0 / 120.0;
+    t.k[K_E4] = 1.0 / 24.0;
+    t.k[K_E3] = 1.0 / 6.0;
+    t.k[K_64LN2] = k64Ln2;
+    t.k[K_LN2_64HI] = kLn2_64Hi;
+    t.k[K_LN2_64LO] = kLn2_64Lo;
+    t.k[K_L7] = 1.0 / 7.0;
+    t.k[K_L6] = -1.0 / 6.0;
+    t.k[K_L5] = 0.2;
+    t.k[K_L3] = 1.0 / 3.0;
+    t.k[K_LN2HI] = kLn2Hi;
+    t.k[K_LN2LO] = kLn2Lo;
+    t.k[K_I2D] = 4503601774854144.0;
+    t.k[K_TWOPI] = 6.283185307179586;
+    t.k[K_S7] = -1.0 / 5040.0;
+    t.k[K_S5] = 1.0 / 120.0;
+    t.k[K_S3] = -1.0 / 6.0;
+    t.k[K_C6] = -1.0 / 720.0;
+    t.k[K_C4] = 1.0 / 24.0;
 }
 
 bool walk_variant_supported(int dv, int precision) {
