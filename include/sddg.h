@@ -330,6 +330,21 @@ sddg_status sddg_quality_report(sddg_ctx* ctx, const double* x, const double* y,
                                 int32_t m_eta, const double* ref_x, const double* ref_y,
                                 const sddg_density* dens, sddg_quality* out);
 
+/* The stochastic-full pipeline's solve (run_stochastic_full,
+ * proj/src/cli.cpp:236-270): boundary tables on the boundary, one Monte Carlo
+ * estimate per interior node (point_id = j*nx + i) in a single GPU batch.
+ * xi, eta: nx*ny; stats->restarts and ->warnings (restart fraction > 1%). */
+sddg_status sddg_stochastic_full(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                 int32_t nx, int32_t ny, const sddg_walk_config* cfg, double* xi,
+                                 double* eta, sddg_sdd_stats* stats);
+
+/* Host: sdd::write_mesh (proj/src/mesh_io.cpp:22-46), the bit-exact
+ * "sddmesh v1" text format (%.17g, LF); the solution grid must match the
+ * mesh shape. */
+sddg_status sddg_write_mesh(const double* x, const double* y, int32_t m_xi, int32_t m_eta,
+                            const double* xi, const double* eta, int32_t nx, int32_t ny,
+                            const char* path);
+
 /* sdd::SmoothConfig (proj/include/sdd/smoothing.hpp:15-22). */
 typedef enum { SDDG_SMOOTH_GLOBAL = 0, SDDG_SMOOTH_PER_SUBDOMAIN = 1 } sddg_smooth_scope;
 typedef struct {

@@ -291,6 +291,11 @@ class Ref(_Lib):
                                                   k, C.byref(cfg), C.c_double(tol), span, _dp(xi), _dp(eta)))
         return xi, eta
 
+    def write_mesh(self, x, y, m_xi, m_eta, xi, eta, nx, ny, path):
+        x, y, xi, eta = map(_f64, (x, y, xi, eta))
+        self._check(self.L.ref_write_mesh(_dp(x), _dp(y), m_xi, m_eta, _dp(xi), _dp(eta), nx, ny,
+                                          path.encode()))
+
     def solve_single_domain(self, dens, dom, nx, ny, tol=1e-8):
         xi, eta = np.zeros(nx * ny), np.zeros(nx * ny)
         self._check(self.L.ref_solve_single_domain(C.byref(dens), C.byref(dom), nx, ny,

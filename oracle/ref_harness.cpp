@@ -25,6 +25,7 @@
 #include "sdd/invert.hpp"
 #include "sdd/quality.hpp"
 #include "sdd/smoothing.hpp"
+#include "sdd/mesh_io.hpp"
 #include "sdd/detsolver.hpp"
 #include "sdd/monitor.hpp"
 #include "sdd/parallel.hpp"
@@ -482,6 +483,21 @@ int ref_solve_sdd_smoothed(const Density* d, const Domain* dom, int nx, int ny, 
     const SddResult r = solve_sdd(m, lay, plan, make_walk(*wc), sc, o, 4);
     std::memcpy(xi_out, r.sol.xi.values.data(), sizeof(double) * r.sol.xi.values.size());
     std::memcpy(eta_out, r.sol.eta.values.data(), sizeof(double) * r.sol.eta.values.size());
+    GUARD_END
+}
+
+int ref_write_mesh(const double* x, const double* y, int m_xi, int m_eta, const double* xi,
+                   const double* eta, int nx, int ny, const char* path) {
+    GUARD_BEGIN
+    const RectDomain rd(0, 1, 0, 1);
+    PhysicalMesh mesh(m_xi, m_eta, rd);
+    const std::size_t n = static_cast<std::size_t>(m_xi) * m_eta;
+    mesh.x.assign(x, x + n);
+    mesh.y.assign(y, y + n);
+    const GridSpec g(rd, nx, ny);
+    const MeshSolution sol(ScalarField(g, std::vector<double>(xi, xi + g.size())),
+                           ScalarField(g, std::vector<double>(eta, eta + g.size())));
+    write_mesh(mesh, sol, path);
     GUARD_END
 }
 

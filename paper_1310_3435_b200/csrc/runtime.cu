@@ -13,7 +13,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <map>
 #include <mutex>
 #include <string>
@@ -1471,6 +1474,89 @@ sddg_status sddg_perona_malik(sddg_ctx* ctx, double* xi, double* eta, int32_t nx
     ck(cudaStreamSynchronize(st), "d2h");
     ctx->last_launches = 2 * cfg->steps;
     API_END(ctx)
+}
+
+sddg_status sddg_stochastic_full(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                 int32_t nx, int32_t ny, const sddg_walk_config* cfg, double* xi,
+                                 double* eta, sddg_sdd_stats* stats) {
+    API_BEGIN(ctx)
+    check_domain(*dom);
+    if (nx < 3 || ny < 3) fail(SDDG_ERR_VALIDATION, "GridSpec: needs nx >= 3 and ny >= 3");
+    const double t0 = now_s();
+    const auto tabs = boundary_tables(*dens, *dom, nx, ny, SDDG_BC_REFERENCE);
+    const sddg_boundary bd = make_boundary_view(*dom, nx, ny, tabs);
+    const double hx = (dom->xmax - dom->xmin) / (nx - 1), hy = (dom->ymax - dom->ymin) / (ny - 1);
+    for (int i = 0; i < nx; ++i) {
+        xi[i] = tabs[0][i];
+        xi[static_cast<size_t>(ny - 1) * nx + i] = tabs[1][i];
+        eta[i] = tabs[4][i];
+        eta[static_cast<size_t>(ny - 1) * nx + i] = tabs[5][i];
+    }
+    for (int j = 0; j < ny; ++j) {
+        xi[static_cast<size_t>(j) * nx] = tabs[2][j];
+        xi[static_cast<size_t>(j) * nx + nx - 1] = tabs[3][j];
+        eta[static_cast<size_t>(j) * nx] = tabs[6][j];
+        eta[static_cast<size_t>(j) * nx + nx - 1] = tabs[7][j];
+    }
+    const int64_t interior = static_cast<int64_t>(nx - 2) * (ny - 2);
+    std::vector<double> px(interior), py(interior);
+    std::vector<uint64_t> pid(interior);
+    for (int64_t n = 0; n < interior; ++n) {
+        const int i = 1 + static_cast<int>(n % (nx - 2)), j = 1 + static_cast<int>(n / (nx - 2));
+        px[n] = dom->xmin + i * hx;
+        py[n] = dom->ymin + j * hy;
+        pid[n] = static_cast<uint64_t>(j) * nx + i;
+    }
+    std::vector<sddg_estimate> est(interior);
+    estimates_host(ctx, *dens, *dom, bd, *cfg, px.data(), py.data(), pid.data(), interior, est.data());
+    int64_t restarts = 0;
+    for (int64_t n = 0; n < interior; ++n) {
+        const size_t g = static_cast<size_t>(pid[n]);
+        xi[g] = est[n].xi;
+        eta[g] = est[n].eta;
+        restarts += est[n].restarts;
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->t_stoc = now_s() - t0;
+        stats->mc_points = interior;
+        stats->restarts = restarts;
+        stats->path_steps = ctx->last_steps;
+        stats->warnings = restarts > interior * cfg->walks / 100 ? 1 : 0;  // cli.cpp:266-268
+    }
+    API_END(ctx)
+}
+
+sddg_status sddg_write_mesh(const double* x, const double* y, int32_t m_xi, int32_t m_eta,
+                            const double* xi, const double* eta, int32_t nx, int32_t ny,
+                            const char* path) {
+    try {
+        if (nx != m_xi || ny != m_eta)
+            fail(SDDG_ERR_VALIDATION, "write_mesh: solution grid " + std::to_string(nx) + "x" +
+                                          std::to_string(ny) + " does not match mesh " +
+                                          std::to_string(m_xi) + "x" + std::to_string(m_eta));
+        auto f17 = [](double v) {
+            char buf[40];
+            std::snprintf(buf, sizeof(buf), "%.17g", v);
+            return std::string(buf);
+        };
+        std::ostringstream os;
+        os << "sddmesh v1 " << m_xi << " " << m_eta << "\n";
+        for (int a = 0; a < m_xi; ++a)
+            for (int b = 0; b < m_eta; ++b) {
+                const size_t n = static_cast<size_t>(b) * m_xi + a;
+                const size_t sidx = static_cast<size_t>(b) * nx + a;
+                os << a << " " << b << " " << f17(x[n]) << " " << f17(y[n]) << " " << f17(xi[sidx])
+                   << " " << f17(eta[sidx]) << "\n";
+            }
+        std::ofstream out(path, std::ios::binary);
+        if (!out) fail(SDDG_ERR_INTERNAL, std::string("write_mesh: cannot open ") + path);
+        out << os.str();
+        if (!out) fail(SDDG_ERR_INTERNAL, std::string("write_mesh: write failed for ") + path);
+    } catch (const Fail& f) {
+        return finish(nullptr, f);
+    }
+    return SDDG_OK;
 }
 
 }  // extern "C"

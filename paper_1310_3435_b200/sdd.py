@@ -817,3 +817,24 @@ def smooth_interface(values, span: int, ctx=None):
     out = np.zeros_like(v)
     _check(lib().sddg_smooth_interface(ctx.handle, _dp(v), len(v), int(span), _dp(out)), ctx.handle)
     return out
+
+
+# --------------------------------------------------------------- stochastic-full, mesh IO
+def stochastic_full(m: MonitorFunction, spec: GridSpec, cfg: WalkConfig, ctx=None):
+    """The stochastic-full solve (run_stochastic_full, proj/src/cli.cpp:236-270):
+    Monte Carlo at every interior node in one GPU batch.  Returns (xi, eta, stats)."""
+    ctx = ctx or default_context()
+    xi, eta = np.zeros(spec.nx * spec.ny), np.zeros(spec.nx * spec.ny)
+    st = _SddStats()
+    d, dom, c = m.c(), spec.domain.c(), cfg.c()
+    _check(lib().sddg_stochastic_full(ctx.handle, C.byref(d), C.byref(dom), spec.nx, spec.ny,
+                                      C.byref(c), _dp(xi), _dp(eta), C.byref(st)), ctx.handle)
+    return xi, eta, {"t_stoc": st.t_stoc, "mc_points": st.mc_points, "restarts": st.restarts,
+                     "path_steps": st.path_steps, "restart_warning": bool(st.warnings)}
+
+
+def write_mesh(mesh: PhysicalMesh, xi, eta, spec: GridSpec, path: str):
+    """sdd::write_mesh (proj/src/mesh_io.cpp:22-46): bit-exact sddmesh v1 text."""
+    x, y, a, b = _f64(mesh.x), _f64(mesh.y), _f64(xi), _f64(eta)
+    _check(lib().sddg_write_mesh(_dp(x), _dp(y), mesh.m_xi, mesh.m_eta, _dp(a), _dp(b), spec.nx,
+                                 spec.ny, path.encode()))

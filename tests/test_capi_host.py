@@ -127,3 +127,18 @@ def test_no_gpu_means_loud_failure():
         pytest.skip("a GPU is present")
     with pytest.raises(sdd.CudaError):
         sdd.Context(0)
+
+
+def test_write_mesh_is_byte_identical_to_reference(golden, tmp_path, refimpl):
+    # sddmesh v1 (proj/src/mesh_io.cpp:22-46): same bytes as the reference writer
+    X = golden["invert_sdd_running33"]
+    xi, eta = golden["sdd_running33_xi"], golden["sdd_running33_eta"]
+    spec = sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), 33, 33)
+    mesh = sdd.PhysicalMesh(33, 33, spec.domain, X[0], X[1])
+    ours, theirs = tmp_path / "ours.txt", tmp_path / "ref.txt"
+    sdd.write_mesh(mesh, xi, eta, spec, str(ours))
+    refimpl.write_mesh(X[0], X[1], 33, 33, xi, eta, 33, 33, str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()
+    assert ours.read_bytes().startswith(b"sddmesh v1 33 33\n")
+    with pytest.raises(sdd.ValidationError):
+        sdd.write_mesh(mesh, xi, eta, sdd.GridSpec(spec.domain, 33, 17), str(ours))

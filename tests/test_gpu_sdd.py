@@ -150,3 +150,20 @@ def test_distributed_solve_sdd_world1_matches_solve_sdd(ctx):
         assert len(est) == r.mc_points
     finally:
         dist.destroy_process_group()
+
+
+def test_stochastic_full_matches_reference_estimates(ctx, oracle):
+    # run_stochastic_full (proj/src/cli.cpp:236-270): every interior node
+    m = sdd.MonitorFunction.running_example()
+    spec = sdd.GridSpec(UNIT, 9, 9)
+    cfg = sdd.WalkConfig(scheme="exponential", lambda_=1000.0, walks=300, seed=5)
+    xi, eta, st = sdd.stochastic_full(m, spec, cfg, ctx=ctx)
+    assert st["mc_points"] == 49 and not st["restart_warning"]
+    odom = B.Domain(0, 1, 0, 1)
+    t = oracle.make_boundary(B.density(B.RUNNING), odom, 9, 9)
+    pts = [(i / 8, j / 8) for j in range(1, 8) for i in range(1, 8)]
+    pid = [j * 9 + i for j in range(1, 8) for i in range(1, 8)]
+    o = oracle.mc_estimate_batch(B.density(B.RUNNING), odom, t, B.walk_cfg(scheme="exp", lam=1000.0, walks=300, seed=5),
+                                 [p[0] for p in pts], [p[1] for p in pts], pid, threads=8)
+    assert np.max(np.abs(xi[pid] - o["xi"])) <= 1e-10 and np.max(np.abs(eta[pid] - o["eta"])) <= 1e-10
+    assert np.array_equal(xi.reshape(9, 9)[0], t.f[0]) and np.array_equal(eta.reshape(9, 9)[:, 0], t.g[2])
