@@ -223,8 +223,25 @@ sddg_status sddg_solve_dirichlet_batch(sddg_ctx* ctx, const double* w_global, in
 typedef enum {
     SDDG_PLACE_ALL = 0,
     SDDG_PLACE_EQUISPACED = 1,
-    SDDG_PLACE_OPTIMAL = 2
-} sddg_placement; /* sdd::PlacementStrategy (decomposition.hpp:40) */
+    SDDG_PLACE_OPTIMAL = 2,
+    /* BASELINE.json config 4 (no reference oracle): k nodes per
+     * line at the grid nodes nearest to equal shares of the trapezoid
+     * integral of the weight w = 1/rho along the line. */
+    SDDG_PLACE_EQUIDISTRIBUTED = 3
+} sddg_placement; /* sdd::PlacementStrategy (decomposition.hpp:40) + config 4 */
+
+typedef enum {
+    SDDG_INTERP_LINEAR = 0, /* reference fill (decomposition.cpp:215-224) */
+    SDDG_INTERP_SPLINE = 1  /* natural cubic spline through the known nodes (config 4, D6) */
+} sddg_interp;
+
+/* sdd::SddOptions (proj/include/sdd/decomposition.hpp:74-77) + fill mode. */
+typedef struct {
+    int32_t smooth_interface; /* loess pre-smoothing of the interface lines */
+    int32_t smooth_span;      /* odd window, reference default 5 */
+    int32_t interp;           /* sddg_interp */
+    int32_t reserved;
+} sddg_sdd_options;
 
 typedef enum {
     SDDG_BC_REFERENCE = 0, /* make_boundary_data: 1D equidistribution (boundary.cpp:44-56) */
@@ -259,7 +276,8 @@ typedef struct {
 sddg_status sddg_solve_interfaces(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                                   int32_t nx, int32_t ny, int32_t sx, int32_t sy,
                                   int32_t placement, int32_t k, const sddg_boundary* bd,
-                                  const sddg_walk_config* cfg, double* xi_lines,
+                                  const sddg_walk_config* cfg, const sddg_sdd_options* opts,
+                                  double* xi_lines,
                                   double* eta_lines, double* se_xi_lines, double* se_eta_lines,
                                   sddg_sdd_stats* stats);
 
@@ -278,8 +296,8 @@ sddg_status sddg_interface_nodes(const sddg_density* dens, const sddg_domain* do
 sddg_status sddg_fill_interfaces(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
                                  int32_t ny, int32_t sx, int32_t sy, int32_t placement, int32_t k,
                                  const sddg_boundary* bd, const sddg_estimate* est, int64_t n,
-                                 double* xi_lines, double* eta_lines, double* se_xi_lines,
-                                 double* se_eta_lines);
+                                 const sddg_sdd_options* opts, double* xi_lines,
+                                 double* eta_lines, double* se_xi_lines, double* se_eta_lines);
 /* GPU: the subdomain phase of solve_sdd (decomposition.cpp:292-355) for
  * subdomains [s_lo, s_hi) (index s = b*sx + a) given the interface lines;
  * fields receives per subdomain its xi then its eta block ((n+1)^2 each,
@@ -289,12 +307,6 @@ sddg_status sddg_solve_subdomains(sddg_ctx* ctx, const sddg_density* dens, const
                                   const double* xi_lines, const double* eta_lines,
                                   const sddg_solver_config* scfg, int32_t s_lo, int32_t s_hi,
                                   double* fields, sddg_solve_info* info);
-
-/* sdd::SddOptions (proj/include/sdd/decomposition.hpp:74-77). */
-typedef struct {
-    int32_t smooth_interface; /* loess pre-smoothing of the interface lines */
-    int32_t smooth_span;      /* odd window, reference default 5 */
-} sddg_sdd_options;
 
 /* Replaces sdd::solve_sdd (proj/include/sdd/decomposition.hpp:91-94):
  * boundary data, interface walks, optional interface smoothing, subdomain

@@ -86,7 +86,7 @@ struct sddg_ctx {
     std::string err;
     std::mutex mu;
     DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm;
-    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err;
+    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large;
     DevBuf m_in, m_out, m_q, m_misc;
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
@@ -418,50 +418,111 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
         max_int = std::max(max_int, (q.nx - 2) * (q.ny - 2));
         max_dim = std::max(max_dim, std::max(q.nx, q.ny));
     }
+    // jobs whose solution fits in shared memory go to the batched K3; larger
+    // ones (e.g. the single-domain 513^2 comparison of config 4) to K3b
     const size_t smem_cap = 227 * 1024;
-    const bool coef_smem = sizeof(double) * 4 * static_cast<size_t>(max_n) <= smem_cap;
-    if (sizeof(double) * static_cast<size_t>(max_n) > smem_cap)
-        fail(SDDG_ERR_VALIDATION, "solve_dirichlet: subdomain exceeds the on-chip solver (" +
-                                      std::to_string(smem_cap / 8) + " nodes)");
-    if (sc.method == SDDG_SOLVER_JACOBI && max_int > solver_max_points())
-        fail(SDDG_ERR_VALIDATION, "solve_dirichlet: Jacobi batch limited to " +
-                                      std::to_string(solver_max_points()) +
-                                      " interior nodes per subdomain; use RBSOR");
+    const bool force_large = std::getenv("SDDG_FORCE_LARGE_SOLVER") != nullptr;
+    std::vector<SolveJob> small, large;
+    int max_n_s = 0, max_int_s = 0, max_dim_s = 0, max_dim_all = 0;
+    int64_t max_n_l = 0;
+    for (int64_t q = 0; q < n; ++q) {
+        const SolveJob& j = jobs[q];
+        const int nn = j.nx * j.ny;
+        max_dim_all = std::max(max_dim_all, std::max(j.nx, j.ny));
+        if (!force_large && sizeof(double) * static_cast<size_t>(nn) <= smem_cap) {
+            small.push_back(j);
+            max_n_s = std::max(max_n_s, nn);
+            max_int_s = std::max(max_int_s, (j.nx - 2) * (j.ny - 2));
+            max_dim_s = std::max(max_dim_s, std::max(j.nx, j.ny));
+        } else {
+            large.push_back(j);
+            max_n_l = std::max<int64_t>(max_n_l, nn);
+        }
+    }
+    (void)max_n;
+    (void)max_int;
+    (void)max_dim;
+    const bool coef_smem = sizeof(double) * 4 * static_cast<size_t>(max_n_s) <= smem_cap;
+    const bool jacobi_small_ok = max_int_s <= solver_max_points();
+    if (sc.method == SDDG_SOLVER_JACOBI && !jacobi_small_ok) {
+        // Jacobi register budget exceeded: route those jobs to K3b as well
+        std::vector<SolveJob> keep;
+        for (const SolveJob& j : small) {
+            if ((j.nx - 2) * (j.ny - 2) > solver_max_points()) {
+                large.push_back(j);
+                max_n_l = std::max<int64_t>(max_n_l, static_cast<int64_t>(j.nx) * j.ny);
+            } else {
+                keep.push_back(j);
+            }
+        }
+        small.swap(keep);
+        max_n_s = max_int_s = 0;
+        for (const SolveJob& j : small) {
+            max_n_s = std::max(max_n_s, j.nx * j.ny);
+            max_int_s = std::max(max_int_s, (j.nx - 2) * (j.ny - 2));
+        }
+    }
     double omega = sc.omega;
     if (sc.method == SDDG_SOLVER_RBSOR && !(omega > 0.0)) {
         const double kPi = 3.14159265358979323846;
-        omega = 2.0 / (1.0 + std::sin(kPi / (max_dim - 1)));
+        omega = 2.0 / (1.0 + std::sin(kPi / (max_dim_all - 1)));
     }
     if (sc.method == SDDG_SOLVER_JACOBI) omega = 1.0;
     const size_t wbytes = sizeof(double) * static_cast<size_t>(gnx) * gny;
     double* dw = static_cast<double*>(c->s_w.ensure(wbytes));
-    SolveJob* dj = static_cast<SolveJob*>(c->s_jobs.ensure(sizeof(SolveJob) * n));
+    SolveJob* dj = static_cast<SolveJob*>(c->s_jobs.ensure(sizeof(SolveJob) * std::max<size_t>(1, small.size())));
     double* dbc = static_cast<double*>(c->s_bc.ensure(sizeof(double) * boff));
     double* du = static_cast<double*>(c->s_u.ensure(sizeof(double) * uoff));
     sddg_solve_info* dinfo = static_cast<sddg_solve_info*>(c->s_info.ensure(sizeof(sddg_solve_info) * n));
     int* derr = static_cast<int*>(c->s_err.ensure(sizeof(int)));
     double* dcoef = nullptr;
-    if (!coef_smem) dcoef = static_cast<double*>(c->s_coef.ensure(sizeof(double) * 3 * max_n * n));
+    if (!small.empty() && !coef_smem)
+        dcoef = static_cast<double*>(c->s_coef.ensure(sizeof(double) * 3 * max_n_s * small.size()));
+    double* dlarge = nullptr;
+    if (!large.empty())
+        dlarge = static_cast<double*>(c->s_large.ensure(sizeof(double) * (5 * max_n_l + 8)));
     cudaStream_t st = c->stream;
     ck(cudaMemcpyAsync(dw, w, wbytes, cudaMemcpyHostToDevice, st), "h2d w");
-    ck(cudaMemcpyAsync(dj, jobs.data(), sizeof(SolveJob) * n, cudaMemcpyHostToDevice, st), "h2d jobs");
     ck(cudaMemcpyAsync(dbc, bc, sizeof(double) * boff, cudaMemcpyHostToDevice, st), "h2d bc");
     ck(cudaMemsetAsync(derr, 0, sizeof(int), st), "memset");
+    // info slots: small jobs first in job order, then large jobs
+    std::vector<int64_t> info_of(n);
+    {
+        int64_t a = 0;
+        std::map<int64_t, int64_t> pos_of_uoff;
+        for (int64_t q = 0; q < n; ++q) pos_of_uoff[jobs[q].u_off] = q;
+        for (const SolveJob& j : small) info_of[a++] = pos_of_uoff[j.u_off];
+        for (const SolveJob& j : large) info_of[a++] = pos_of_uoff[j.u_off];
+    }
     ck(cudaEventRecord(c->ev0, st), "event");
-    ck(launch_solve_batch(dw, gnx, hx, hy, n, dj, dbc, sc.tol, sc.max_iters, sc.init_blend,
-                          sc.method, omega, du, dinfo, derr, st, max_n, max_int, dcoef,
-                          coef_smem ? 1 : 0),
-       "solver launch");
+    int launches = 0;
+    if (!small.empty()) {
+        ck(cudaMemcpyAsync(dj, small.data(), sizeof(SolveJob) * small.size(), cudaMemcpyHostToDevice, st),
+           "h2d jobs");
+        ck(launch_solve_batch(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
+                              sc.max_iters, sc.init_blend, sc.method, omega, du, dinfo, derr, st,
+                              max_n_s, max_int_s, dcoef, coef_smem ? 1 : 0),
+           "solver launch");
+        ++launches;
+    }
+    for (size_t q = 0; q < large.size(); ++q) {
+        ck(launch_solve_large(dw, gnx, hx, hy, large[q], dbc, sc.tol, sc.max_iters, sc.init_blend,
+                              sc.method, omega, du, dinfo + small.size() + q, derr, dlarge, st, c->sms),
+           "large solver launch");
+        ++launches;
+    }
     ck(cudaEventRecord(c->ev1, st), "event");
     int herr = 0;
+    std::vector<sddg_solve_info> hinfo(n);
     ck(cudaMemcpyAsync(u, du, sizeof(double) * uoff, cudaMemcpyDeviceToHost, st), "d2h u");
-    ck(cudaMemcpyAsync(info, dinfo, sizeof(sddg_solve_info) * n, cudaMemcpyDeviceToHost, st), "d2h");
+    ck(cudaMemcpyAsync(hinfo.data(), dinfo, sizeof(sddg_solve_info) * n, cudaMemcpyDeviceToHost, st), "d2h");
     ck(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, st), "d2h err");
     ck(cudaStreamSynchronize(st), "solver");
+    for (int64_t a = 0; a < n; ++a) info[info_of[a]] = hinfo[a];
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
     c->last_ms = ms;
-    c->last_launches = 1;
+    c->last_launches = launches;
     c->last_steps = 0;
     if (herr == 4) fail(SDDG_ERR_NUMERICAL, "solve_dirichlet: maximum principle violated");
 }
@@ -553,6 +614,30 @@ std::vector<std::vector<int>> plan(const sddg_density& d, const Layout& L, int s
                 nodes.push_back(p);
             }
             if (nodes.empty()) nodes.push_back(n / 2);
+        } else if (strategy == SDDG_PLACE_EQUIDISTRIBUTED) {
+            // BASELINE config 4: grid nodes nearest to equal shares
+            // of the trapezoid integral of w = 1/rho along the line
+            if (k < 1 || k > n - 2)
+                fail(SDDG_ERR_VALIDATION, "plan_interface_points: equidistributed count " +
+                                              std::to_string(k) + " not in [1, " +
+                                              std::to_string(n - 2) + "]");
+            std::vector<double> cum(n, 0.0);
+            double wprev = 0.0;
+            for (int p = 0; p < n; ++p) {
+                const double x = line.vertical ? L.dom.xmin + line.fixed * L.hx() : L.dom.xmin + p * L.hx();
+                const double y = line.vertical ? L.dom.ymin + p * L.hy() : L.dom.ymin + line.fixed * L.hy();
+                const double w = 1.0 / h.rho(x, y);
+                if (p > 0) cum[p] = cum[p - 1] + 0.5 * (wprev + w);
+                wprev = w;
+            }
+            for (int j = 1; j <= k; ++j) {
+                const double target = cum[n - 1] * j / (k + 1);
+                int hi = static_cast<int>(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+                hi = std::min(std::max(hi, 1), n - 1);
+                const int pos = (target - cum[hi - 1] < cum[hi] - target) ? hi - 1 : hi;
+                const int c = std::clamp(pos, 1, n - 2);
+                if (nodes.empty() || nodes.back() != c) nodes.push_back(c);
+            }
         } else {
             fail(SDDG_ERR_VALIDATION, "unknown placement strategy");
         }
@@ -652,8 +737,42 @@ NodeSet interface_nodes(const Layout& L, const std::vector<std::vector<int>>& pl
 
 // Linear fill between known nodes and crossing reconciliation
 // (proj/src/decomposition.cpp:176-246) from per-node estimates in NodeSet order.
+// Natural cubic spline through (xs, ys) evaluated at integer positions
+// between consecutive knots (BASELINE config 4 fill).
+void spline_fill(const std::vector<int>& xs, std::vector<double>& v) {
+    const int m = static_cast<int>(xs.size());
+    if (m < 3) return;  // two knots: the linear fill already in place is the spline
+    std::vector<double> h(m - 1), a(m, 0.0), b(m, 1.0), c(m, 0.0), r(m, 0.0), M(m, 0.0);
+    for (int i = 0; i + 1 < m; ++i) h[i] = xs[i + 1] - xs[i];
+    for (int i = 1; i + 1 < m; ++i) {
+        a[i] = h[i - 1];
+        b[i] = 2.0 * (h[i - 1] + h[i]);
+        c[i] = h[i];
+        r[i] = 6.0 * ((v[xs[i + 1]] - v[xs[i]]) / h[i] - (v[xs[i]] - v[xs[i - 1]]) / h[i - 1]);
+    }
+    // Thomas algorithm with M_0 = M_{m-1} = 0
+    for (int i = 1; i < m; ++i) {
+        const double f = a[i] / b[i - 1];
+        b[i] -= f * c[i - 1];
+        r[i] -= f * r[i - 1];
+    }
+    M[m - 1] = 0.0;
+    for (int i = m - 2; i >= 1; --i) M[i] = (r[i] - c[i] * M[i + 1]) / b[i];
+    M[0] = 0.0;
+    for (int i = 0; i + 1 < m; ++i) {
+        const double y0 = v[xs[i]], y1 = v[xs[i + 1]], hh = h[i];
+        for (int q = xs[i] + 1; q < xs[i + 1]; ++q) {
+            const double t1 = q - xs[i], t0 = xs[i + 1] - q;
+            v[q] = (M[i] * t0 * t0 * t0 + M[i + 1] * t1 * t1 * t1) / (6.0 * hh) +
+                   (y0 / hh - M[i] * hh / 6.0) * t0 + (y1 / hh - M[i + 1] * hh / 6.0) * t1;
+        }
+    }
+}
+
 IfcResult fill_interfaces(const Layout& L, const NodeSet& ns, const sddg_boundary& bd,
-                          const sddg_estimate* est) {
+                          const sddg_estimate* est, int interp = SDDG_INTERP_LINEAR) {
+    if (interp != SDDG_INTERP_LINEAR && interp != SDDG_INTERP_SPLINE)
+        fail(SDDG_ERR_VALIDATION, "unknown interface interpolation");
     IfcResult out;
     out.mc_points = static_cast<int64_t>(ns.px.size());
     for (size_t k = 0; k < ns.px.size(); ++k) {
@@ -695,6 +814,13 @@ IfcResult fill_interfaces(const Layout& L, const NodeSet& ns, const sddg_boundar
             }
             prev = pos;
         }
+        if (interp == SDDG_INTERP_SPLINE) {
+            std::vector<int> knots;
+            for (int pos = 0; pos < n; ++pos)
+                if (known[pos]) knots.push_back(pos);
+            spline_fill(knots, xi);
+            spline_fill(knots, eta);
+        }
         out.xi[l] = std::move(xi);
         out.eta[l] = std::move(eta);
         out.sxi[l] = std::move(sx);
@@ -717,7 +843,7 @@ IfcResult fill_interfaces(const Layout& L, const NodeSet& ns, const sddg_boundar
 // solve_interfaces (proj/src/decomposition.cpp:147-248), walks on the GPU.
 IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
                            const std::vector<std::vector<int>>& pl, const sddg_boundary& bd,
-                           const sddg_walk_config& cfg) {
+                           const sddg_walk_config& cfg, int interp = SDDG_INTERP_LINEAR) {
     const NodeSet ns = interface_nodes(L, pl);
     std::vector<sddg_estimate> est(ns.px.size());
     int64_t steps = 0;
@@ -726,7 +852,7 @@ IfcResult solve_interfaces(sddg_ctx* c, const sddg_density& d, const Layout& L,
                        static_cast<int64_t>(ns.px.size()), est.data());
         steps = c->last_steps;
     }
-    IfcResult out = fill_interfaces(L, ns, bd, est.data());
+    IfcResult out = fill_interfaces(L, ns, bd, est.data(), interp);
     out.path_steps = steps;
     return out;
 }
@@ -974,7 +1100,7 @@ void sddg_destroy(sddg_ctx* c) {
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
                       &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
-                      &c->s_coef, &c->s_err, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
+                      &c->s_coef, &c->s_err, &c->s_large, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1151,13 +1277,14 @@ sddg_status sddg_plan_interface_points(const sddg_density* dens, const sddg_doma
 sddg_status sddg_solve_interfaces(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                                   int32_t nx, int32_t ny, int32_t sx, int32_t sy, int32_t placement,
                                   int32_t k, const sddg_boundary* bd, const sddg_walk_config* cfg,
-                                  double* xi, double* eta, double* sxi, double* seta,
-                                  sddg_sdd_stats* stats) {
+                                  const sddg_sdd_options* opts, double* xi, double* eta,
+                                  double* sxi, double* seta, sddg_sdd_stats* stats) {
     API_BEGIN(ctx)
     const double t0 = now_s();
     const Layout L = build_layout(*dom, nx, ny, sx, sy);
     const auto pl = plan(*dens, L, placement, k);
-    const IfcResult r = solve_interfaces(ctx, *dens, L, pl, *bd, *cfg);
+    const IfcResult r = solve_interfaces(ctx, *dens, L, pl, *bd, *cfg,
+                                         opts ? opts->interp : SDDG_INTERP_LINEAR);
     size_t off = 0;
     for (size_t l = 0; l < r.xi.size(); ++l) {
         const size_t n = r.xi[l].size();
@@ -1192,7 +1319,7 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
     const sddg_boundary bd = make_boundary_view(*dom, nx, ny, tabs);
     const auto pl = plan(*dens, L, placement, k);
     const double t0 = now_s();
-    IfcResult ifc = solve_interfaces(ctx, *dens, L, pl, bd, *cfg);
+    IfcResult ifc = solve_interfaces(ctx, *dens, L, pl, bd, *cfg, opts ? opts->interp : SDDG_INTERP_LINEAR);
     const double t_stoc = ifc.mc_points > 0 ? now_s() - t0 : 0.0;
     // optional interface pre-smoothing (decomposition.cpp:274-282)
     double t_smooth = 0.0;
@@ -1265,14 +1392,15 @@ sddg_status sddg_interface_nodes(const sddg_density* dens, const sddg_domain* do
 sddg_status sddg_fill_interfaces(const sddg_density* dens, const sddg_domain* dom, int32_t nx,
                                  int32_t ny, int32_t sx, int32_t sy, int32_t placement, int32_t k,
                                  const sddg_boundary* bd, const sddg_estimate* est, int64_t n,
-                                 double* xi, double* eta, double* sxi, double* seta) {
+                                 const sddg_sdd_options* opts, double* xi, double* eta, double* sxi,
+                                 double* seta) {
     try {
         const Layout L = build_layout(*dom, nx, ny, sx, sy);
         const NodeSet ns = interface_nodes(L, plan(*dens, L, placement, k));
         if (static_cast<int64_t>(ns.px.size()) != n)
             fail(SDDG_ERR_VALIDATION, "fill_interfaces: estimate count does not match the plan");
         check_boundary(*bd);
-        const IfcResult r = fill_interfaces(L, ns, *bd, est);
+        const IfcResult r = fill_interfaces(L, ns, *bd, est, opts ? opts->interp : SDDG_INTERP_LINEAR);
         size_t off = 0;
         for (size_t l = 0; l < r.xi.size(); ++l) {
             const size_t m = r.xi[l].size();

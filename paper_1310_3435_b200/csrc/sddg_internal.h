@@ -85,6 +85,12 @@ struct SolveJob {
 // else in coef_scratch (n_jobs * 3*max_n doubles).  max_interior <=
 // solver_max_points() for METHOD Jacobi.
 int solver_max_points();
+// K3b: one grid too large for shared memory, cooperative kernel; scratch 5*N+8 doubles
+cudaError_t launch_solve_large(const double* w_global, int gnx, double hx, double hy,
+                               const SolveJob& job, const double* bc, double tol,
+                               int64_t max_iters_cfg, int init_blend, int method, double omega,
+                               double* u_out, sddg_solve_info* info, int* err, double* scratch,
+                               cudaStream_t s, int sms);
 cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
                                int64_t n_jobs, const SolveJob* jobs, const double* bc,
                                double tol, int64_t max_iters_cfg, int init_blend, int method,

@@ -260,3 +260,237 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
 }
 
 }  // namespace sddg
+
+// ---------------------------------------------------------------------------
+// K3b: one large subdomain (or single-domain grid) that does not fit in
+// shared memory: a cooperative persistent kernel over the whole grid with
+// grid-wide barriers between half-sweeps, u / cE / cN / inv_den in global
+// memory (L2-resident for the BASELINE sizes: 513^2 x 4 arrays = 8.4 MB).
+// Same arithmetic, stopping rule and max-principle check as K3.
+#include <cooperative_groups.h>
+
+namespace sddg {
+
+namespace {
+
+__device__ __forceinline__ double grid_max(double v, double* red, unsigned long long* slot) {
+    // block max -> one atomicMax per block on the (non-negative) bit pattern
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = v < u ? u : v;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = red[0];
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) m = m < red[k] ? red[k] : m;
+        atomicMax(slot, static_cast<unsigned long long>(__double_as_longlong(m)));
+    }
+    return 0.0;
+}
+
+template <int METHOD>
+__global__ void __launch_bounds__(256)
+solve_large_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2, SolveJob J,
+                   const double* __restrict__ bc, double tol, int64_t max_iters_cfg, int init_blend,
+                   double omega, double* __restrict__ u, double* __restrict__ v,
+                   double* __restrict__ cE, double* __restrict__ cN, double* __restrict__ inv,
+                   unsigned long long* slots, sddg_solve_info* info, int* err) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[8];
+    const int nx = J.nx, ny = J.ny, N = nx * ny;
+    const double* B = bc + J.bc_off;
+    const double* T = B + nx;
+    const double* L = T + nx;
+    const double* Rt = L + ny;
+    const long long gtid = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long gstride = static_cast<long long>(gridDim.x) * blockDim.x;
+    for (long long c = gtid; c < N; c += gstride) {
+        const int i = static_cast<int>(c % nx), j = static_cast<int>(c / nx);
+        const double wc = wg[(int64_t)(J.j0 + j) * gnx + (J.i0 + i)];
+        cE[c] = i + 1 < nx ? 0.5 * (wc + wg[(int64_t)(J.j0 + j) * gnx + (J.i0 + i + 1)]) : 0.0;
+        cN[c] = j + 1 < ny ? 0.5 * (wc + wg[(int64_t)(J.j0 + j + 1) * gnx + (J.i0 + i)]) : 0.0;
+    }
+    // boundary range via the slots (min stored negated)
+    double lmin = DBL_MAX, lmax = -DBL_MAX;
+    for (long long k = gtid; k < 2 * (nx + ny); k += gstride) {
+        lmin = B[k] < lmin ? B[k] : lmin;
+        lmax = lmax < B[k] ? B[k] : lmax;
+    }
+    grid.sync();
+    for (long long c = gtid; c < N; c += gstride) {
+        const int i = static_cast<int>(c % nx), j = static_cast<int>(c / nx);
+        inv[c] = (i > 0 && j > 0 && i + 1 < nx && j + 1 < ny)
+                     ? 1.0 / ((cE[c] + cE[c - 1]) * ihx2 + (cN[c] + cN[c - nx]) * ihy2)
+                     : 0.0;
+    }
+    // max over a signed range needs an order-preserving key: slots[3] = max(-min), slots[4] = max
+    {
+        double a = -lmin, b = lmax;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ua = __shfl_xor_sync(0xffffffffu, a, o), ub = __shfl_xor_sync(0xffffffffu, b, o);
+            a = a < ua ? ua : a;
+            b = b < ub ? ub : b;
+        }
+        auto key = [](double x) {  // monotone double -> u64
+            const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(x));
+            return (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
+        };
+        if ((threadIdx.x & 31) == 0) {
+            atomicMax(&slots[3], key(a));
+            atomicMax(&slots[4], key(b));
+        }
+    }
+    grid.sync();
+    auto unkey = [](unsigned long long k) {
+        const unsigned long long bits = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+        return __longlong_as_double(static_cast<long long>(bits));
+    };
+    const double bmin = -unkey(slots[3]);
+    const double bmax = unkey(slots[4]);
+    for (long long c = gtid; c < N; c += gstride) {
+        const int i = static_cast<int>(c % nx), j = static_cast<int>(c / nx);
+        double val;
+        if (init_blend) {
+            const double ty = static_cast<double>(j) / (ny - 1);
+            const double tx = static_cast<double>(i) / (nx - 1);
+            const double xb = (1.0 - tx) * L[j] + tx * Rt[j];
+            const double yb = (1.0 - ty) * B[i] + ty * T[i];
+            const double bil = ((1.0 - tx) * (1.0 - ty) * B[0] + tx * ty * T[nx - 1]) +
+                               (tx * (1.0 - ty) * B[nx - 1] + (1.0 - tx) * ty * T[0]);
+            val = xb + yb - bil;
+            val = val < bmin ? bmin : (bmax < val ? bmax : val);
+        } else {
+            val = 0.5 * (bmin + bmax);
+        }
+        if (j == 0) val = B[i];
+        if (j == ny - 1) val = T[i];
+        if (i == 0) val = L[j];
+        if (i == nx - 1) val = Rt[j];
+        u[c] = val;
+        v[c] = val;
+    }
+    grid.sync();
+    const int mi = nx - 2, mj = ny - 2;
+    const int64_t max_iters =
+        max_iters_cfg > 0 ? max_iters_cfg : 200LL * (nx > ny ? nx : ny) * (nx > ny ? nx : ny);
+    int64_t iters = 0;
+    double upd = 0.0, prev = -1.0;
+    bool conv = false;
+    double* cur = u;
+    double* nxt = v;
+    const int half = (mi + 1) / 2;
+    while (iters < max_iters) {
+        ++iters;
+        double lupd = 0.0;
+        if (METHOD == 0) {
+            for (long long p = gtid; p < static_cast<long long>(mi) * mj; p += gstride) {
+                const long long c = (p / mi + 1) * nx + (p % mi + 1);
+                const double xp = (cE[c] * cur[c + 1] + cE[c - 1] * cur[c - 1]) * ihx2;
+                const double yp = (cN[c] * cur[c + nx] + cN[c - nx] * cur[c - nx]) * ihy2;
+                const double nu = (xp + yp) * inv[c];
+                nxt[c] = nu;
+                const double du = fabs(nu - cur[c]);
+                lupd = lupd < du ? du : lupd;
+            }
+        } else {
+            for (int colour = 0; colour < 2; ++colour) {
+                for (long long p = gtid; p < static_cast<long long>(mj) * half; p += gstride) {
+                    const int j = static_cast<int>(p / half) + 1;
+                    const int i = 2 * static_cast<int>(p % half) + 1 + ((j + 1 + colour) & 1);
+                    if (i > mi) continue;
+                    const long long c = static_cast<long long>(j) * nx + i;
+                    const double xp = (cE[c] * cur[c + 1] + cE[c - 1] * cur[c - 1]) * ihx2;
+                    const double yp = (cN[c] * cur[c + nx] + cN[c - nx] * cur[c - nx]) * ihy2;
+                    const double gs = (xp + yp) * inv[c];
+                    const double nv = cur[c] + omega * (gs - cur[c]);
+                    const double du = fabs(nv - cur[c]);
+                    lupd = lupd < du ? du : lupd;
+                    cur[c] = nv;
+                }
+                if (colour == 0) grid.sync();
+            }
+        }
+        const int s = static_cast<int>(iters % 3);
+        grid_max(lupd, red, &slots[s]);
+        grid.sync();
+        upd = __longlong_as_double(static_cast<long long>(slots[s]));
+        if (gtid == 0) slots[(s + 2) % 3] = 0ull;  // next-but-one iteration's slot
+        if (METHOD == 0) {
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
+        }
+        if (upd < tol) {
+            if (upd == 0.0 || upd < 1e-4 * tol) {
+                conv = true;
+                break;
+            }
+            if (prev > 0.0 && upd < prev) {
+                const double rho = upd / prev;
+                if (upd * rho / (1.0 - rho) < tol) {
+                    conv = true;
+                    break;
+                }
+            }
+        }
+        prev = upd;
+    }
+    grid.sync();
+    const double slack = 1e-12 * (1.0 + fabs(bmin) + fabs(bmax));
+    for (long long c = gtid; c < N; c += gstride) {
+        const int i = static_cast<int>(c % nx), j = static_cast<int>(c / nx);
+        const double val = cur[c];
+        if (i > 0 && j > 0 && i + 1 < nx && j + 1 < ny && (val < bmin - slack || val > bmax + slack))
+            atomicCAS(err, 0, 4);
+        u[c] = val;  // result in u (cur may be v after an odd Jacobi count)
+    }
+    if (gtid == 0) {
+        sddg_solve_info r;
+        r.iterations = iters;
+        r.final_update = upd;
+        r.converged = conv ? 1 : 0;
+        r.reserved = 0;
+        *info = r;
+    }
+}
+
+}  // namespace
+
+// Solves one job with the cooperative kernel; scratch holds 5*N doubles + 8 slots.
+cudaError_t launch_solve_large(const double* w_global, int gnx, double hx, double hy,
+                               const SolveJob& job, const double* bc, double tol,
+                               int64_t max_iters_cfg, int init_blend, int method, double omega,
+                               double* u_out, sddg_solve_info* info, int* err, double* scratch,
+                               cudaStream_t s, int sms) {
+    const double ihx2 = 1.0 / (hx * hx);
+    const double ihy2 = 1.0 / (hy * hy);
+    const long long N = static_cast<long long>(job.nx) * job.ny;
+    double* u = scratch;
+    double* v = u + N;
+    double* cE = v + N;
+    double* cN = cE + N;
+    double* inv = cN + N;
+    unsigned long long* slots = reinterpret_cast<unsigned long long*>(inv + N);
+    cudaMemsetAsync(slots, 0, 8 * sizeof(unsigned long long), s);
+    void* fn = method == SDDG_SOLVER_JACOBI ? reinterpret_cast<void*>(solve_large_kernel<0>)
+                                          : reinterpret_cast<void*>(solve_large_kernel<1>);
+    int bps = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fn, 256, 0);
+    if (e != cudaSuccess) return e;
+    const long long need = (N + 255) / 256;
+    int grid = static_cast<int>(std::min<long long>(static_cast<long long>(bps) * sms, std::max<long long>(1, need)));
+    SolveJob J = job;
+    void* args[] = {(void*)&w_global, (void*)&gnx, (void*)&ihx2, (void*)&ihy2, (void*)&J, (void*)&bc,
+                    (void*)&tol, (void*)&max_iters_cfg, (void*)&init_blend, (void*)&omega,
+                    (void*)&u, (void*)&v, (void*)&cE, (void*)&cN, (void*)&inv, (void*)&slots,
+                    (void*)&info, (void*)&err};
+    e = cudaLaunchCooperativeKernel(fn, grid, 256, args, 0, s);
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(u_out + job.u_off, u, sizeof(double) * N, cudaMemcpyDeviceToDevice, s);
+}
+
+}  // namespace sddg

@@ -59,7 +59,8 @@ GRAD_REFERENCE, GRAD_ANALYTIC = 0, 1
 LINEAR, EXPONENTIAL = 0, 1
 FP64, FP32 = 0, 1
 JACOBI, RBSOR = 0, 1
-PLACE = {"all": 0, "equispaced": 1, "optimal": 2}
+PLACE = {"all": 0, "equispaced": 1, "optimal": 2, "equidistributed": 3}
+INTERP = {"linear": 0, "spline": 1}
 BC_REFERENCE, BC_IDENTITY = 0, 1
 
 
@@ -585,7 +586,7 @@ class InterfaceSolution:
 
 
 def solve_interfaces(plan: InterfacePlan, m: MonitorFunction, bd: BoundaryData, cfg: WalkConfig,
-                     layout: SubdomainLayout, ctx=None) -> InterfaceSolution:
+                     layout: SubdomainLayout, ctx=None, interp: str = "linear") -> InterfaceSolution:
     """sdd::solve_interfaces (proj/include/sdd/decomposition.hpp:70-72).
 
     The plan must come from plan_interface_points on the same layout (the
@@ -597,9 +598,10 @@ def solve_interfaces(plan: InterfacePlan, m: MonitorFunction, bd: BoundaryData, 
     xi, eta, sx, se = (np.zeros(tot) for _ in range(4))
     st = _SddStats()
     d, dom, b, c = m.c(), g.domain.c(), bd.c(), cfg.c()
+    o = SddOptions(interp=interp).c()
     _check(lib().sddg_solve_interfaces(ctx.handle, C.byref(d), C.byref(dom), g.nx, g.ny,
                                        layout.n_sub_x, layout.n_sub_y, PLACE.get(plan.strategy, 99),
-                                       int(plan.k), C.byref(b), C.byref(c), _dp(xi), _dp(eta),
+                                       int(plan.k), C.byref(b), C.byref(c), C.byref(o), _dp(xi), _dp(eta),
                                        _dp(sx), _dp(se), C.byref(st)), ctx.handle)
     split = lambda a: [a[o:o + n].copy() for o, n in zip(np.cumsum([0] + lens[:-1]), lens)]
     return InterfaceSolution(split(xi), split(eta), split(sx), split(se), st.mc_points,
@@ -622,14 +624,21 @@ class SddResult:
 
 
 class _SddOptions(C.Structure):
-    _fields_ = [("smooth_interface", C.c_int32), ("smooth_span", C.c_int32)]
+    _fields_ = [("smooth_interface", C.c_int32), ("smooth_span", C.c_int32), ("interp", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 @dataclass
 class SddOptions:
-    """sdd::SddOptions (proj/include/sdd/decomposition.hpp:74-77)."""
+    """sdd::SddOptions (proj/include/sdd/decomposition.hpp:74-77) + the
+    interface fill ("linear" = reference, "spline" = BASELINE config 4)."""
     smooth_interface: bool = False
     smooth_span: int = 5
+    interp: str = "linear"
+
+    def c(self):
+        return _SddOptions(1 if self.smooth_interface else 0, int(self.smooth_span),
+                           INTERP.get(self.interp, 99), 0)
 
 
 def solve_sdd(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan, wcfg: WalkConfig,
@@ -641,7 +650,7 @@ def solve_sdd(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan, 
     xi, eta = np.zeros(g.nx * g.ny), np.zeros(g.nx * g.ny)
     st = _SddStats()
     d, dom, c, sc = m.c(), g.domain.c(), wcfg.c(), scfg.c()
-    o = _SddOptions(1 if (opts and opts.smooth_interface) else 0, opts.smooth_span if opts else 5)
+    o = (opts or SddOptions()).c()
     _check(lib().sddg_solve_sdd(ctx.handle, C.byref(d), C.byref(dom), g.nx, g.ny, layout.n_sub_x,
                                 layout.n_sub_y, PLACE.get(plan.strategy, 99), int(plan.k),
                                 int(bc_mode), C.byref(c), C.byref(sc), C.byref(o), _dp(xi), _dp(eta),
@@ -669,7 +678,7 @@ def interface_nodes(m: MonitorFunction, layout: SubdomainLayout, plan: Interface
 
 
 def fill_interfaces(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan,
-                    bd: BoundaryData, est: np.ndarray) -> InterfaceSolution:
+                    bd: BoundaryData, est: np.ndarray, interp: str = "linear") -> InterfaceSolution:
     """Interface lines from per-node estimates (sddg_fill_interfaces)."""
     g = layout.global_
     lens = [ln.length for ln in layout.lines]
@@ -680,7 +689,8 @@ def fill_interfaces(m: MonitorFunction, layout: SubdomainLayout, plan: Interface
     _check(lib().sddg_fill_interfaces(C.byref(d), C.byref(dom), g.nx, g.ny, layout.n_sub_x,
                                       layout.n_sub_y, PLACE.get(plan.strategy, 99), int(plan.k),
                                       C.byref(b), est.ctypes.data_as(C.c_void_p),
-                                      C.c_int64(len(est)), _dp(xi), _dp(eta), _dp(sx), _dp(se)))
+                                      C.c_int64(len(est)), C.byref(SddOptions(interp=interp).c()),
+                                      _dp(xi), _dp(eta), _dp(sx), _dp(se)))
     split = lambda a: [a[o:o + n].copy() for o, n in zip(np.cumsum([0] + lens[:-1]), lens)]
     return InterfaceSolution(split(xi), split(eta), split(sx), split(se), len(est),
                              int(est["restarts"].sum()), int(est["warn"].sum()), 0)
@@ -838,3 +848,13 @@ def write_mesh(mesh: PhysicalMesh, xi, eta, spec: GridSpec, path: str):
     x, y, a, b = _f64(mesh.x), _f64(mesh.y), _f64(xi), _f64(eta)
     _check(lib().sddg_write_mesh(_dp(x), _dp(y), mesh.m_xi, mesh.m_eta, _dp(a), _dp(b), spec.nx,
                                  spec.ny, path.encode()))
+
+
+def laplacian_smooth(xi, eta, spec: GridSpec, sweeps: int, ctx=None):
+    """BASELINE config 4's "Laplacian smoothing, N sweeps" as the reference
+    maps it: Perona-Malik FTCS with c = 1 (k huge) and
+    dt = hx*hy/4, i.e. the 4-neighbour average for hx = hy."""
+    dt = spec.hx() * spec.hy() / 4.0
+    xi2, eta2, _ = perona_malik(xi, eta, spec, SmoothConfig(k=1e150, dt=dt, steps=sweeps, scope="global"),
+                                ctx=ctx)
+    return xi2, eta2

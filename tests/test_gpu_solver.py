@@ -171,3 +171,61 @@ def test_config3_batch_rbsor_against_reference_jacobi_sample(oracle, ctx):
         wl = w.reshape(g, g)[j0:j0 + ny, i0:i0 + nx].ravel()
         u_ref, *_ = oracle.solve_dirichlet(wl, nx, ny, 1 / 1024, 1 / 1024, *bcs[k].arrays(), tol=1e-13)
         assert np.max(np.abs(res[k].values - u_ref)) <= 1e-10
+
+
+def test_large_grid_path_jacobi_bit_identical(golden, oracle, ctx, monkeypatch):
+    # K3b (cooperative, global memory) runs the same reference iteration
+    monkeypatch.setenv("SDDG_FORCE_LARGE_SOLVER", "1")
+    for name in ("ring17_t10", "running33x17_t8", "ring33_maxit"):
+        kind, nx, ny, tol, mi, blend = SOLVES[name]
+        w = golden[f"solve_{name}_w"]
+        r = sdd.solve_dirichlet(w, nx, ny, 1.0 / (nx - 1), 1.0 / (ny - 1), _bc(oracle, kind, nx, ny, "xi"),
+                                sdd.SolverConfig(tol=tol, max_iters=mi, init_blend=blend), ctx=ctx)
+        info = golden[f"solve_{name}_xi_info"]
+        assert np.array_equal(r.values, golden[f"solve_{name}_xi_u"])
+        assert r.iterations == int(info[0]) and r.converged == bool(info[2])
+
+
+def test_large_grid_rbsor_against_sparse_direct(oracle, ctx):
+    # a 257^2 single-domain solve (does not fit shared memory) vs scipy spsolve
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    n = 257
+    w = oracle.weight_values(B.density(B.TWOBUMP_W), UNIT, n, n)
+    bc = _bc(oracle, B.TWOBUMP_W, n, n, "xi")
+    r = sdd.solve_dirichlet(w, n, n, 1 / (n - 1), 1 / (n - 1), bc, sdd.SolverConfig(tol=1e-13, method="rbsor"),
+                            ctx=ctx)
+    assert r.converged
+    h2 = (1 / (n - 1)) ** 2
+    W = w.reshape(n, n)
+    U = np.zeros((n, n))
+    U[0, :], U[-1, :], U[:, 0], U[:, -1] = bc.bottom, bc.top, bc.left, bc.right
+    m = n - 2
+    idx = lambda i, j: (j - 1) * m + (i - 1)
+    rows, cols, vals, rhs = [], [], [], np.zeros(m * m)
+    for j in range(1, n - 1):
+        for i in range(1, n - 1):
+            k = idx(i, j)
+            cs = {(i + 1, j): 0.5 * (W[j, i] + W[j, i + 1]), (i - 1, j): 0.5 * (W[j, i] + W[j, i - 1]),
+                  (i, j + 1): 0.5 * (W[j, i] + W[j + 1, i]), (i, j - 1): 0.5 * (W[j, i] + W[j - 1, i])}
+            rows.append(k); cols.append(k); vals.append(sum(cs.values()) / h2)
+            for (ii, jj), c in cs.items():
+                if ii in (0, n - 1) or jj in (0, n - 1):
+                    rhs[k] += c / h2 * U[jj, ii]
+                else:
+                    rows.append(k); cols.append(idx(ii, jj)); vals.append(-c / h2)
+    A = sp.csr_matrix((vals, (rows, cols)), shape=(m * m, m * m))
+    U[1:-1, 1:-1] = spla.spsolve(A, rhs).reshape(m, m)
+    assert np.max(np.abs(r.values - U.ravel())) <= 1e-10
+
+
+def test_single_domain_513_config4_reference_solve(oracle, ctx):
+    # config 4's single-domain comparison grid (513^2) goes through K3b
+    n = 513
+    w = oracle.weight_values(B.density(B.TWOBUMP_W), UNIT, n, n)
+    res = sdd.solve_dirichlet_batch(w, n, n, 1 / 512, 1 / 512, [(0, 0, n, n)] * 2,
+                                    [_bc(oracle, B.TWOBUMP_W, n, n, "xi"), _bc(oracle, B.TWOBUMP_W, n, n, "eta")],
+                                    sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx)
+    assert all(r.converged for r in res)
+    X = res[0].values.reshape(n, n)
+    assert (np.diff(X, axis=1) > 0).all()   # xi strictly increasing in x (max principle per row)
