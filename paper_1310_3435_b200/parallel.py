@@ -79,7 +79,7 @@ def all_gather_rows(local: np.ndarray, indices: np.ndarray, n_total: int, row_by
     return out
 
 
-def solve_interfaces_distributed(plan, m, bd, cfg, layout, estimator=None, ctx=None):
+def solve_interfaces_distributed(plan, m, bd, cfg, layout, estimator=None, ctx=None, interp="linear"):
     """solve_interfaces over all ranks.  estimator(px, py, pid) -> records
     (sdd.ESTIMATE_DTYPE); default: this rank's GPU through the C-ABI."""
     rank, world = dist.get_rank(), dist.get_world_size()
@@ -92,7 +92,7 @@ def solve_interfaces_distributed(plan, m, bd, cfg, layout, estimator=None, ctx=N
     local = estimator(px[mine], py[mine], pid[mine]) if len(mine) else np.zeros(0, sdd.ESTIMATE_DTYPE)
     rows = all_gather_rows(local, mine, len(px), sdd.ESTIMATE_DTYPE.itemsize)
     est = rows.view(sdd.ESTIMATE_DTYPE).reshape(-1)
-    return sdd.fill_interfaces(m, layout, plan, bd, est), est
+    return sdd.fill_interfaces(m, layout, plan, bd, est, interp=interp), est
 
 
 def subdomain_range(n_sub: int, world: int, rank: int):
@@ -101,11 +101,11 @@ def subdomain_range(n_sub: int, world: int, rank: int):
 
 
 def solve_sdd_distributed(m, layout, plan, wcfg, scfg, bc_mode=sdd.BC_REFERENCE, estimator=None,
-                          solver=None, ctx=None):
+                          solver=None, ctx=None, interp="linear"):
     """solve_sdd over all ranks; every rank returns the assembled (xi, eta)."""
     rank, world = dist.get_rank(), dist.get_world_size()
     bd = sdd.make_boundary_data(m, layout.global_, bc_mode)
-    ifc, est = solve_interfaces_distributed(plan, m, bd, wcfg, layout, estimator, ctx)
+    ifc, est = solve_interfaces_distributed(plan, m, bd, wcfg, layout, estimator, ctx, interp)
     n_sub = layout.subdomain_count()
     lo, hi = subdomain_range(n_sub, world, rank)
     if solver is None:

@@ -80,6 +80,34 @@ for prec in ("fp64", "fp32"):
         out[f"config5_{prec}_{walks}"] = walk_rate(sdd.MonitorFunction.ring(analytic=True), p5, pid5, bd5, cfg,
                                                    reps=1)
 
+# ---- config 4 end to end: 513^2, 4x4, two-bump, 32 integral-w-equidistributed nodes per
+# line, 2e5 paths, dt 1e-5 fp64, spline fill, Laplacian smoothing (5 sweeps), quality
+# against the single-domain solve -- all on the GPU
+import time as _t
+m4 = sdd.MonitorFunction.two_bump(analytic=True)
+spec4 = sdd.GridSpec(UNIT, 513, 513)
+lay4 = sdd.build_layout(spec4, 4, 4)
+plan4 = sdd.plan_interface_points("equidistributed", 32, m4, lay4)
+t0 = _t.perf_counter()
+r4 = sdd.solve_sdd(m4, lay4, plan4, sdd.WalkConfig(scheme="linear", dt=1e-5, walks=200_000, seed=1),
+                   sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx, opts=sdd.SddOptions(interp="spline"))
+t_sdd = _t.perf_counter() - t0
+t0 = _t.perf_counter()
+xs, es = sdd.laplacian_smooth(r4.xi, r4.eta, spec4, 5, ctx=ctx)
+t_smooth = _t.perf_counter() - t0
+mesh4 = sdd.invert_mesh(xs, es, spec4, 513, 513, ctx=ctx)
+t0 = _t.perf_counter()
+lay1 = sdd.build_layout(spec4, 1, 1)
+single = sdd.solve_sdd(m4, lay1, sdd.plan_interface_points("all", 0, m4, lay1), sdd.WalkConfig(walks=1),
+                       sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx)
+t_1 = _t.perf_counter() - t0
+ref4 = sdd.invert_mesh(single.xi, single.eta, spec4, 513, 513, ctx=ctx)
+q4 = sdd.quality_report(mesh4, ref4, m4.with_grad(sdd.GRAD_REFERENCE), ctx=ctx)
+out["config4_end_to_end"] = {"mc_points": r4.mc_points, "path_steps": r4.path_steps, "t_stoc_s": r4.t_stoc,
+                             "t_sub_s": r4.t_sub, "t_solve_sdd_wall_s": t_sdd, "t_laplacian_s": t_smooth,
+                             "t_single_domain_513_s": t_1, "q_max": q4.q_max, "q_mean": q4.q_mean,
+                             "r_max": q4.r_max, "r_mean": q4.r_mean, "l_inf": q4.l_inf}
+
 # ---- K3 subdomain solver batches
 def solver_batch(g, subs_n, tol, method, n_jobs=None):
     m = sdd.MonitorFunction.shock()

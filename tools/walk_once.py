@@ -1,0 +1,33 @@
+"""Run one walk batch of a BASELINE config (for ncu captures):
+python tools/walk_once.py {config2|config3|config5} {fp64|fp32} WALKS"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1310_3435_b200 import sdd  # noqa: E402
+
+cfgname, prec, walks = sys.argv[1], sys.argv[2], int(sys.argv[3])
+ctx = sdd.Context(0)
+UNIT = sdd.RectDomain(0, 1, 0, 1)
+if cfgname == "config3":
+    m, grid, subs, dt = sdd.MonitorFunction.shock(analytic=True), 1025, 8, 1e-5
+elif cfgname == "config2":
+    m, grid, subs, dt = sdd.MonitorFunction.ring(analytic=True), 129, 4, 2e-5
+else:
+    m, grid, subs, dt = sdd.MonitorFunction.ring(analytic=True), 129, 4, 1e-5
+spec = sdd.GridSpec(UNIT, grid, grid)
+bd = sdd.make_boundary_data(m, spec)
+if cfgname == "config5":
+    pts = np.clip(np.random.default_rng(1).uniform(0, 1, (4096, 2)), 1e-9, 1 - 1e-9)
+    pid = np.arange(4096, dtype=np.uint64)
+else:
+    lay = sdd.build_layout(spec, subs, subs)
+    px, py, pid = sdd.interface_nodes(m, lay, sdd.plan_interface_points("all", 0, m, lay))
+    pts = np.stack([px, py], 1)
+cfg = sdd.WalkConfig(scheme="linear", dt=dt, walks=walks, seed=1, precision=prec)
+for _ in range(2):
+    sdd.mc_estimate_batch(pts, pid, m, UNIT, bd, cfg, ctx=ctx)
+    st = ctx.last_stats()
+    print(f"{cfgname} {prec} walks={walks}: {st['path_steps'] / (st['kernel_ms'] / 1e3):.4e} path-steps/s")
