@@ -65,22 +65,37 @@ struct RealOps<double, FAST> {
     __device__ static __forceinline__ double sq(double v) { return sqrt(v); }
 };
 
+// fp32 walks (config 3): SFU intrinsics.  ln u1 near 1 goes through a short
+// log1p series in d = 1 - u1 (exact on the 24-bit grid of u01_open_f), so the
+// radius keeps its relative accuracy where MUFU.LG2 is only absolutely accurate.
 template <bool FAST>
 struct RealOps<float, FAST> {
     __device__ static __forceinline__ float u(uint64_t u) { return u01_f(u); }
     __device__ static __forceinline__ float u_open(uint64_t u) { return u01_open_f(u); }
+    __device__ static __forceinline__ float ln_open(uint64_t a) {
+        const uint32_t k = static_cast<uint32_t>(a >> 40);          // u1 = (k + 1/2) 2^-24
+        const float u1 = __fmaf_rn(static_cast<float>(k), 0x1.0p-24f, 0x1.0p-25f);
+        const float d = __fmaf_rn(static_cast<float>(0xFFFFFFu - k), 0x1.0p-24f, 0x1.0p-25f);  // 1 - u1
+        // -ln(1-d) = d + d^2/2 + ... + d^6/6 for d <= 1/16 (next term < 1e-8 relative)
+        float p = __fmaf_rn(d, 0.16666667f, 0.2f);
+        p = __fmaf_rn(p, d, 0.25f);
+        p = __fmaf_rn(p, d, 0.33333334f);
+        p = __fmaf_rn(p, d, 0.5f);
+        p = __fmaf_rn(p, d, 1.0f);
+        const float series = -(p * d);
+        return d <= 0.0625f ? series : __logf(u1);
+    }
     __device__ static __forceinline__ void box_muller(const fm::FmTables&, uint64_t a, uint64_t b,
                                                       float& z0, float& z1) {
-        const float u1 = u01_open_f(a);
-        const float u2 = u01_f(b);
-        const float r = sqrtf(-2.0f * logf(u1));
+        const float v = -2.0f * ln_open(a);
+        const float r = v * rsqrtf(v);
         float s, c;
-        sincospif(2.0f * u2, &s, &c);
+        __sincosf(6.2831853f * u01_f(b), &s, &c);
         z0 = r * c;
         z1 = r * s;
     }
     __device__ static __forceinline__ float ex(const fm::FmTables&, float v) { return __expf(v); }
-    __device__ static __forceinline__ float lg(const fm::FmTables&, float v) { return logf(v); }
+    __device__ static __forceinline__ float lg(const fm::FmTables&, float v) { return __logf(v); }
     __device__ static __forceinline__ float sq(float v) { return sqrtf(v); }
 };
 
