@@ -116,6 +116,21 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+def ncu_summary():
+    """Pipe / issue utilisation of K1 from the committed ncu capture
+    (profiles/ncu_walk_summary.json; measured with ncu, not in this run)."""
+    path = os.path.join(ROOT, "profiles", "ncu_walk_summary.json")
+    try:
+        d = json.load(open(path))["fp64_config2"]
+        m = d["metrics"]
+        return {"source": "profiles/ncu_walk_summary.json (" + d["command"] + ")",
+                "issue_slots_busy_pct": float(m["sm__inst_issued.avg.pct_of_peak_sustained_active"]["value"]),
+                "fp64_pipe_pct": float(m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]["value"]),
+                "instructions_per_path_step": d["instructions_per_path_step"]}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def cpu_reference_sample(ref, B, threads, walks=CPU_SAMPLE_WALKS, seed=1):
     """The reference's mc_estimate (FD ring drift -- its only route for a
     user density) over the fixed node subsample; returns (path-steps, seconds)."""
@@ -362,7 +377,8 @@ def main():
                          "path_steps_per_launch": steps_per_launch,
                          "peak_source": "measured on this GPU by sddg_probe_fma_peak (independent "
                                         "FMA chains; MEASURED_PEAKS.json has no non-tensor peak)",
-                         "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64},
+                         "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64,
+                         "ncu": ncu_summary()},
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,
