@@ -4,9 +4,9 @@ Workload (BASELINE.json configs[1], the config the metric is quoted on):
 unit square, 129x129 global grid split 4x4, every interior node of the six
 interface lines (753 unique Monte Carlo nodes), ring density w with the
 analytic drift grad(w)/w, Euler-Maruyama dt = 2e-5 with the reference's
-Brownian-bridge exit test, fp64.  One bench step = the walk phase of
-solve_interfaces over all 753 nodes at 10^4 paths per node (a tenth of the
-config's 10^5; the seed changes every step), i.e. ~6e10 path-steps.
+Brownian-bridge exit test, fp64.  One bench step = the whole walk phase of
+config 2's solve_interfaces: all 753 nodes at the config's 10^5 paths per node
+(~6.2e11 path-steps; the seed changes every step).
 
   value  : path-steps/s, device-resident inputs (sddg_mc_estimate_batch_device),
            CUDA events on the launching stream, max over ranks, L2 flushed
@@ -42,7 +42,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-GRID, SUBS, DT, WALKS_PER_STEP, CONFIG_WALKS = 129, 4, 2e-5, 10_000, 100_000
+GRID, SUBS, DT, WALKS_PER_STEP, CONFIG_WALKS = 129, 4, 2e-5, 100_000, 100_000
 # naive census of FP64 operations per interior path-step (transcendental = 1),
 # SURVEY.md 8(d) / DESIGN.md "Roofline"
 DP_FLOPS_PER_STEP = 57
@@ -200,7 +200,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
@@ -219,10 +219,15 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    backend = os.environ.get("SDDG_BENCH_BACKEND", "nccl")  # gloo: multi-rank path check on 1 GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    cdev = "cuda" if backend == "nccl" else "cpu"  # device of the collective tensors
     ctx = sdd.Context(local)
     stream = torch.cuda.current_stream()
 
@@ -275,7 +280,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([elapsed_ms, float(total_steps), k1_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([elapsed_ms, float(total_steps), k1_ms], dtype=torch.float64, device=cdev)
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -303,7 +308,7 @@ def main():
                                   cfg_for(args.warmup + k), ctx=ctx)
             e_sec += time.perf_counter() - t0
             e_steps += ctx.last_stats()["path_steps"]
-        et = torch.tensor([e_sec, float(e_steps)], dtype=torch.float64, device="cuda")
+        et = torch.tensor([e_sec, float(e_steps)], dtype=torch.float64, device=cdev)
         if world > 1:
             emax = et.clone()
             dist.all_reduce(emax, op=dist.ReduceOp.MAX)
@@ -361,9 +366,9 @@ def main():
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic",
-            "config": {"workload": "BASELINE config 2 walk phase: 129^2 grid, 4x4 subdomains, all 753 "
-                                   "interface nodes, ring density (analytic grad w / w), linear EM "
-                                   "dt=2e-5 + bridge exit test",
+            "config": {"workload": "BASELINE config 2 walk phase (one step = the full config): 129^2 "
+                                   "grid, 4x4 subdomains, all 753 interface nodes x 1e5 paths, ring "
+                                   "density (analytic grad w / w), linear EM dt=2e-5 + bridge exit test",
                        "paths_per_node_per_step": args.walks, "config_paths_per_node": CONFIG_WALKS,
                        "nodes_per_rank": n, "drift": args.drift, "precision": args.precision,
                        "l2": "flushed (256 MiB write) before every timed step",
