@@ -290,3 +290,29 @@ def test_fastmath_accuracy(ctx):
     assert exp_u <= 4 and log_u <= 4 and sc_u <= 4 and sqrt_u <= 2 and rcp_u <= 2, list(m)
     print("fastmath max ulp (exp, log, sincos, sqrt, rcp, log near 1):", list(m))
     assert log_abs_near1 <= 4096, list(m)  # cancellation near u = 1: <= 1e-12 relative
+
+
+def test_config3_fp32_vs_fp64_exceedances_against_null(ctx):
+    # at config 3's 14,273 nodes x 2 fields, count |z| > 4 between
+    # independent fp32 and fp64 estimates against the H0 expectation
+    # (2 * 14273 * 6.3e-5 = 1.8) and check the aggregate chi^2 / dof
+    m = sdd.MonitorFunction.shock(analytic=True)
+    spec = sdd.GridSpec(UNIT, 1025, 1025)
+    bd = sdd.make_boundary_data(m, spec)
+    lay = sdd.build_layout(spec, 8, 8)
+    px, py, pid = sdd.interface_nodes(m, lay, sdd.plan_interface_points("all", 0, m, lay))
+    pts = np.stack([px, py], 1)
+    a = sdd.mc_estimate_batch(pts, pid, m, UNIT, bd,
+                              sdd.WalkConfig(scheme="linear", dt=1e-5, walks=256, seed=101), ctx=ctx)
+    b = sdd.mc_estimate_batch(pts, pid, m, UNIT, bd,
+                              sdd.WalkConfig(scheme="linear", dt=1e-5, walks=256, seed=202, precision="fp32"),
+                              ctx=ctx)
+    z = []
+    for f, s in (("xi", "se_xi"), ("eta", "se_eta")):
+        se = np.hypot(a[s], b[s])
+        ok = se > 0
+        z.append((a[f][ok] - b[f][ok]) / se[ok])
+    z = np.concatenate(z)
+    assert len(z) > 20000
+    assert np.sum(np.abs(z) > 4) <= 10
+    assert 0.9 <= np.mean(z ** 2) <= 1.1
