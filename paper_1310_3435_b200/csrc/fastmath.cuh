@@ -177,10 +177,22 @@ enum FmK {
     K_S7, K_S5, K_S3, K_C6,                // -1/5040, 1/120, -1/6, -1/720
     K_C4, K_PAD1, K_PAD2, K_PAD3           // 1/24
 };
-#ifdef SDDG_FM_IMMEDIATES
+// Constants: SDDG_FM_IMMEDIATES -> 64-bit immediates (ptxas rematerialises
+// them with UMOV pairs in the loop); SDDG_FM_LDS_HOISTED -> plain smem reads
+// (ptxas hoists and spills them); default -> one ld.shared per use.
+__device__ __forceinline__ double lds_f64(const double* p) {
+    double r;
+    asm volatile("ld.shared.f64 %0, [%1];"
+                 : "=d"(r)
+                 : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+    return r;
+}
+#if defined(SDDG_FM_IMMEDIATES)
 #define FMK(i, v) (v)
-#else
+#elif defined(SDDG_FM_LDS_HOISTED)
 #define FMK(i, v) (T.k[i])
+#else
+#define FMK(i, v) (lds_f64(&T.k[i]))  // default: A/B best (+3.6% vs immediates)
 #endif
 
 constexpr double k64Ln2 = 92.33248261689366;       // 64 / ln 2
