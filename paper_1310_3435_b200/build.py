@@ -36,7 +36,7 @@ UNITS = {
     "probe.cu": [],
     "runtime.cu": [],
 }
-HEADERS = ["density.cuh", "philox.cuh", "walk_kernel.cuh", "sddg_internal.h", "host_density.h"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
 
 def _mtime(p):
