@@ -7,6 +7,6 @@ timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.log 2>&
 if [ "${NCU:-1}" = 1 ]; then
 timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain_$TAG.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launch rc=$?"
-timeout 300 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain2_$TAG.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_kernel -s 1 -c 1 -o gpurun_out/walk_full_$TAG python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
+timeout 300 python bench.py --steps 1 --warmup 1 --walks 10000 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain2_$TAG.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_kernel -s 1 -c 1 -o gpurun_out/walk_full_$TAG python bench.py --steps 1 --warmup 1 --walks 10000 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 fi
