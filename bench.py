@@ -126,9 +126,17 @@ def ncu_summary():
         return {"source": "profiles/ncu_walk_summary.json (" + d["command"] + ")",
                 "issue_slots_busy_pct": float(m["sm__inst_issued.avg.pct_of_peak_sustained_active"]["value"]),
                 "fp64_pipe_pct": float(m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]["value"]),
-                "instructions_per_path_step": d["instructions_per_path_step"]}
+                "instructions_per_path_step": d["instructions_per_path_step"],
+                "dram_bytes_per_walk": d.get("dram_bytes_per_walk")}
     except (OSError, KeyError, ValueError):
         return None
+
+
+def traffic_per_launch(walks):
+    s = ncu_summary()
+    if not s or not s.get("dram_bytes_per_walk"):
+        return None
+    return s["dram_bytes_per_walk"] * walks
 
 
 def cpu_reference_sample(ref, B, threads, walks=CPU_SAMPLE_WALKS, seed=1):
@@ -375,7 +383,11 @@ def main():
                        "parallelism": f"weak x{world} (independent node batches per rank)"},
             "roofline": {"bound": "fp64" if args.precision == "fp64" else "fp32",
                          "achieved": achieved, "peak": prec_peak, "unit": "TFLOP/s",
-                         "frac": achieved / prec_peak if prec_peak else None, "traffic": None,
+                         "frac": achieved / prec_peak if prec_peak else None,
+                         "traffic": traffic_per_launch(n * args.walks),
+                         "traffic_note": "DRAM read+write bytes per launch = ncu dram__bytes per walk "
+                                         "(profiles/ncu_walk_summary.json) x walks in this launch; "
+                                         "algorithmic: 20 B per walk record",
                          "kernel": "walk_kernel (K1)",
                          "algorithmic_flops_per_path_step": DP_FLOPS_PER_STEP,
                          "k1_ms_per_launch": k1_avg_s * 1e3,
