@@ -172,6 +172,32 @@ sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* den
                                           const double* d_py, const uint64_t* d_point_id,
                                           int64_t n, sddg_estimate* d_out, void* stream);
 
+/* ------------------------------------------------ fused multi-GPU gather
+ * The one collective of the sharded path (an all-gather of the per-node
+ * records) fused into the finalize kernel K2: each rank opens every other
+ * rank's gather buffer through CUDA IPC (NVLink peer memory on one box) and
+ * K2 stores each finished record into all of them; a host barrier after the
+ * call completes the exchange.  Replaces the NCCL all-gather of
+ * paper_1310_3435_b200/parallel.py (transport="nccl"). */
+typedef struct {
+    unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} sddg_ipc_handle;
+sddg_status sddg_gather_alloc(sddg_ctx* ctx, int64_t n_records, void** d_buf,
+                              sddg_ipc_handle* handle);
+sddg_status sddg_gather_open(sddg_ctx* ctx, const sddg_ipc_handle* handle, void** d_peer);
+sddg_status sddg_gather_close(sddg_ctx* ctx, void* d_peer);
+sddg_status sddg_gather_free(sddg_ctx* ctx, void* d_buf);
+sddg_status sddg_gather_read(sddg_ctx* ctx, const void* d_buf, int64_t n_records,
+                             sddg_estimate* out);
+/* sddg_mc_estimate_batch for this rank's n nodes, whose records land at
+ * slot global_index[k] of each of the n_peers gather buffers (own buffer
+ * included; n_total slots each).  Returns after the stores complete. */
+sddg_status sddg_mc_estimate_gather(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                    const sddg_boundary* bd, const sddg_walk_config* cfg,
+                                    const double* px, const double* py, const uint64_t* point_id,
+                                    const int64_t* global_index, int64_t n, void* const* peer_bufs,
+                                    int32_t n_peers, int64_t n_total);
+
 /* Per-path results of walks [walk_lo, walk_lo+n) at one start point: the
  * parity view of run_walk (proj/src/sde.cpp:151-183). */
 sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,

@@ -16,7 +16,7 @@ constexpr int kReduceThreads = 256;
 __global__ void __launch_bounds__(kReduceThreads)
 reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
               const uint32_t* __restrict__ meta, int64_t walks, const uint32_t* __restrict__ perm,
-              sddg_estimate* out) {
+              sddg_estimate* out, const GatherTargets gt) {
     __shared__ double part[4][kReduceThreads];
     __shared__ unsigned long long icnt[5][kReduceThreads / 32];
     const int64_t node = blockIdx.x;
@@ -100,16 +100,24 @@ reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
         e.sum_ff = tff;
         e.sum_gg = tgg;
         e.path_steps = 0;  // filled by the host from the kernel counter
-        out[perm ? perm[node] : node] = e;
+        const uint32_t k = perm ? perm[node] : static_cast<uint32_t>(node);
+        out[k] = e;
+        // fused all-gather: store the finished record straight into every
+        // rank's gather buffer (NVLink peer memory opened through CUDA IPC)
+        if (gt.n_peers > 0) {
+            const int64_t slot = gt.global_index[k];
+#pragma unroll 1
+            for (int p = 0; p < gt.n_peers; ++p) gt.peers[p][slot] = e;
+        }
     }
 }
 
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
                           int64_t walks, int64_t n_nodes, const uint32_t* perm, sddg_estimate* out,
-                          cudaStream_t s) {
+                          cudaStream_t s, const GatherTargets& gt) {
     if (n_nodes <= 0) return cudaSuccess;
     reduce_kernel<<<static_cast<unsigned>(n_nodes), kReduceThreads, 0, s>>>(rf, rg, meta, walks, perm,
-                                                                            out);
+                                                                            out, gt);
     return cudaGetLastError();
 }
 

@@ -93,6 +93,7 @@ struct sddg_ctx {
     std::map<int, int> occ;  // (dv*2+prec) -> blocks per SM
     std::vector<cudaEvent_t> bev;  // per-batch walk-kernel events
     DevBuf fm_tables;              // fastmath.cuh FmTables (performance mode)
+    DevBuf gidx;                   // fused-gather global indices
 };
 
 namespace {
@@ -284,7 +285,11 @@ void raise_kernel_error(const Counters& hc) {
 void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
                    const sddg_boundary& bd, const sddg_walk_config& cfg, const double* d_px,
                    const double* d_py, const uint64_t* d_pid, int64_t n, sddg_estimate* d_out,
-                   cudaStream_t st, const double* hpx, const double* hpy) {
+                   cudaStream_t st, const double* hpx, const double* hpy,
+                   const GatherTargets* gt = nullptr) {
+    GatherTargets none;
+    none.n_peers = 0;
+    none.global_index = nullptr;
     const int dv = drift_variant(d, cfg.precision);
     const double* dtab = upload_tables(c, bd);
     const std::vector<uint32_t> perm = lpt_order(dom, hpx, hpy, n);
@@ -332,7 +337,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         ck(cudaEventRecord(c->bev[2 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
         ck(cudaEventRecord(c->bev[2 * bi + 1], st), "event");
-        ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, d_out, st), "reduce launch");
+        ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, d_out, st, gt ? *gt : none), "reduce launch");
         launches += 3;
     }
     Counters hc;
@@ -358,7 +363,8 @@ void check_points(const sddg_domain& dom, const double* px, const double* py, in
 
 void estimates_host(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
                     const sddg_boundary& bd, const sddg_walk_config& cfg, const double* px,
-                    const double* py, const uint64_t* pid, int64_t n, sddg_estimate* out) {
+                    const double* py, const uint64_t* pid, int64_t n, sddg_estimate* out,
+                    const GatherTargets* gt = nullptr) {
     validate_walk(cfg);
     check_domain(dom);
     check_boundary(bd);
@@ -374,7 +380,7 @@ void estimates_host(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     ck(cudaMemcpyAsync(dpy, py, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
     ck(cudaMemcpyAsync(dpid, pid, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
     sddg_estimate* dout = static_cast<sddg_estimate*>(c->est.ensure(sizeof(sddg_estimate) * n));
-    run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream, px, py);
+    run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream, px, py, gt);
     ck(cudaMemcpyAsync(out, dout, sizeof(sddg_estimate) * n, cudaMemcpyDeviceToHost, c->stream),
        "d2h");
     ck(cudaStreamSynchronize(c->stream), "d2h sync");
@@ -1099,7 +1105,7 @@ void sddg_destroy(sddg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err, &c->s_large, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
@@ -1685,6 +1691,77 @@ sddg_status sddg_write_mesh(const double* x, const double* y, int32_t m_xi, int3
         return finish(nullptr, f);
     }
     return SDDG_OK;
+}
+
+// ------------------------------------------------------------ fused gather
+
+sddg_status sddg_gather_alloc(sddg_ctx* ctx, int64_t n_records, void** d_buf,
+                              sddg_ipc_handle* handle) {
+    API_BEGIN(ctx)
+    if (n_records < 1) fail(SDDG_ERR_VALIDATION, "gather_alloc: n_records must be >= 1");
+    void* p = nullptr;
+    ck(cudaMalloc(&p, sizeof(sddg_estimate) * n_records), "cudaMalloc gather");
+    ck(cudaMemset(p, 0, sizeof(sddg_estimate) * n_records), "memset gather");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        ck(e, "cudaIpcGetMemHandle");
+    }
+    static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(sddg_ipc_handle), "ipc handle size");
+    std::memset(handle, 0, sizeof(*handle));
+    std::memcpy(handle->bytes, &h, sizeof(h));
+    *d_buf = p;
+    API_END(ctx)
+}
+
+sddg_status sddg_gather_open(sddg_ctx* ctx, const sddg_ipc_handle* handle, void** d_peer) {
+    API_BEGIN(ctx)
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle->bytes, sizeof(h));
+    ck(cudaIpcOpenMemHandle(d_peer, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    API_END(ctx)
+}
+
+sddg_status sddg_gather_close(sddg_ctx* ctx, void* d_peer) {
+    API_BEGIN(ctx)
+    ck(cudaIpcCloseMemHandle(d_peer), "cudaIpcCloseMemHandle");
+    API_END(ctx)
+}
+
+sddg_status sddg_gather_free(sddg_ctx* ctx, void* d_buf) {
+    API_BEGIN(ctx)
+    ck(cudaFree(d_buf), "cudaFree gather");
+    API_END(ctx)
+}
+
+sddg_status sddg_gather_read(sddg_ctx* ctx, const void* d_buf, int64_t n_records,
+                             sddg_estimate* out) {
+    API_BEGIN(ctx)
+    ck(cudaMemcpy(out, d_buf, sizeof(sddg_estimate) * n_records, cudaMemcpyDeviceToHost), "d2h gather");
+    API_END(ctx)
+}
+
+sddg_status sddg_mc_estimate_gather(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
+                                    const sddg_boundary* bd, const sddg_walk_config* cfg,
+                                    const double* px, const double* py, const uint64_t* pid,
+                                    const int64_t* global_index, int64_t n, void* const* peer_bufs,
+                                    int32_t n_peers, int64_t n_total) {
+    API_BEGIN(ctx)
+    if (n_peers < 1 || n_peers > kMaxPeers)
+        fail(SDDG_ERR_VALIDATION, "mc_estimate_gather: 1.." + std::to_string(kMaxPeers) + " peers");
+    for (int64_t k = 0; k < n; ++k)
+        if (global_index[k] < 0 || global_index[k] >= n_total)
+            fail(SDDG_ERR_VALIDATION, "mc_estimate_gather: global index out of range");
+    GatherTargets gt;
+    gt.n_peers = n_peers;
+    for (int p = 0; p < n_peers; ++p) gt.peers[p] = static_cast<sddg_estimate*>(peer_bufs[p]);
+    int64_t* dgi = static_cast<int64_t*>(ctx->gidx.ensure(sizeof(int64_t) * std::max<int64_t>(1, n)));
+    ck(cudaMemcpyAsync(dgi, global_index, sizeof(int64_t) * n, cudaMemcpyHostToDevice, ctx->stream), "h2d");
+    gt.global_index = dgi;
+    std::vector<sddg_estimate> local(n);
+    estimates_host(ctx, *dens, *dom, *bd, *cfg, px, py, pid, n, local.data(), &gt);
+    API_END(ctx)
 }
 
 }  // extern "C"

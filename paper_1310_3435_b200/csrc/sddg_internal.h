@@ -70,10 +70,17 @@ cudaError_t occupancy_walk_ref(int dv, int* b);
 cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
 cudaError_t occupancy_walk_fast(int dv, int precision, int* b);
 
-// reduce.cu: K2 fixed chunk-order finalize, one CTA per node
+// reduce.cu: K2 fixed chunk-order finalize, one CTA per node; with peers,
+// also the fused all-gather (each record stored into every rank's buffer)
+constexpr int kMaxPeers = 16;
+struct GatherTargets {
+    int n_peers;                     // 0: no fused gather
+    const int64_t* global_index;     // local node k -> slot in the gather buffers (device)
+    sddg_estimate* peers[kMaxPeers];  // device pointers (local or IPC-mapped peer memory)
+};
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
                           int64_t walks, int64_t n_nodes, const uint32_t* perm, sddg_estimate* out,
-                          cudaStream_t s);
+                          cudaStream_t s, const GatherTargets& gt);
 
 // solver.cu: K3 batched Dirichlet solves
 struct SolveJob {

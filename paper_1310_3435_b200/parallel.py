@@ -6,7 +6,10 @@ over subdomains (proj/src/decomposition.cpp:172-174, 298-355).
 Here every rank
   1. walks a cost-balanced shard of the interface nodes (K1/K2 on its GPU),
   2. all-gathers the fixed-size sddg_estimate records (the one data-path
-     collective: ~128 B per node, 1.8 MB for config 3's 14,273 nodes),
+     collective: ~128 B per node, 1.8 MB for config 3's 14,273 nodes) --
+     transport="nccl" through torch.distributed, transport="peer" fused
+     into the finalize kernel K2, which stores every record straight into
+     each rank's gather buffer over NVLink peer memory (CUDA IPC),
   3. fills the interface lines (identical on every rank, host C++),
   4. solves a contiguous range of subdomains (K3 on its GPU),
   5. all-gathers the subdomain fields and assembles the mesh.
@@ -79,12 +82,45 @@ def all_gather_rows(local: np.ndarray, indices: np.ndarray, n_total: int, row_by
     return out
 
 
-def solve_interfaces_distributed(plan, m, bd, cfg, layout, estimator=None, ctx=None, interp="linear"):
+def peer_gather_estimates(px, py, pid, mine, m, domain, bd, cfg, ctx=None):
+    """Walk this rank's nodes and deliver every record to every rank with
+    the fused K2 + peer-store path (sddg_mc_estimate_gather).  The handles
+    travel once over the host group; afterwards no collective runs on the
+    data path, only the completion barrier."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n_total = len(px)
+    buf = sdd.PeerGather(n_total, ctx)
+    try:
+        handles = [None] * world
+        dist.all_gather_object(handles, buf.handle)
+        ptrs = [buf.ptr.value if r == rank else buf.open(handles[r]) for r in range(world)]
+        if len(mine):
+            sdd.mc_estimate_gather(np.stack([px[mine], py[mine]], 1), pid[mine], mine, ptrs, n_total,
+                                   m, domain, bd, cfg, ctx=ctx)
+        dist.barrier()          # every rank's stores into every buffer have completed
+        est = buf.read()
+        dist.barrier()          # nobody frees a buffer a peer may still map
+    finally:
+        buf.close()
+    return est
+
+
+def solve_interfaces_distributed(plan, m, bd, cfg, layout, estimator=None, ctx=None, interp="linear",
+                                 transport="nccl"):
     """solve_interfaces over all ranks.  estimator(px, py, pid) -> records
-    (sdd.ESTIMATE_DTYPE); default: this rank's GPU through the C-ABI."""
+    (sdd.ESTIMATE_DTYPE); default: this rank's GPU through the C-ABI.
+    transport="peer" uses the fused K2 peer-store gather instead of the
+    NCCL all-gather (needs the default estimator)."""
     rank, world = dist.get_rank(), dist.get_world_size()
     px, py, pid = sdd.interface_nodes(m, layout, plan)
     mine = shard(expected_cost(px, py, layout.global_.domain), world)[rank]
+    if transport == "peer":
+        if estimator is not None:
+            raise sdd.ValidationError("transport='peer' runs the walks itself; no estimator")
+        est = peer_gather_estimates(px, py, pid, mine, m, layout.global_.domain, bd, cfg, ctx)
+        return sdd.fill_interfaces(m, layout, plan, bd, est, interp=interp), est
+    if transport != "nccl":
+        raise sdd.ValidationError(f"unknown transport {transport!r}")
     if estimator is None:
         def estimator(x, y, p):
             return sdd.mc_estimate_batch(np.stack([x, y], 1), p, m, layout.global_.domain, bd, cfg,
@@ -101,11 +137,12 @@ def subdomain_range(n_sub: int, world: int, rank: int):
 
 
 def solve_sdd_distributed(m, layout, plan, wcfg, scfg, bc_mode=sdd.BC_REFERENCE, estimator=None,
-                          solver=None, ctx=None, interp="linear"):
+                          solver=None, ctx=None, interp="linear", transport="nccl"):
     """solve_sdd over all ranks; every rank returns the assembled (xi, eta)."""
     rank, world = dist.get_rank(), dist.get_world_size()
     bd = sdd.make_boundary_data(m, layout.global_, bc_mode)
-    ifc, est = solve_interfaces_distributed(plan, m, bd, wcfg, layout, estimator, ctx, interp)
+    ifc, est = solve_interfaces_distributed(plan, m, bd, wcfg, layout, estimator, ctx, interp,
+                                            transport)
     n_sub = layout.subdomain_count()
     lo, hi = subdomain_range(n_sub, world, rank)
     if solver is None:

@@ -436,6 +436,68 @@ def mc_estimate_batch_device(px, py, pid, out, m, domain, bd, cfg, ctx=None, str
         C.c_void_p(out.data_ptr()), st), ctx.handle)
 
 
+class _IpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
+class PeerGather:
+    """A device gather buffer of n_total ESTIMATE records that other ranks
+    (processes) open through CUDA IPC and write into directly
+    (sddg_gather_alloc/open/close/free/read)."""
+
+    def __init__(self, n_total: int, ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.n_total = int(n_total)
+        self.ptr = C.c_void_p()
+        h = _IpcHandle()
+        _check(lib().sddg_gather_alloc(self.ctx.handle, C.c_int64(self.n_total), C.byref(self.ptr),
+                                       C.byref(h)), self.ctx.handle)
+        self.handle = bytes(h.bytes)
+        self._opened = []
+
+    def open(self, handle: bytes) -> int:
+        """Map a peer's buffer; returns its device address in this process."""
+        h = _IpcHandle()
+        C.memmove(h.bytes, handle, 64)
+        p = C.c_void_p()
+        _check(lib().sddg_gather_open(self.ctx.handle, C.byref(h), C.byref(p)), self.ctx.handle)
+        self._opened.append(p)
+        return p.value
+
+    def read(self) -> np.ndarray:
+        out = np.zeros(self.n_total, ESTIMATE_DTYPE)
+        _check(lib().sddg_gather_read(self.ctx.handle, self.ptr, C.c_int64(self.n_total),
+                                      out.ctypes.data_as(C.c_void_p)), self.ctx.handle)
+        return out
+
+    def close(self):
+        for p in self._opened:
+            _check(lib().sddg_gather_close(self.ctx.handle, p), self.ctx.handle)
+        self._opened = []
+        if self.ptr:
+            _check(lib().sddg_gather_free(self.ctx.handle, self.ptr), self.ctx.handle)
+            self.ptr = C.c_void_p()
+
+
+def mc_estimate_gather(points, point_ids, global_index, peer_ptrs, n_total, m, domain, bd, cfg,
+                       ctx=None):
+    """mc_estimate_batch whose records K2 stores at slot global_index[k] of
+    every buffer in peer_ptrs (device addresses valid in this process)."""
+    ctx = ctx or default_context()
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
+    px, py = _f64(pts[:, 0]), _f64(pts[:, 1])
+    pid = np.ascontiguousarray(point_ids, dtype=np.uint64)
+    gi = np.ascontiguousarray(global_index, dtype=np.int64)
+    if len(pid) != len(px) or len(gi) != len(px):
+        raise ValidationError("point_ids / global_index length mismatch")
+    peers = (C.c_void_p * len(peer_ptrs))(*[C.c_void_p(int(p)) for p in peer_ptrs])
+    d, dom, b, c = m.c(), domain.c(), bd.c(), cfg.c()
+    _check(lib().sddg_mc_estimate_gather(ctx.handle, C.byref(d), C.byref(dom), C.byref(b), C.byref(c),
+                                         _dp(px), _dp(py), pid.ctypes.data_as(C.c_void_p),
+                                         gi.ctypes.data_as(C.c_void_p), C.c_int64(len(px)), peers,
+                                         C.c_int32(len(peer_ptrs)), C.c_int64(n_total)), ctx.handle)
+
+
 def walk_dump(p, point_id, m, domain, bd, cfg, walk_lo=0, n=1, ctx=None) -> np.ndarray:
     """Per-path (f, g, exit point, steps, epoch, edge) of walks [walk_lo, walk_lo+n)."""
     ctx = ctx or default_context()

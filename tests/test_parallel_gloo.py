@@ -66,6 +66,13 @@ def _worker(rank, world, port, errq):
                                                        solver=fake_solver_factory(lay))
         rxi, reta = sdd.assemble(lay, fake_solver_factory(lay)(0, lay.subdomain_count()))
         assert np.array_equal(xi, rxi) and np.array_equal(eta, reta)
+        for kw in ({"transport": "bogus"}, {"transport": "peer", "estimator": fake_estimator}):
+            try:
+                parallel.solve_interfaces_distributed(plan, m, bd, cfg, lay, **kw)
+            except sdd.ValidationError:
+                pass
+            else:
+                raise AssertionError(f"{kw} accepted")
         dist.barrier()
         dist.destroy_process_group()
     except BaseException as exc:  # surface the failure in the parent
