@@ -73,10 +73,16 @@ __device__ __forceinline__ double poly2(const double* c, double x) {
 __device__ __forceinline__ double frcp(double d) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+#ifdef SDDG_FM_V1
     double e = fma(-d, r, 1.0);
     r = fma(r, e, r);
     e = fma(-d, r, 1.0);
     return fma(r, e, r);
+#else
+    // 1/d = r / (1 - e) = r (1 + e + e^2 + ...): one cubic step (error e^3)
+    const double e = fma(-d, r, 1.0);
+    return fma(r, fma(e, e, e), r);
+#endif
 }
 
 // a / b with one residual correction (~0.5-1 ulp)
@@ -94,11 +100,15 @@ __device__ __forceinline__ double fsqrt_pos(double v) {
     double g = v * y;                 // ~sqrt(v)
     double r = fma(-g, h, 0.5);
     g = fma(g, r, g);
+#ifdef SDDG_FM_V1
     h = fma(h, r, h);
     r = fma(-g, h, 0.5);
     g = fma(g, r, g);
     h = fma(h, r, h);
-    const double d = fma(-g, g, v);   // residual correction
+#endif
+    // one coupled step leaves g with error ~e0^2; the residual correction
+    // squares it again (h's own error only enters at second order)
+    const double d = fma(-g, g, v);
     return fma(d, h, g);
 }
 
@@ -175,7 +185,7 @@ enum FmK {
     K_L7, K_L6, K_L5, K_L3,                // 1/7, -1/6, 1/5, 1/3
     K_LN2HI, K_LN2LO, K_I2D, K_TWOPI,      // ln2 hi, lo, 2^52+2^31, 2 pi
     K_S7, K_S5, K_S3, K_C6,                // -1/5040, 1/120, -1/6, -1/720
-    K_C4, K_PAD1, K_PAD2, K_PAD3           // 1/24
+    K_C4, K_OPEN, K_SCB, K_TWOPI53         // 1/24, 1 - 2^-53, 2^52 + 2^44, 2 pi 2^-53
 };
 // Constants: SDDG_FM_IMMEDIATES -> 64-bit immediates (ptxas rematerialises
 // them with UMOV pairs in the loop); SDDG_FM_LDS_HOISTED -> plain smem reads
@@ -257,6 +267,47 @@ __device__ __forceinline__ void fsincos_2pi_tab(const FmTables& T, double u, dou
     pc = fma(pc, d2, -0.5);
     const double cm1 = pc * d2;
     const double* e = T.sc[__double2loint(t) & 255];
+    const double s0 = e[0], c0 = e[1];
+    sn = s0 + fma(c0, sd, s0 * cm1);
+    cs = c0 + fma(-s0, sd, c0 * cm1);
+}
+
+// Box-Muller inputs straight from the raw 64-bit draws (performance mode):
+// the same values as u01_open_d / u01_d without the I2F conversion pipe.
+//
+// u1 = (2k + 1) 2^-53, k = a >> 12 (rng.hpp:61-63): M = 1 + k 2^-52 is built
+// from the bits and M - (1 - 2^-53) is exact (Sterbenz).
+__device__ __forceinline__ double u01_open_bits(const FmTables& T, uint64_t a) {
+    const uint32_t hi = static_cast<uint32_t>(a >> 44) | 0x3ff00000u;
+    const uint32_t lo = static_cast<uint32_t>(a >> 12);
+    return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo)) -
+           FMK(K_OPEN, 1.0 - 0x1.0p-53);
+}
+
+// sin, cos of 2 pi u2 with u2 = k 2^-53, k = b >> 11 (rng.hpp:58): the
+// reduction 256 u2 = j + f is done on the integer k.  With s = b + 2^55
+// (mod 2^64), j = s >> 56 (mod 256) and k - 2^45 j + 2^44 = bits 11..55 of s,
+// so f 2^53 is an exact double after one subtraction and
+// d = 2 pi f = (f 2^53) (2 pi 2^-53) rounds exactly like 2 pi * f.
+// Ties (f = +-1/512) round up instead of to even: both are correct.
+__device__ __forceinline__ void fsincos_2pi_bits(const FmTables& T, uint64_t b, double& sn,
+                                                 double& cs) {
+    const uint32_t sh = static_cast<uint32_t>(b >> 32) + 0x00800000u;  // high word of b + 2^55
+    const uint32_t sl = static_cast<uint32_t>(b);
+    const uint32_t j = sh >> 24;
+    const uint32_t vlo = __funnelshift_r(sl, sh, 11);                     // bits 11..42
+    const uint32_t vhi = ((sh >> 11) & 0x1fffu) | 0x43300000u;             // bits 43..55
+    const double fi = __hiloint2double(static_cast<int>(vhi), static_cast<int>(vlo)) -
+                      FMK(K_SCB, 4521191813414912.0);                      // f 2^53, exact
+    const double d = fi * FMK(K_TWOPI53, 6.283185307179586 * 0x1.0p-53);
+    const double d2 = d * d;
+    double ps = fma(d2, FMK(K_S7, -0.0001984126984126984), FMK(K_S5, 0.008333333333333333));
+    ps = fma(ps, d2, FMK(K_S3, -0.16666666666666666));
+    const double sd = fma(ps * d2, d, d);
+    double pc = fma(d2, FMK(K_C6, -0.001388888888888889), FMK(K_C4, 0.041666666666666664));
+    pc = fma(pc, d2, -0.5);
+    const double cm1 = pc * d2;
+    const double* e = T.sc[j];
     const double s0 = e[0], c0 = e[1];
     sn = s0 + fma(c0, sd, s0 * cm1);
     cs = c0 + fma(-s0, sd, c0 * cm1);

@@ -98,6 +98,16 @@ __global__ void fastmath_check(int64_t n, const fm::FmTables* __restrict__ tg,
     sincospi(2.0 * t, &s2, &c2);
     if (fabs(s2) > 1e-3) atomicMax(&maxulp[2], ulp_diff(s, s2));
     if (fabs(c2) > 1e-3) atomicMax(&maxulp[2], ulp_diff(c, c2));
+    // Box-Muller inputs from raw draws: u1 exact; sincos(2 pi u2) in slot 2
+    uint64_t b = static_cast<uint64_t>(i) * 0x9E3779B97F4A7C15ull;
+    b ^= b >> 29;
+    b *= 0xBF58476D1CE4E5B9ull;
+    b ^= b >> 32;
+    if (fm::u01_open_bits(T, b) != u01_open_d(b)) atomicMax(&maxulp[1], 1ull << 40);
+    fm::fsincos_2pi_bits(T, b, s, c);
+    sincospi(2.0 * u01_d(b), &s2, &c2);
+    if (fabs(s2) > 1e-3) atomicMax(&maxulp[2], ulp_diff(s, s2));
+    if (fabs(c2) > 1e-3) atomicMax(&maxulp[2], ulp_diff(c, c2));
     const double xs = 80.0 * t;
     atomicMax(&maxulp[3], ulp_diff(fm::fsqrt_pos(xs), sqrt(xs)));
     atomicMax(&maxulp[4], ulp_diff(fm::frcp(1.0 + xs), 1.0 / (1.0 + xs)));

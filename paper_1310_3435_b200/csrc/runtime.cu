@@ -1037,6 +1037,9 @@ void make_fm_tables(void* out) {
     t.k[K_S3] = -1.0 / 6.0;
     t.k[K_C6] = -1.0 / 720.0;
     t.k[K_C4] = 1.0 / 24.0;
+    t.k[K_OPEN] = 1.0 - 0x1.0p-53;
+    t.k[K_SCB] = 4521191813414912.0;  // 2^52 + 2^44
+    t.k[K_TWOPI53] = 6.283185307179586 * 0x1.0p-53;
 }
 
 bool walk_variant_supported(int dv, int precision) {

@@ -41,13 +41,14 @@ struct RealOps<double, FAST> {
     // rng.hpp:66-73: r = sqrt(-2 ln u1), a = 2 pi u2, z = (r cos a, r sin a)
     __device__ static __forceinline__ void box_muller(const fm::FmTables& T, uint64_t a,
                                                       uint64_t b, double& z0, double& z1) {
-        const double u1 = u01_open_d(a);
-        const double u2 = u01_d(b);
         double s, c, r;
         if constexpr (FAST) {
-            r = fm::fsqrt_pos(-2.0 * fm::flog_tab(T, u1));
-            fm::fsincos_2pi_tab(T, u2, s, c);
+            // the same u1, u2 built from the raw bits (fastmath.cuh)
+            r = fm::fsqrt_pos(-2.0 * fm::flog_tab(T, fm::u01_open_bits(T, a)));
+            fm::fsincos_2pi_bits(T, b, s, c);
         } else {
+            const double u1 = u01_open_d(a);
+            const double u2 = u01_d(b);
             r = sqrt(-2.0 * log(u1));
             sincos(6.283185307179586476925286766559 * u2, &s, &c);
         }
@@ -297,13 +298,15 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
             Real hx = Real(0), hy = Real(0);
             int edge = 0;
             bool nb = true;
-            if (!dom.inside(nxp, nyp)) {
-                segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
-                exited = true;
-            } else if constexpr (SCHEME == 0) {
-                if constexpr (BRIDGE) {
-                    nb = dom.in_box(nxp, nyp);
-                    if (!(nb && in_box)) {
+            if constexpr (SCHEME == 0 && BRIDGE) {
+                // inner box first: box inside the domain, so both ends in the
+                // box means no exit and no bridge draw (the common step)
+                nb = dom.in_box(nxp, nyp);
+                if (!(nb && in_box)) {
+                    if (!dom.inside(nxp, nyp)) {
+                        segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+                        exited = true;
+                    } else {
                         // exact pre-filter: an edge draws only if d0*d1 <= 40 dt
                         const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
                         const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
@@ -314,7 +317,10 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
                                                                   rng, hx, hy, edge);
                     }
                 }
-            } else {
+            } else if (!dom.inside(nxp, nyp)) {
+                segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+                exited = true;
+            } else if constexpr (SCHEME == 1) {
                 exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T,
                                                       rng, hx, hy, edge);
             }
