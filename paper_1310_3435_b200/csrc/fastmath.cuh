@@ -162,30 +162,44 @@ __device__ __forceinline__ void fsincos_2pi(double u, double& sn, double& cs) {
 
 // ---------------------------------------------------------------------------
 // Table-driven variants (glibc-style reductions) used by the walk kernel:
-// a small table in shared memory replaces most polynomial terms, cutting the
-// step's elementary-function cost from ~150 to ~90 instructions.  Tables are
-// built on the host in 80-bit long double and rounded once (runtime.cu
-// make_fm_tables); each CTA copies them to shared memory at start.
+// tables in shared memory replace most polynomial terms.  Tables are built on
+// the host in 80-bit long double and rounded once (runtime.cu make_fm_tables);
+// each CTA copies them to shared memory at start.
+//
+// Table sizes: 2^kExBits entries of 2^(j/N) for exp, 2^kLgBits of (1/c, log c)
+// for log, 2^kScBits of (sin, cos)(2 pi j/N).  The default (large) tables fill
+// 64 KB and let every polynomial drop two degrees; they need one 1024-thread
+// CTA per SM (walk_kernel.cuh).  SDDG_FM_SMALL selects the 7.9 KB set that
+// fits 8 x 128-thread CTAs per SM.
 namespace sddg {
 namespace fm {
 
+#ifdef SDDG_FM_SMALL
+constexpr int kExBits = 6, kLgBits = 7, kScBits = 8;
+#else
+constexpr int kExBits = 10, kLgBits = 10, kScBits = 11;
+#endif
+constexpr int kExN = 1 << kExBits, kLgN = 1 << kLgBits, kScN = 1 << kScBits;
+// first j with c_j = 1 + (j + 1/2)/kLgN >= sqrt 2 (log(c_j / 2) branch)
+constexpr int kLgSplit = kLgBits == 7 ? 53 : 424;
+static_assert(kLgBits == 7 || kLgBits == 10, "log split index");
+
 struct FmTables {
-    double sc[256][2];   // sin, cos of 2 pi j / 256
-    double lg[128][3];   // 1/c_j, log(c_j) (hi, lo) [or log(c_j / 2) for c_j >= sqrt 2]
-    double e2[64];       // 2^(j/64)
-    double k[24];        // polynomial / reduction constants (FmK), read with LDS so the
-                         // step loop does not rematerialise 64-bit immediates (2 UMOV each)
+    double k[32];          // polynomial / reduction constants (FmK), read with LDS so the
+                           // step loop does not rematerialise 64-bit immediates (2 UMOV each)
+    double e2[kExN];       // 2^(j/kExN)
+    double lg[kLgN][3];    // -2/c_j, -2 log(c_j) (hi, lo) [log(c_j / 2) for j >= kLgSplit]
+    double sc[kScN][2];    // sin, cos of 2 pi j / kScN
 };
-static_assert(sizeof(FmTables) == 7872, "FmTables layout");
 
 // indices into FmTables::k (pairs adjacent in use order -> LDS.128)
 enum FmK {
     K_E6 = 0, K_E5, K_E4, K_E3,            // 1/720, 1/120, 1/24, 1/6
-    K_64LN2, K_LN2_64HI, K_LN2_64LO, K_PAD0, // 64/ln2, ln2/64 hi, lo
-    K_L7, K_L6, K_L5, K_L3,                // 1/7, -1/6, 1/5, 1/3
-    K_LN2HI, K_LN2LO, K_I2D, K_TWOPI,      // ln2 hi, lo, 2^52+2^31, 2 pi
+    K_EXS, K_EXHI, K_EXLO, K_PAD0,         // kExN/ln2, ln2/kExN hi, lo
+    K_L7, K_L6, K_L5, K_L3,                // 1/448, 1/192, 1/80, 1/12 (log1p in R = -2r)
+    K_LN2HI, K_LN2LO, K_I2D, K_TWOPI,      // -2 ln2 hi, lo, 2^52+2^31, 2 pi
     K_S7, K_S5, K_S3, K_C6,                // -1/5040, 1/120, -1/6, -1/720
-    K_C4, K_OPEN, K_SCB, K_TWOPI53         // 1/24, 1 - 2^-53, 2^52 + 2^44, 2 pi 2^-53
+    K_C4, K_OPEN, K_SCB, K_TWOPI53         // 1/24, 1 - 2^-53, 2^52 + 2^52/kScN, 2 pi 2^-53
 };
 // Constants: SDDG_FM_IMMEDIATES -> 64-bit immediates (ptxas rematerialises
 // them with UMOV pairs in the loop); SDDG_FM_LDS_HOISTED -> plain smem reads
@@ -205,71 +219,110 @@ __device__ __forceinline__ double lds_f64(const double* p) {
 #define FMK(i, v) (lds_f64(&T.k[i]))  // default: A/B best (+3.6% vs immediates)
 #endif
 
-constexpr double k64Ln2 = 92.33248261689366;       // 64 / ln 2
-constexpr double kLn2_64Hi = 0.010830424696249145;  // ln 2 / 64
-constexpr double kLn2_64Lo = 3.623510646634843e-19;
+// host-side values of the reduction constants (runtime.cu fills FmTables::k)
+constexpr double kExScale = kExN / 0.69314718055994530941723212145818;
+constexpr double kExHi = kLn2Hi / kExN;  // exact power-of-two scalings of ln2 hi/lo
+constexpr double kExLo = kLn2Lo / kExN;
 
-// exp(x), x in [-700, 0]: x = (64 e + j) ln2/64 + r, |r| <= ln2/128
+// exp(x), x <= 0: x = (N e + j) ln2/N + r, |r| <= ln2/(2N), N = kExN.  Below
+// x = -707.7 the scale exponent is clamped (one integer max instead of a
+// double fmax): the result stays a tiny positive normal instead of wrapping.
 __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
-    x = fmax(x, -700.0);
-    const double t = fma(x, FMK(K_64LN2, k64Ln2), kRound);
+    const double t = fma(x, FMK(K_EXS, kExScale), kRound);
     const double n = t - kRound;
-    double r = fma(n, -FMK(K_LN2_64HI, kLn2_64Hi), x);
-    r = fma(n, -FMK(K_LN2_64LO, kLn2_64Lo), r);
-    // e^r - 1 = r + r^2/2 + ... + r^6/720  (next term ~3e-20)
-    double p = fma(r, FMK(K_E6, 0.001388888888888889), FMK(K_E5, 0.008333333333333333));
-    p = fma(p, r, FMK(K_E4, 0.041666666666666664));
-    p = fma(p, r, FMK(K_E3, 0.16666666666666666));
+    double r = fma(n, -FMK(K_EXHI, kExHi), x);
+    r = fma(n, -FMK(K_EXLO, kExLo), r);
+    double p;
+    if constexpr (kExBits >= 10) {
+        // e^r - 1 = r + r^2/2 + r^3/6 + r^4/24  (|r| <= 3.4e-4: next term ~4e-20)
+        p = fma(r, FMK(K_E4, 0.041666666666666664), FMK(K_E3, 0.16666666666666666));
+    } else {
+        // e^r - 1 = r + r^2/2 + ... + r^6/720  (next term ~3e-20)
+        p = fma(r, FMK(K_E6, 0.001388888888888889), FMK(K_E5, 0.008333333333333333));
+        p = fma(p, r, FMK(K_E4, 0.041666666666666664));
+        p = fma(p, r, FMK(K_E3, 0.16666666666666666));
+    }
     p = fma(p, r, 0.5);
     p = fma(p, r, 1.0);
     p = p * r;
-    const int ni = __double2loint(t);
-    const double s = T.e2[ni & 63];
-    const double v = fma(s, p, s);  // 2^(j/64) e^r
-    return __hiloint2double(__double2hiint(v) + ((ni >> 6) << 20), __double2loint(v));
+    const int ni = max(__double2loint(t), -kExN * 1021);
+    const double s = T.e2[ni & (kExN - 1)];
+    const double v = fma(s, p, s);  // 2^(j/N) e^r
+    return __hiloint2double(__double2hiint(v) + ((ni >> kExBits) << 20), __double2loint(v));
 }
 
-// log(u), u in (2^-54, 1]: u = 2^k m, m in [1,2); c_j = 1 + (j+1/2)/128 of m's
-// top 7 mantissa bits; r = m / c_j - 1 (|r| <= 1/256);  log u = (k + a) ln2 +
-// log(c_j / 2^a) + log1p(r), a = [c_j >= sqrt 2] (no cancellation near u = 1).
-__device__ __forceinline__ double flog_tab(const FmTables& T, double u) {
+// -2 log(u), u in (2^-54, 1] (the Box-Muller radius squared): u = 2^k m,
+// m in [1,2); c_j = 1 + (j+1/2)/N of m's top kLgBits mantissa bits;
+// r = m / c_j - 1 (|r| <= 1/(2N)); log u = (k + a) ln2 + log(c_j / 2^a) +
+// log1p(r), a = [c_j >= sqrt 2] (no cancellation near u = 1).  Everything is
+// carried pre-scaled by -2 -- R = -2 r = m (-2/c_j) + 2, the table's
+// -2 log c_j, the polynomial coefficients scaled by powers of two -- so each
+// rounding is the exact -2 multiple of the unscaled one: the result is
+// bit-identical to -2 * log(u) computed the plain way, minus the multiply.
+__device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     const int hi = __double2hiint(u);
     const int lo = __double2loint(u);
-    const int j = (hi >> 13) & 127;
-    const int k = ((hi >> 20) - 1023) + (j >= 53 ? 1 : 0);  // c_53 = 1.4180 >= sqrt 2
+    const int j = (hi >> (20 - kLgBits)) & (kLgN - 1);
+    const int k = ((hi >> 20) - 1023) + (j >= kLgSplit ? 1 : 0);
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double* e = T.lg[j];
-    const double r = fma(m, e[0], -1.0);
-    // log1p(r) = r - r^2/2 + ... + r^7/7  (next term ~3e-20)
-    double p = fma(r, FMK(K_L7, 0.14285714285714285), FMK(K_L6, -0.16666666666666666));
-    p = fma(p, r, FMK(K_L5, 0.2));
-    p = fma(p, r, -0.25);
-    p = fma(p, r, FMK(K_L3, 0.3333333333333333));
-    p = fma(p, r, -0.5);
-    p = p * r;
+    const double R = fma(m, e[0], 2.0);
+    double p;
+    if constexpr (kLgBits >= 10) {
+        // log1p(r) = r - r^2/2 + r^3/3 - r^4/4 + r^5/5 (|r| <= 2^-11: next
+        // term ~5e-18 relative), Horner in R = -2r
+        p = fma(R, FMK(K_L5, 1.0 / 80.0), 0.03125);
+    } else {
+        // log1p(r) = r - r^2/2 + ... + r^7/7 (next term ~3e-20), Horner in R
+        p = fma(R, FMK(K_L7, 1.0 / 448.0), FMK(K_L6, 1.0 / 192.0));
+        p = fma(p, R, FMK(K_L5, 1.0 / 80.0));
+        p = fma(p, R, 0.03125);
+    }
+    p = fma(p, R, FMK(K_L3, 1.0 / 12.0));
+    p = fma(p, R, 0.25);
+    p = p * R;
     const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - FMK(K_I2D, 4503601774854144.0);
-    const double h = fma(dk, FMK(K_LN2HI, kLn2Hi), e[1]);
-    return h + (fma(p, r, r) + fma(dk, FMK(K_LN2LO, kLn2Lo), e[2]));
+    const double h = fma(dk, FMK(K_LN2HI, -2.0 * kLn2Hi), e[1]);
+    return h + (fma(p, R, R) + fma(dk, FMK(K_LN2LO, -2.0 * kLn2Lo), e[2]));
 }
 
-// sin, cos of 2 pi u, u in [0, 1): 2 pi u = 2 pi j/256 + d, |d| <= pi/256
-__device__ __forceinline__ void fsincos_2pi_tab(const FmTables& T, double u, double& sn,
-                                                double& cs) {
-    const double t = fma(256.0, u, kRound);
-    const double q = t - kRound;                       // rint(256 u)
-    const double d = FMK(K_TWOPI, 6.283185307179586) * fma(-0.00390625, q, u);  // exact f, |f| <= 1/512
+// log(u), u in (2^-54, 1]: exactly -1/2 of fm2log_tab
+__device__ __forceinline__ double flog_tab(const FmTables& T, double u) {
+    return -0.5 * fm2log_tab(T, u);
+}
+
+// sin d, cos d - 1 for |d| <= pi/kScN, then the table rotation
+__device__ __forceinline__ void sincos_rotate(const FmTables& T, int j, double d, double& sn,
+                                              double& cs) {
     const double d2 = d * d;
-    // sin d = d (1 - d^2/6 + d^4/120 - d^6/5040), cos d - 1 = d^2 (-1/2 + d^2/24 - d^4/720)
-    double ps = fma(d2, FMK(K_S7, -0.0001984126984126984), FMK(K_S5, 0.008333333333333333));
-    ps = fma(ps, d2, FMK(K_S3, -0.16666666666666666));
+    double ps, pc;
+    if constexpr (kScBits >= 11) {
+        // sin d = d (1 - d^2/6 + d^4/120), cos d - 1 = d^2 (-1/2 + d^2/24)
+        // (|d| <= 1.5e-3: next terms ~3e-21 and ~2e-20)
+        ps = fma(d2, FMK(K_S5, 0.008333333333333333), FMK(K_S3, -0.16666666666666666));
+        pc = fma(d2, FMK(K_C4, 0.041666666666666664), -0.5);
+    } else {
+        // sin d = d (1 - d^2/6 + d^4/120 - d^6/5040), cos d - 1 = d^2 (-1/2 + d^2/24 - d^4/720)
+        ps = fma(d2, FMK(K_S7, -0.0001984126984126984), FMK(K_S5, 0.008333333333333333));
+        ps = fma(ps, d2, FMK(K_S3, -0.16666666666666666));
+        pc = fma(d2, FMK(K_C6, -0.001388888888888889), FMK(K_C4, 0.041666666666666664));
+        pc = fma(pc, d2, -0.5);
+    }
     const double sd = fma(ps * d2, d, d);
-    double pc = fma(d2, FMK(K_C6, -0.001388888888888889), FMK(K_C4, 0.041666666666666664));
-    pc = fma(pc, d2, -0.5);
     const double cm1 = pc * d2;
-    const double* e = T.sc[__double2loint(t) & 255];
+    const double* e = T.sc[j];
     const double s0 = e[0], c0 = e[1];
     sn = s0 + fma(c0, sd, s0 * cm1);
     cs = c0 + fma(-s0, sd, c0 * cm1);
+}
+
+// sin, cos of 2 pi u, u in [0, 1): 2 pi u = 2 pi j/N + d, |d| <= pi/N
+__device__ __forceinline__ void fsincos_2pi_tab(const FmTables& T, double u, double& sn,
+                                                double& cs) {
+    const double t = fma(static_cast<double>(kScN), u, kRound);
+    const double q = t - kRound;                       // rint(N u)
+    const double d = FMK(K_TWOPI, 6.283185307179586) * fma(-1.0 / kScN, q, u);  // exact f
+    sincos_rotate(T, __double2loint(t) & (kScN - 1), d, sn, cs);
 }
 
 // Box-Muller inputs straight from the raw 64-bit draws (performance mode):
@@ -285,32 +338,24 @@ __device__ __forceinline__ double u01_open_bits(const FmTables& T, uint64_t a) {
 }
 
 // sin, cos of 2 pi u2 with u2 = k 2^-53, k = b >> 11 (rng.hpp:58): the
-// reduction 256 u2 = j + f is done on the integer k.  With s = b + 2^55
-// (mod 2^64), j = s >> 56 (mod 256) and k - 2^45 j + 2^44 = bits 11..55 of s,
-// so f 2^53 is an exact double after one subtraction and
-// d = 2 pi f = (f 2^53) (2 pi 2^-53) rounds exactly like 2 pi * f.
-// Ties (f = +-1/512) round up instead of to even: both are correct.
+// reduction N u2 = j + f (N = 2^B = kScN) is done on the integer k.  With
+// s = b + 2^(63-B) (mod 2^64), j = s >> (64-B) (mod N) and
+// k - 2^(53-B) j + 2^(52-B) = bits 11..(63-B) of s, so f 2^53 is an exact
+// double after one subtraction and d = 2 pi f = (f 2^53)(2 pi 2^-53) rounds
+// exactly like 2 pi * f.  Ties (f = +-1/(2N)) round up instead of to even:
+// both are correct.
 __device__ __forceinline__ void fsincos_2pi_bits(const FmTables& T, uint64_t b, double& sn,
                                                  double& cs) {
-    const uint32_t sh = static_cast<uint32_t>(b >> 32) + 0x00800000u;  // high word of b + 2^55
+    constexpr int B = kScBits;
+    const uint32_t sh = static_cast<uint32_t>(b >> 32) + (1u << (31 - B));  // high word of s
     const uint32_t sl = static_cast<uint32_t>(b);
-    const uint32_t j = sh >> 24;
-    const uint32_t vlo = __funnelshift_r(sl, sh, 11);                     // bits 11..42
-    const uint32_t vhi = ((sh >> 11) & 0x1fffu) | 0x43300000u;             // bits 43..55
+    const uint32_t j = sh >> (32 - B);
+    const uint32_t vlo = __funnelshift_r(sl, sh, 11);                          // bits 11..42
+    const uint32_t vhi = ((sh >> 11) & ((1u << (21 - B)) - 1u)) | 0x43300000u;  // bits 43..63-B
     const double fi = __hiloint2double(static_cast<int>(vhi), static_cast<int>(vlo)) -
-                      FMK(K_SCB, 4521191813414912.0);                      // f 2^53, exact
+                      FMK(K_SCB, 4503599627370496.0 + 4503599627370496.0 / kScN);  // f 2^53
     const double d = fi * FMK(K_TWOPI53, 6.283185307179586 * 0x1.0p-53);
-    const double d2 = d * d;
-    double ps = fma(d2, FMK(K_S7, -0.0001984126984126984), FMK(K_S5, 0.008333333333333333));
-    ps = fma(ps, d2, FMK(K_S3, -0.16666666666666666));
-    const double sd = fma(ps * d2, d, d);
-    double pc = fma(d2, FMK(K_C6, -0.001388888888888889), FMK(K_C4, 0.041666666666666664));
-    pc = fma(pc, d2, -0.5);
-    const double cm1 = pc * d2;
-    const double* e = T.sc[j];
-    const double s0 = e[0], c0 = e[1];
-    sn = s0 + fma(c0, sd, s0 * cm1);
-    cs = c0 + fma(-s0, sd, c0 * cm1);
+    sincos_rotate(T, static_cast<int>(j), d, sn, cs);
 }
 
 }  // namespace fm

@@ -1,3 +1,4 @@
+#include <algorithm>
 // probe.cu -- measured non-tensor peaks of this B200 for the walk kernel's
 // roofline (MEASURED_PEAKS.json only carries HBM and bf16 tensor peaks).
 //   fp64: independent DFMA chains, 2 flops per DFMA
@@ -78,12 +79,13 @@ __device__ unsigned long long ulp_diff(double a, double b) {
 // accuracy for speed; its ulp error there is reported separately, slot 5)
 __global__ void fastmath_check(int64_t n, const fm::FmTables* __restrict__ tg,
                                unsigned long long* maxulp) {
-    __shared__ fm::FmTables T;
+    extern __shared__ double tsm[];
+    const fm::FmTables& T = *reinterpret_cast<const fm::FmTables*>(tsm);
     for (int k = threadIdx.x; k < static_cast<int>(sizeof(fm::FmTables) / 8); k += blockDim.x)
-        reinterpret_cast<double*>(&T)[k] = reinterpret_cast<const double*>(tg)[k];
+        tsm[k] = reinterpret_cast<const double*>(tg)[k];
     __syncthreads();
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double t = (static_cast<double>(i) + 0.5) / static_cast<double>(n);  // (0,1)
     const double xe = -700.0 * t * t;
     atomicMax(&maxulp[0], ulp_diff(fm::fexp_tab(T, xe), exp(xe)));
@@ -111,6 +113,7 @@ __global__ void fastmath_check(int64_t n, const fm::FmTables* __restrict__ tg,
     const double xs = 80.0 * t;
     atomicMax(&maxulp[3], ulp_diff(fm::fsqrt_pos(xs), sqrt(xs)));
     atomicMax(&maxulp[4], ulp_diff(fm::frcp(1.0 + xs), 1.0 / (1.0 + xs)));
+    }
 }
 
 }  // namespace
@@ -120,7 +123,10 @@ cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long*
     cudaError_t e = cudaMalloc(&d, 6 * sizeof(unsigned long long));
     if (e != cudaSuccess) return e;
     cudaMemset(d, 0, 6 * sizeof(unsigned long long));
-    fastmath_check<<<static_cast<unsigned>((n + 255) / 256), 256>>>(
+    constexpr int sm = static_cast<int>(sizeof(fm::FmTables));
+    cudaFuncSetAttribute(fastmath_check, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 8);
+    fastmath_check<<<static_cast<unsigned>(blocks), 256, sm>>>(
         n, static_cast<const fm::FmTables*>(tables), d);
     e = cudaMemcpy(host_maxulp6, d, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(d);

@@ -90,7 +90,7 @@ struct sddg_ctx {
     DevBuf m_in, m_out, m_q, m_misc;
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
-    std::map<int, int> occ;  // (dv*2+prec) -> blocks per SM
+    std::map<int, std::pair<int, int>> occ;  // (dv*2+prec) -> (CTAs per SM, threads per CTA)
     std::vector<cudaEvent_t> bev;  // per-batch walk-kernel events
     DevBuf fm_tables;              // fastmath.cuh FmTables (performance mode)
     DevBuf gidx;                   // fused-gather global indices
@@ -172,19 +172,21 @@ void check_boundary(const sddg_boundary& b) {
 
 // ------------------------------------------------------------ K1 + K2
 
-int walk_grid(sddg_ctx* c, int dv, int prec, uint64_t total) {
+// Persistent grid of the walk kernel: (CTAs, threads per CTA)
+std::pair<int, int> walk_grid(sddg_ctx* c, int dv, int prec, uint64_t total) {
     const int key = dv * 2 + prec;
     auto it = c->occ.find(key);
-    int bps;
+    std::pair<int, int> o;
     if (it == c->occ.end()) {
-        ck(walk_occupancy(dv, prec, &bps), "occupancy");
-        c->occ[key] = bps;
+        ck(walk_occupancy(dv, prec, &o.first, &o.second), "occupancy");
+        c->occ[key] = o;
     } else {
-        bps = it->second;
+        o = it->second;
     }
-    const uint64_t full = static_cast<uint64_t>(std::max(1, bps)) * c->sms;
-    const uint64_t need = (total + kWalkBlock - 1) / kWalkBlock;
-    return static_cast<int>(std::max<uint64_t>(1, std::min(full, need)));
+    const uint64_t blk = static_cast<uint64_t>(o.second);
+    const uint64_t full = static_cast<uint64_t>(std::max(1, o.first)) * c->sms;
+    const uint64_t need = (total + blk - 1) / blk;
+    return {static_cast<int>(std::max<uint64_t>(1, std::min(full, need))), o.second};
 }
 
 int64_t batch_budget_walks() {
@@ -331,8 +333,8 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         a.pid = d_pid;
         a.perm = dperm + b;
         a.total = static_cast<uint64_t>(nb) * W;
-        const int grid = walk_grid(c, dv, cfg.precision, a.total);
-        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * kWalkBlock);
+        const auto [grid, blk] = walk_grid(c, dv, cfg.precision, a.total);
+        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * blk);
         ck(cudaGetLastError(), "set_next");
         ck(cudaEventRecord(c->bev[2 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
@@ -1000,36 +1002,39 @@ namespace sddg {
 void make_fm_tables(void* out) {
     fm::FmTables& t = *static_cast<fm::FmTables*>(out);
     const long double pi = acosl(-1.0L), ln2 = logl(2.0L);
-    for (int j = 0; j < 256; ++j) {
-        const long double a = 2.0L * pi * j / 256.0L;
+    for (int j = 0; j < fm::kScN; ++j) {
+        const long double a = 2.0L * pi * j / fm::kScN;
         t.sc[j][0] = static_cast<double>(sinl(a));
         t.sc[j][1] = static_cast<double>(cosl(a));
     }
-    for (int j = 0; j < 128; ++j) {
-        const double c = 1.0 + (j + 0.5) / 128.0;
+    for (int j = 0; j < fm::kLgN; ++j) {
+        const double c = 1.0 + (j + 0.5) / fm::kLgN;
         const double rc = static_cast<double>(1.0L / c);
         long double L = -logl(static_cast<long double>(rc));  // log(1/rc), consistent with r
-        if (j >= 53) L -= ln2;                               // log(c/2) branch
-        t.lg[j][0] = rc;
-        t.lg[j][1] = static_cast<double>(L);
-        t.lg[j][2] = static_cast<double>(L - static_cast<long double>(t.lg[j][1]));
+        if (j >= fm::kLgSplit) L -= ln2;                    // log(c/2) branch
+        // stored pre-scaled by -2 (exact): fastmath.cuh fm2log_tab
+        const double Lhi = static_cast<double>(L);
+        t.lg[j][0] = -2.0 * rc;
+        t.lg[j][1] = -2.0 * Lhi;
+        t.lg[j][2] = -2.0 * static_cast<double>(L - static_cast<long double>(Lhi));
     }
-    for (int j = 0; j < 64; ++j) t.e2[j] = static_cast<double>(exp2l(j / 64.0L));
+    for (int j = 0; j < fm::kExN; ++j)
+        t.e2[j] = static_cast<double>(exp2l(static_cast<long double>(j) / fm::kExN));
     using namespace fm;
     for (double& v : t.k) v = 0.0;
     t.k[K_E6] = 1.0 / 720.0;
     t.k[K_E5] = 1.0 / 120.0;
     t.k[K_E4] = 1.0 / 24.0;
     t.k[K_E3] = 1.0 / 6.0;
-    t.k[K_64LN2] = k64Ln2;
-    t.k[K_LN2_64HI] = kLn2_64Hi;
-    t.k[K_LN2_64LO] = kLn2_64Lo;
-    t.k[K_L7] = 1.0 / 7.0;
-    t.k[K_L6] = -1.0 / 6.0;
-    t.k[K_L5] = 0.2;
-    t.k[K_L3] = 1.0 / 3.0;
-    t.k[K_LN2HI] = kLn2Hi;
-    t.k[K_LN2LO] = kLn2Lo;
+    t.k[K_EXS] = kExScale;
+    t.k[K_EXHI] = kExHi;
+    t.k[K_EXLO] = kExLo;
+    t.k[K_L7] = 1.0 / 448.0;  // log1p coefficients in R = -2r (exact power-of-2 scalings)
+    t.k[K_L6] = 1.0 / 192.0;
+    t.k[K_L5] = 1.0 / 80.0;
+    t.k[K_L3] = 1.0 / 12.0;
+    t.k[K_LN2HI] = -2.0 * kLn2Hi;
+    t.k[K_LN2LO] = -2.0 * kLn2Lo;
     t.k[K_I2D] = 4503601774854144.0;
     t.k[K_TWOPI] = 6.283185307179586;
     t.k[K_S7] = -1.0 / 5040.0;
@@ -1038,7 +1043,7 @@ void make_fm_tables(void* out) {
     t.k[K_C6] = -1.0 / 720.0;
     t.k[K_C4] = 1.0 / 24.0;
     t.k[K_OPEN] = 1.0 - 0x1.0p-53;
-    t.k[K_SCB] = 4521191813414912.0;  // 2^52 + 2^44
+    t.k[K_SCB] = 4503599627370496.0 + 4503599627370496.0 / kScN;  // 2^52 + 2^52 / N
     t.k[K_TWOPI53] = 6.283185307179586 * 0x1.0p-53;
 }
 
@@ -1053,10 +1058,10 @@ cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cuda
     return launch_walk_ref(dv, a, grid, s);
 }
 
-cudaError_t walk_occupancy(int dv, int precision, int* b) {
+cudaError_t walk_occupancy(int dv, int precision, int* b, int* block) {
     if (!walk_variant_supported(dv, precision)) return cudaErrorInvalidValue;
-    if (dv >= 32) return occupancy_walk_fast(dv, precision, b);
-    return occupancy_walk_ref(dv, b);
+    if (dv >= 32) return occupancy_walk_fast(dv, precision, b, block);
+    return occupancy_walk_ref(dv, b, block);
 }
 
 }  // namespace sddg
@@ -1216,8 +1221,8 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         a.err_flag = &cnt->err_flag;
         a.err_info = &cnt->err_info;
         a.dump = dd;
-        const int grid = walk_grid(ctx, dv, cfg->precision, a.total);
-        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * kWalkBlock);
+        const auto [grid, blk] = walk_grid(ctx, dv, cfg->precision, a.total);
+        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * blk);
         ck(cudaEventRecord(ctx->ev0, st), "event");
         ck(launch_walk(dv, cfg->precision, a, grid, st), "walk kernel launch");
         ck(cudaEventRecord(ctx->ev1, st), "event");

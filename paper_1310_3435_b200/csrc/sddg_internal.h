@@ -63,16 +63,22 @@ void make_fm_tables(void* host_tables7680);
 // walk_ref.cu (fp64, -fmad=false) and walk_fast.cu (analytic drifts, fp64 + fp32)
 bool walk_variant_supported(int dv, int precision);
 cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
-cudaError_t walk_occupancy(int dv, int precision, int* blocks_per_sm);
+cudaError_t walk_occupancy(int dv, int precision, int* blocks_per_sm, int* block);
 // the two TUs' own dispatchers
 cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s);
-cudaError_t occupancy_walk_ref(int dv, int* b);
+cudaError_t occupancy_walk_ref(int dv, int* b, int* block);
 cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
-cudaError_t occupancy_walk_fast(int dv, int precision, int* b);
+cudaError_t occupancy_walk_fast(int dv, int precision, int* b, int* block);
 
 // reduce.cu: K2 fixed chunk-order finalize, one CTA per node; with peers,
 // also the fused all-gather (each record stored into every rank's buffer)
 constexpr int kMaxPeers = 16;
+// walk_kernel.cuh: per-lane bookkeeping of the running walk (shared memory)
+struct LaneState {
+    uint64_t g;       // record slot of the running walk
+    uint64_t steps;   // path steps finished by this lane
+    uint32_t node, walk, epoch, pad;
+};
 struct GatherTargets {
     int n_peers;                     // 0: no fused gather
     const int64_t* global_index;     // local node k -> slot in the gather buffers (device)

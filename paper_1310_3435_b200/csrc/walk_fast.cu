@@ -17,10 +17,10 @@ cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid,
     return cudaErrorInvalidValue;
 }
 
-cudaError_t occupancy_walk_fast(int dv, int precision, int* b) {
+cudaError_t occupancy_walk_fast(int dv, int precision, int* b, int* block) {
     switch (dv) {
-#define X(V) case V: return precision == SDDG_FP64 ? occupancy_variant<V, double>(b) \
-                                                   : occupancy_variant<V, float>(b);
+#define X(V) case V: return precision == SDDG_FP64 ? occupancy_variant<V, double>(b, block) \
+                                                   : occupancy_variant<V, float>(b, block);
         SDDG_FAST_VARIANTS(X)
 #undef X
     }

@@ -41,19 +41,21 @@ struct RealOps<double, FAST> {
     // rng.hpp:66-73: r = sqrt(-2 ln u1), a = 2 pi u2, z = (r cos a, r sin a)
     __device__ static __forceinline__ void box_muller(const fm::FmTables& T, uint64_t a,
                                                       uint64_t b, double& z0, double& z1) {
-        double s, c, r;
-        if constexpr (FAST) {
-            // the same u1, u2 built from the raw bits (fastmath.cuh)
-            r = fm::fsqrt_pos(-2.0 * fm::flog_tab(T, fm::u01_open_bits(T, a)));
-            fm::fsincos_2pi_bits(T, b, s, c);
-        } else {
-            const double u1 = u01_open_d(a);
-            const double u2 = u01_d(b);
-            r = sqrt(-2.0 * log(u1));
-            sincos(6.283185307179586476925286766559 * u2, &s, &c);
-        }
+        const double u1 = u01_open_d(a);
+        const double u2 = u01_d(b);
+        double s, c;
+        const double r = sqrt(-2.0 * log(u1));
+        sincos(6.283185307179586476925286766559 * u2, &s, &c);
         z0 = r * c;
         z1 = r * s;
+    }
+    // performance mode: scale * radius and the angle's sin/cos, with u1, u2
+    // built from the raw bits (fastmath.cuh); z = (R cs, R sn) / scale
+    __device__ static __forceinline__ void bm_polar(const fm::FmTables& T, uint64_t a, uint64_t b,
+                                                    double scale, double& R, double& sn,
+                                                    double& cs) {
+        R = scale * fm::fsqrt_pos(fm::fm2log_tab(T, fm::u01_open_bits(T, a)));
+        fm::fsincos_2pi_bits(T, b, sn, cs);
     }
     __device__ static __forceinline__ double ex(const fm::FmTables& T, double v) {
         if constexpr (FAST) return fm::fexp_tab(T, v);
@@ -86,14 +88,11 @@ struct RealOps<float, FAST> {
         const float series = -(p * d);
         return d <= 0.0625f ? series : __logf(u1);
     }
-    __device__ static __forceinline__ void box_muller(const fm::FmTables&, uint64_t a, uint64_t b,
-                                                      float& z0, float& z1) {
+    __device__ static __forceinline__ void bm_polar(const fm::FmTables&, uint64_t a, uint64_t b,
+                                                    float scale, float& R, float& sn, float& cs) {
         const float v = -2.0f * ln_open(a);
-        const float r = v * rsqrtf(v);
-        float s, c;
-        __sincosf(6.2831853f * u01_f(b), &s, &c);
-        z0 = r * c;
-        z1 = r * s;
+        R = scale * (v * rsqrtf(v));
+        __sincosf(6.2831853f * u01_f(b), &sn, &cs);
     }
     __device__ static __forceinline__ float ex(const fm::FmTables&, float v) { return __expf(v); }
     __device__ static __forceinline__ float lg(const fm::FmTables&, float v) { return __logf(v); }
@@ -229,9 +228,28 @@ __device__ __forceinline__ double table_at(const double* __restrict__ t, int n, 
     return (1.0 - u) * __ldg(t + k) + u * __ldg(t + k + 1);
 }
 
+// Launch shape per variant.  Performance-mode fp64 reads the fastmath tables
+// from shared memory; with the large tables (64 KB) one CTA fills an SM:
+// 1024 threads at 64 registers, or 640 at 96 for the register-hungrier
+// shock drift.  Everything else: 128-thread CTAs, several per SM.
+template <int DV, typename Real>
+__host__ __device__ constexpr bool walk_uses_tables() {
+    return DV >= DV_RING_AN && sizeof(Real) == 8;
+}
+constexpr bool kBigTables = sizeof(fm::FmTables) > 24 * 1024;
+template <int DV, typename Real>
+__host__ __device__ constexpr int walk_block() {
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return DV == DV_SHOCK_AN ? 640 : 1024;
+    return kWalkBlock;
+}
+template <int DV, typename Real>
+__host__ __device__ constexpr int walk_min_blocks() {
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return 1;
+    return (DV == DV_SHOCK_AN || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
+}
+
 template <int DV, typename Real, int SCHEME, bool BRIDGE>
-__global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING_AN) ? 5
-                                                                                   : kWalkMinBlocks)
+__global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Real>())
     walk_kernel(const __grid_constant__ WalkArgs a) {
     constexpr bool FAST = DV >= DV_RING_AN;
     using Ops = RealOps<Real, FAST>;
@@ -242,35 +260,59 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);
     const uint32_t max_steps = a.max_steps32;
-    // performance mode: elementary-function tables in shared memory
+    // performance mode: elementary-function tables in (dynamic) shared memory
     extern __shared__ double dyn_smem[];
     fm::FmTables& T = *reinterpret_cast<fm::FmTables*>(dyn_smem);
-    if constexpr (FAST && sizeof(Real) == 8) {
-        const double* src = reinterpret_cast<const double*>(a.fm_tables);
-        for (int k = threadIdx.x; k < static_cast<int>(sizeof(fm::FmTables) / 8); k += blockDim.x)
-            dyn_smem[k] = src[k];
+    if constexpr (walk_uses_tables<DV, Real>()) {
+        const double2* src = reinterpret_cast<const double2*>(a.fm_tables);
+        double2* dst = reinterpret_cast<double2*>(dyn_smem);
+        for (int k = threadIdx.x; k < static_cast<int>(sizeof(fm::FmTables) / 16); k += blockDim.x)
+            dst[k] = src[k];
         __syncthreads();
     }
 
-    uint64_t g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    uint64_t my_steps = 0;
-    if (g < a.total) {
-        // ---- walk setup (re-entered for every new walk)
-        uint64_t slot = g / static_cast<uint64_t>(a.walks);
-        uint32_t node = a.perm ? a.perm[slot] : static_cast<uint32_t>(slot);
-        uint32_t walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
-        uint64_t pid = a.pid[node];
-        uint32_t epoch = 0;
-        Real x = Real(a.px[node]), y = Real(a.py[node]);
-        bool in_box = dom.in_box(x, y);
+    // Per-walk bookkeeping that only the rare exit / restart paths touch
+    // (record slot, node, walk, epoch, step total) lives in shared memory, so
+    // the step loop keeps its 64 registers for the step itself.
+    __shared__ LaneState lane_state[walk_block<DV, Real>()];
+    LaneState& L = lane_state[threadIdx.x];
+    L.g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    L.steps = 0;
+    if (L.g < a.total) {
+        Real x, y;
         LaneStream rng;
-        rng.init(pid, walk, epoch);
+        // ---- walk setup (re-entered for every new walk)
+        auto start_walk = [&](uint64_t g) {
+            const uint64_t slot = g / static_cast<uint64_t>(a.walks);
+            const uint32_t node = a.perm ? a.perm[slot] : static_cast<uint32_t>(slot);
+            L.node = node;
+            L.walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
+            L.epoch = 0;
+            x = Real(a.px[node]);
+            y = Real(a.py[node]);
+            rng.init(a.pid[node], L.walk, 0);
+        };
+        start_walk(L.g);
+        bool in_box = dom.in_box(x, y);
         uint32_t step = 0;
+#ifndef SDDG_WALK_NO_UNROLL
+#pragma unroll 2  // two step copies: x, y alternate registers (no loop-carried moves)
+#endif
         for (;;) {
             // ---- one step
             Real bx, by, nxp, nyp, z0, z1;
             bool ok;
-            if constexpr (SCHEME == 0) {
+            if constexpr (SCHEME == 0 && FAST) {
+                // x + b dt + sqrt(2 dt) z with b dt = c v and sqrt(2 dt) z = R (cs, sn)
+                Real c, vx, vy, R, sn, cs;
+                drift_cv<DV>(T, x, y, dt, c, vx, vy);
+                ok = true;  // closed forms: finite everywhere
+                uint64_t ua, ub;
+                rng.next_pair(a.rk, ua, ub);
+                Ops::bm_polar(T, ua, ub, sq2dt, R, sn, cs);
+                nxp = fma(R, cs, fma(c, vx, x));
+                nyp = fma(R, sn, fma(c, vy, y));
+            } else if constexpr (SCHEME == 0) {
                 ok = drift<DV, Real>(P, T, x, y, bx, by);
                 uint64_t ua, ub;
                 rng.next_pair(a.rk, ua, ub);
@@ -283,15 +325,22 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
                 ok = drift<DV, Real>(P, T, x, y, bx, by);
                 uint64_t ua, ub;
                 rng.next_pair(a.rk, ua, ub);
-                Ops::box_muller(T, ua, ub, z0, z1);
                 const Real s = Ops::sq(Real(2) * edt);
-                nxp = x + bx * edt + s * z0;
-                nyp = y + by * edt + s * z1;
+                if constexpr (FAST) {
+                    Real R, sn, cs;
+                    Ops::bm_polar(T, ua, ub, s, R, sn, cs);
+                    nxp = x + bx * edt + R * cs;
+                    nyp = y + by * edt + R * sn;
+                } else {
+                    Ops::box_muller(T, ua, ub, z0, z1);
+                    nxp = x + bx * edt + s * z0;
+                    nyp = y + by * edt + s * z1;
+                }
             }
             ++step;
             if (!ok) {
                 atomicCAS(a.err_flag, 0, 3);  // EvaluationError
-                atomicExch(a.err_info, static_cast<unsigned long long>(pid));
+                atomicExch(a.err_info, static_cast<unsigned long long>(a.pid[L.node]));
                 break;
             }
             bool exited = false;
@@ -330,14 +379,15 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
                 in_box = nb;
                 if (step < max_steps) continue;
                 // max_steps reached: restart on the next epoch's stream
-                my_steps += step;
-                ++epoch;
+                L.steps += step;
+                const uint32_t epoch = ++L.epoch;
+                const uint32_t node = L.node;
                 if (epoch >= 1024u) {
                     atomicCAS(a.err_flag, 0, 4);  // NumericalError
-                    atomicExch(a.err_info, static_cast<unsigned long long>(pid));
+                    atomicExch(a.err_info, static_cast<unsigned long long>(a.pid[node]));
                     break;
                 }
-                rng.init(pid, walk, epoch);
+                rng.init(a.pid[node], L.walk, epoch);
                 x = Real(a.px[node]);
                 y = Real(a.py[node]);
                 in_box = dom.in_box(x, y);
@@ -351,7 +401,8 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
             const int tn = horiz ? a.tnx : a.tny;
             const double fv = table_at(a.tf[edge], tn, par);
             const double gv = table_at(a.tg[edge], tn, par);
-            my_steps += step;
+            L.steps += step;
+            const uint64_t g = L.g;
             if (a.dump) {
                 sddg_path& r = a.dump[g];
                 r.f = fv;
@@ -359,27 +410,22 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
                 r.ex = dhx;
                 r.ey = dhy;
                 r.steps = step;
-                r.epoch = static_cast<int32_t>(epoch);
+                r.epoch = static_cast<int32_t>(L.epoch);
                 r.edge = edge;
             } else {
                 a.rec_f[g] = fv;
                 a.rec_g[g] = gv;
-                a.rec_meta[g] = static_cast<uint32_t>(edge) | (epoch << 2);
+                a.rec_meta[g] = static_cast<uint32_t>(edge) | (L.epoch << 2);
             }
-            g = atomicAdd(a.next, 1ull);
-            if (g >= a.total) break;
-            slot = g / static_cast<uint64_t>(a.walks);
-            node = a.perm ? a.perm[slot] : static_cast<uint32_t>(slot);
-            walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
-            pid = a.pid[node];
-            epoch = 0;
-            x = Real(a.px[node]);
-            y = Real(a.py[node]);
+            const uint64_t gn = atomicAdd(a.next, 1ull);
+            if (gn >= a.total) break;
+            L.g = gn;
+            start_walk(gn);
             in_box = dom.in_box(x, y);
-            rng.init(pid, walk, epoch);
             step = 0;
         }
     }
+    uint64_t my_steps = L.steps;
     // path-step count: warp sum, one atomic per warp
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_steps += __shfl_xor_sync(0xffffffffu, my_steps, o);
@@ -390,25 +436,46 @@ __global__ void __launch_bounds__(kWalkBlock, (DV == DV_SHOCK_AN || DV < DV_RING
 // All (SCHEME, BRIDGE) instantiations of one drift variant.
 template <int DV, typename Real>
 constexpr size_t walk_smem() {
-    return (DV >= DV_RING_AN && sizeof(Real) == 8) ? sizeof(fm::FmTables) : 0;
+    return walk_uses_tables<DV, Real>() ? sizeof(fm::FmTables) : 0;
 }
 
-template <int DV, typename Real>
-cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
+template <int DV, typename Real, int SCHEME, bool BRIDGE>
+cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
     constexpr size_t sm = walk_smem<DV, Real>();
-    if (a.scheme == SDDG_SCHEME_EXPONENTIAL)
-        walk_kernel<DV, Real, 1, false><<<grid, kWalkBlock, sm, s>>>(a);
-    else if (a.bridge)
-        walk_kernel<DV, Real, 0, true><<<grid, kWalkBlock, sm, s>>>(a);
-    else
-        walk_kernel<DV, Real, 0, false><<<grid, kWalkBlock, sm, s>>>(a);
+    if constexpr (sm > 48 * 1024) {
+        static bool attr = false;  // once per process and variant (the device is fixed per ctx)
+        if (!attr) {
+            const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       static_cast<int>(sm));
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+    }
+    walk_kernel<DV, Real, SCHEME, BRIDGE><<<grid, walk_block<DV, Real>(), sm, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int DV, typename Real>
-cudaError_t occupancy_variant(int* b) {
+cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
+    if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false>(a, grid, s);
+    if (a.bridge) return launch_one<DV, Real, 0, true>(a, grid, s);
+    return launch_one<DV, Real, 0, false>(a, grid, s);
+}
+
+// CTAs per SM and threads per CTA of the variant's bridge-test kernel
+template <int DV, typename Real>
+cudaError_t occupancy_variant(int* b, int* block) {
+    constexpr size_t sm = walk_smem<DV, Real>();
+    *block = walk_block<DV, Real>();
+    if constexpr (sm > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, 0, true>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+    }
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(b, walk_kernel<DV, Real, 0, true>,
-                                                         kWalkBlock, walk_smem<DV, Real>());
+                                                         walk_block<DV, Real>(), sm);
 }
 
 }  // namespace sddg

@@ -20,9 +20,9 @@ cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s)
     return cudaErrorInvalidValue;
 }
 
-cudaError_t occupancy_walk_ref(int dv, int* b) {
+cudaError_t occupancy_walk_ref(int dv, int* b, int* block) {
     switch (dv) {
-#define X(V) case V: return occupancy_variant<V, double>(b);
+#define X(V) case V: return occupancy_variant<V, double>(b, block);
         SDDG_REF_VARIANTS(X)
 #undef X
     }
