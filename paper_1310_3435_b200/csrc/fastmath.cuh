@@ -188,7 +188,8 @@ struct FmTables {
     double k[32];          // polynomial / reduction constants (FmK), read with LDS so the
                            // step loop does not rematerialise 64-bit immediates (2 UMOV each)
     double e2[kExN];       // 2^(j/kExN)
-    double lg[kLgN][3];    // -2/c_j, -2 log(c_j) (hi, lo) [log(c_j / 2) for j >= kLgSplit]
+    double lg[kLgN][2];    // -2 rc_j, 2 log(rc_j) [+2 ln2 for j >= kLgSplit]: rc_j ~ 1/c_j chosen
+                           // so that log(rc_j) is within 2^-8 ulp of a double (no lo part)
     double sc[kScN][2];    // sin, cos of 2 pi j / kScN
 };
 
@@ -203,7 +204,9 @@ enum FmK {
 };
 // Constants: SDDG_FM_IMMEDIATES -> 64-bit immediates (ptxas rematerialises
 // them with UMOV pairs in the loop); SDDG_FM_LDS_HOISTED -> plain smem reads
-// (ptxas hoists and spills them); default -> one ld.shared per use.
+// (ptxas hoists and spills them); SDDG_FM_LDS -> one ld.shared per use (adds
+// a third of the step's shared-memory wavefronts); default -> __constant__
+// bank (LDC or direct operands; no shared-memory traffic).
 __device__ __forceinline__ double lds_f64(const double* p) {
     double r;
     asm volatile("ld.shared.f64 %0, [%1];"
@@ -213,16 +216,30 @@ __device__ __forceinline__ double lds_f64(const double* p) {
 }
 #if defined(SDDG_FM_IMMEDIATES)
 #define FMK(i, v) (v)
+#elif defined(SDDG_FM_LDS)
+#define FMK(i, v) (lds_f64(&T.k[i]))  // +3.6% vs immediates; keeps the LSU busier than CBANK
 #elif defined(SDDG_FM_LDS_HOISTED)
 #define FMK(i, v) (T.k[i])
 #else
-#define FMK(i, v) (lds_f64(&T.k[i]))  // default: A/B best (+3.6% vs immediates)
+#define SDDG_FM_CBANK
+#define FMK(i, v) (kFmC[i])  // default: constant-bank operands (A/B best, +1% vs LDS)
 #endif
 
 // host-side values of the reduction constants (runtime.cu fills FmTables::k)
 constexpr double kExScale = kExN / 0.69314718055994530941723212145818;
 constexpr double kExHi = kLn2Hi / kExN;  // exact power-of-two scalings of ln2 hi/lo
 constexpr double kExLo = kLn2Lo / kExN;
+#ifdef SDDG_FM_CBANK
+// the FmTables::k values in FmK order, as a constant bank
+static __constant__ double kFmC[32] = {
+    1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
+    kExScale, kExHi, kExLo, 0.0,
+    1.0 / 448.0, 1.0 / 192.0, 1.0 / 80.0, 1.0 / 12.0,
+    -2.0 * kLn2Hi, -2.0 * kLn2Lo, 4503601774854144.0, 6.283185307179586,
+    -1.0 / 5040.0, 1.0 / 120.0, -1.0 / 6.0, -1.0 / 720.0,
+    1.0 / 24.0, 1.0 - 0x1.0p-53, 4503599627370496.0 + 4503599627370496.0 / kScN,
+    6.283185307179586 * 0x1.0p-53};
+#endif
 
 // exp(x), x <= 0: x = (N e + j) ln2/N + r, |r| <= ln2/(2N), N = kExN.  Below
 // x = -707.7 the scale exponent is clamped (one integer max instead of a
@@ -252,13 +269,15 @@ __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
 }
 
 // -2 log(u), u in (2^-54, 1] (the Box-Muller radius squared): u = 2^k m,
-// m in [1,2); c_j = 1 + (j+1/2)/N of m's top kLgBits mantissa bits;
-// r = m / c_j - 1 (|r| <= 1/(2N)); log u = (k + a) ln2 + log(c_j / 2^a) +
-// log1p(r), a = [c_j >= sqrt 2] (no cancellation near u = 1).  Everything is
-// carried pre-scaled by -2 -- R = -2 r = m (-2/c_j) + 2, the table's
-// -2 log c_j, the polynomial coefficients scaled by powers of two -- so each
-// rounding is the exact -2 multiple of the unscaled one: the result is
-// bit-identical to -2 * log(u) computed the plain way, minus the multiply.
+// m in [1,2); c_j = 1 + (j+1/2)/N of m's top kLgBits mantissa bits; rc_j a
+// double within a few hundred ulp of 1/c_j whose log is almost exactly a
+// double (Gal's accurate-table trick, so one table word suffices);
+// r = m rc_j - 1 (|r| <= 1/(2N) + 2^-44); log u = (k + a) ln2 - log(rc_j 2^a)
+// + log1p(r), a = [c_j >= sqrt 2] (no cancellation near u = 1).  Everything
+// is carried pre-scaled by -2 -- R = -2 r = m (-2 rc_j) + 2, the table's
+// 2 log rc_j, the polynomial coefficients scaled by powers of two -- so each
+// rounding is the exact -2 multiple of the unscaled one: the result equals
+// -2 * log(u) computed the plain way, minus the multiply.
 __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     const int hi = __double2hiint(u);
     const int lo = __double2loint(u);
@@ -283,7 +302,7 @@ __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     p = p * R;
     const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - FMK(K_I2D, 4503601774854144.0);
     const double h = fma(dk, FMK(K_LN2HI, -2.0 * kLn2Hi), e[1]);
-    return h + (fma(p, R, R) + fma(dk, FMK(K_LN2LO, -2.0 * kLn2Lo), e[2]));
+    return h + fma(dk, FMK(K_LN2LO, -2.0 * kLn2Lo), fma(p, R, R));
 }
 
 // log(u), u in (2^-54, 1]: exactly -1/2 of fm2log_tab

@@ -1008,15 +1008,33 @@ void make_fm_tables(void* out) {
         t.sc[j][1] = static_cast<double>(cosl(a));
     }
     for (int j = 0; j < fm::kLgN; ++j) {
+        // Gal's accurate table: among the 2048 doubles nearest fl(1/c_j), take
+        // the rc whose log lies closest to a double (80-bit logl resolves 11
+        // bits past the double; typically within 2^-8 ulp, always < 2^-5)
         const double c = 1.0 + (j + 0.5) / fm::kLgN;
-        const double rc = static_cast<double>(1.0L / c);
-        long double L = -logl(static_cast<long double>(rc));  // log(1/rc), consistent with r
-        if (j >= fm::kLgSplit) L -= ln2;                    // log(c/2) branch
+        const double rc0 = static_cast<double>(1.0L / c);
+        double rc = rc0, up = rc0, dn = rc0, best_rc = rc0;
+        long double L = 0.0L, best_L = 0.0L, best_err = 1.0L;
+        for (int t = 0; t < 2048; ++t) {  // rc0, rc0+1ulp, rc0-1ulp, rc0+2ulp, ...
+            if (t > 0) rc = (t & 1) ? (up = std::nextafter(up, 2.0)) : (dn = std::nextafter(dn, 0.0));
+            L = -logl(static_cast<long double>(rc));       // log(1/rc), consistent with r
+            if (j >= fm::kLgSplit) L -= ln2;              // log(c/2) branch
+            const double Lh = static_cast<double>(L);
+            const long double ulp =
+                static_cast<long double>(std::nextafter(std::fabs(Lh), 1e300) - std::fabs(Lh));
+            const long double err = fabsl(L - static_cast<long double>(Lh)) / ulp;
+            if (err < best_err) {
+                best_err = err;
+                best_rc = rc;
+                best_L = L;
+            }
+            if (err <= 1.0L / 256.0L) break;
+        }
+        rc = best_rc;
+        L = best_L;
         // stored pre-scaled by -2 (exact): fastmath.cuh fm2log_tab
-        const double Lhi = static_cast<double>(L);
         t.lg[j][0] = -2.0 * rc;
-        t.lg[j][1] = -2.0 * Lhi;
-        t.lg[j][2] = -2.0 * static_cast<double>(L - static_cast<long double>(Lhi));
+        t.lg[j][1] = -2.0 * static_cast<double>(L);
     }
     for (int j = 0; j < fm::kExN; ++j)
         t.e2[j] = static_cast<double>(exp2l(static_cast<long double>(j) / fm::kExN));

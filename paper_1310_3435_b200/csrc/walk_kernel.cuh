@@ -239,11 +239,19 @@ __host__ __device__ constexpr bool walk_uses_tables() {
 constexpr bool kBigTables = sizeof(fm::FmTables) > 24 * 1024;
 template <int DV, typename Real>
 __host__ __device__ constexpr int walk_block() {
+#ifdef SDDG_WALK_TABLE_BLOCK
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables && DV != DV_SHOCK_AN)
+        return SDDG_WALK_TABLE_BLOCK;
+#endif
     if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return DV == DV_SHOCK_AN ? 640 : 1024;
     return kWalkBlock;
 }
 template <int DV, typename Real>
 __host__ __device__ constexpr int walk_min_blocks() {
+#ifdef SDDG_WALK_TABLE_BLOCKS_PER_SM
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables && DV != DV_SHOCK_AN)
+        return SDDG_WALK_TABLE_BLOCKS_PER_SM;
+#endif
     if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return 1;
     return (DV == DV_SHOCK_AN || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
 }
