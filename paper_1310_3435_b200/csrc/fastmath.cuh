@@ -198,7 +198,7 @@ enum FmK {
     K_E6 = 0, K_E5, K_E4, K_E3,            // 1/720, 1/120, 1/24, 1/6
     K_EXS, K_EXHI, K_EXLO, K_PAD0,         // kExN/ln2, ln2/kExN hi, lo
     K_L7, K_L6, K_L5, K_L3,                // 1/448, 1/192, 1/80, 1/12 (log1p in R = -2r)
-    K_LN2HI, K_LN2LO, K_I2D, K_TWOPI,      // -2 ln2 hi, lo, 2^52+2^31, 2 pi
+    K_LN2HI, K_LN2LO, K_I2D, K_TWOPI,      // 2 ln2 hi, lo, (unused), 2 pi
     K_S7, K_S5, K_S3, K_C6,                // -1/5040, 1/120, -1/6, -1/720
     K_C4, K_OPEN, K_SCB, K_TWOPI53         // 1/24, 1 - 2^-53, 2^52 + 2^52/kScN, 2 pi 2^-53
 };
@@ -227,6 +227,15 @@ __device__ __forceinline__ double lds_f64(const double* p) {
 
 // host-side values of the reduction constants (runtime.cu fills FmTables::k)
 constexpr double kExScale = kExN / 0.69314718055994530941723212145818;
+// Low-order coefficients rounded to 21 significant bits (low word zero), so
+// each is a 32-bit immediate of its DFMA instead of a constant load: their
+// terms are <= 2^-36 of the result, so the 2^-22 coefficient error stays
+// below 0.02 ulp.  The reduction scale only picks n (r is exact from n).
+constexpr double kE4i = 0x1.55555p-5;    // ~1/24
+constexpr double kE3i = 0x1.55555p-3;    // ~1/6
+constexpr double kS5i = 0x1.11111p-7;    // ~1/120
+constexpr double kC4i = 0x1.55555p-5;    // ~1/24
+constexpr double kExScaleI = kExBits == 10 ? 0x1.71547p+10 : 0x1.71547p+6;  // ~N/ln2
 constexpr double kExHi = kLn2Hi / kExN;  // exact power-of-two scalings of ln2 hi/lo
 constexpr double kExLo = kLn2Lo / kExN;
 #ifdef SDDG_FM_CBANK
@@ -235,7 +244,7 @@ static __constant__ double kFmC[32] = {
     1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
     kExScale, kExHi, kExLo, 0.0,
     1.0 / 448.0, 1.0 / 192.0, 1.0 / 80.0, 1.0 / 12.0,
-    -2.0 * kLn2Hi, -2.0 * kLn2Lo, 4503601774854144.0, 6.283185307179586,
+    2.0 * kLn2Hi, 2.0 * kLn2Lo, 4503601774854144.0, 6.283185307179586,
     -1.0 / 5040.0, 1.0 / 120.0, -1.0 / 6.0, -1.0 / 720.0,
     1.0 / 24.0, 1.0 - 0x1.0p-53, 4503599627370496.0 + 4503599627370496.0 / kScN,
     6.283185307179586 * 0x1.0p-53};
@@ -245,14 +254,14 @@ static __constant__ double kFmC[32] = {
 // x = -707.7 the scale exponent is clamped (one integer max instead of a
 // double fmax): the result stays a tiny positive normal instead of wrapping.
 __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
-    const double t = fma(x, FMK(K_EXS, kExScale), kRound);
+    const double t = fma(x, kExScaleI, kRound);
     const double n = t - kRound;
     double r = fma(n, -FMK(K_EXHI, kExHi), x);
     r = fma(n, -FMK(K_EXLO, kExLo), r);
     double p;
     if constexpr (kExBits >= 10) {
         // e^r - 1 = r + r^2/2 + r^3/6 + r^4/24  (|r| <= 3.4e-4: next term ~4e-20)
-        p = fma(r, FMK(K_E4, 0.041666666666666664), FMK(K_E3, 0.16666666666666666));
+        p = fma(r, kE4i, kE3i);
     } else {
         // e^r - 1 = r + r^2/2 + ... + r^6/720  (next term ~3e-20)
         p = fma(r, FMK(K_E6, 0.001388888888888889), FMK(K_E5, 0.008333333333333333));
@@ -282,7 +291,7 @@ __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     const int hi = __double2hiint(u);
     const int lo = __double2loint(u);
     const int j = (hi >> (20 - kLgBits)) & (kLgN - 1);
-    const int k = ((hi >> 20) - 1023) + (j >= kLgSplit ? 1 : 0);
+    const int nk = (1023 - (hi >> 20)) - (j >= kLgSplit ? 1 : 0);  // -k >= 0
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
     const double* e = T.lg[j];
     const double R = fma(m, e[0], 2.0);
@@ -300,9 +309,10 @@ __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     p = fma(p, R, FMK(K_L3, 1.0 / 12.0));
     p = fma(p, R, 0.25);
     p = p * R;
-    const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - FMK(K_I2D, 4503601774854144.0);
-    const double h = fma(dk, FMK(K_LN2HI, -2.0 * kLn2Hi), e[1]);
-    return h + fma(dk, FMK(K_LN2LO, -2.0 * kLn2Lo), fma(p, R, R));
+    // -k as a double without the conversion pipe: (2^52 + nk) - 2^52
+    const double dnk = __hiloint2double(0x43300000, nk) - 4503599627370496.0;
+    const double h = fma(dnk, FMK(K_LN2HI, 2.0 * kLn2Hi), e[1]);
+    return h + fma(dnk, FMK(K_LN2LO, 2.0 * kLn2Lo), fma(p, R, R));
 }
 
 // log(u), u in (2^-54, 1]: exactly -1/2 of fm2log_tab
@@ -318,8 +328,8 @@ __device__ __forceinline__ void sincos_rotate(const FmTables& T, int j, double d
     if constexpr (kScBits >= 11) {
         // sin d = d (1 - d^2/6 + d^4/120), cos d - 1 = d^2 (-1/2 + d^2/24)
         // (|d| <= 1.5e-3: next terms ~3e-21 and ~2e-20)
-        ps = fma(d2, FMK(K_S5, 0.008333333333333333), FMK(K_S3, -0.16666666666666666));
-        pc = fma(d2, FMK(K_C4, 0.041666666666666664), -0.5);
+        ps = fma(d2, kS5i, FMK(K_S3, -0.16666666666666666));
+        pc = fma(d2, kC4i, -0.5);
     } else {
         // sin d = d (1 - d^2/6 + d^4/120 - d^6/5040), cos d - 1 = d^2 (-1/2 + d^2/24 - d^4/720)
         ps = fma(d2, FMK(K_S7, -0.0001984126984126984), FMK(K_S5, 0.008333333333333333));
@@ -372,7 +382,7 @@ __device__ __forceinline__ void fsincos_2pi_bits(const FmTables& T, uint64_t b, 
     const uint32_t vlo = __funnelshift_r(sl, sh, 11);                          // bits 11..42
     const uint32_t vhi = ((sh >> 11) & ((1u << (21 - B)) - 1u)) | 0x43300000u;  // bits 43..63-B
     const double fi = __hiloint2double(static_cast<int>(vhi), static_cast<int>(vlo)) -
-                      FMK(K_SCB, 4503599627370496.0 + 4503599627370496.0 / kScN);  // f 2^53
+                      (4503599627370496.0 + 4503599627370496.0 / kScN);  // f 2^53 (immediate)
     const double d = fi * FMK(K_TWOPI53, 6.283185307179586 * 0x1.0p-53);
     sincos_rotate(T, static_cast<int>(j), d, sn, cs);
 }

@@ -1051,8 +1051,8 @@ void make_fm_tables(void* out) {
     t.k[K_L6] = 1.0 / 192.0;
     t.k[K_L5] = 1.0 / 80.0;
     t.k[K_L3] = 1.0 / 12.0;
-    t.k[K_LN2HI] = -2.0 * kLn2Hi;
-    t.k[K_LN2LO] = -2.0 * kLn2Lo;
+    t.k[K_LN2HI] = 2.0 * kLn2Hi;  // multiplies -k (fm2log_tab)
+    t.k[K_LN2LO] = 2.0 * kLn2Lo;
     t.k[K_I2D] = 4503601774854144.0;
     t.k[K_TWOPI] = 6.283185307179586;
     t.k[K_S7] = -1.0 / 5040.0;
