@@ -1,12 +1,19 @@
-# one measurement round on the B200: smoke, tests, bench, launch list, full ncu of the walk kernel
+# one measurement round on the B200: smoke, tests, bench, and ONE ncu pass
+#   NCU=launch: launch list of the bench (gpu__time_duration per launch)
+#   NCU=full:   full capture of the walk kernel at --walks 10000
+#   NCU=0:      none
 set -x
 TAG=${TAG:-x}
+if [ "${TESTS:-1}" = 1 ]; then
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke_$TAG.log
 timeout 1200 python -m pytest tests -q -m gpu 2>&1 | tail -15 > gpurun_out/tests_$TAG.log; cat gpurun_out/tests_$TAG.log
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?"; grep '^{' gpurun_out/bench_$TAG.log | cut -c1-400
-if [ "${NCU:-1}" = 1 ]; then
-timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain_$TAG.log 2>&1 && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launch rc=$?"
-timeout 300 python bench.py --steps 1 --warmup 1 --walks 10000 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain2_$TAG.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_kernel -s 1 -c 1 -o gpurun_out/walk_full_$TAG python bench.py --steps 1 --warmup 1 --walks 10000 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
 fi
+case "${NCU:-launch}" in
+launch)
+timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain_$TAG.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launch rc=$?" ;;
+full)
+timeout 300 python bench.py --steps 1 --warmup 1 --walks 10000 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/bench_ncu_plain2_$TAG.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_kernel -s 1 -c 1 -o gpurun_out/walk_full_$TAG python bench.py --steps 1 --warmup 1 --walks 10000 --no-cpu-baseline --no-e2e --no-mesh > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?" ;;
+esac
