@@ -28,7 +28,7 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I" + os.path.join(ROOT, "include")]
 UNITS = {
     "walk_ref.cu": ["-fmad=false"],
-    "walk_fast.cu": ["-fmad=true"],
+    "walk_fast.cu": ["-fmad=true", "-ftz=true"],  # fp32 walks: no denormal fix-ups around SFU ops
     "reduce.cu": ["-fmad=false"],
     "solver.cu": ["-fmad=false"],
     "mesh.cu": ["-fmad=false"],
@@ -46,7 +46,8 @@ def _mtime(p):
 def _compile(unit, flags, verbose):
     src = os.path.join(CSRC, unit)
     obj = os.path.join(OBJ_DIR, unit.replace(".cu", ".o"))
-    deps = [src] + [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "sddg.h")]
+    deps = [src, os.path.abspath(__file__)] + [os.path.join(CSRC, h) for h in HEADERS] + \
+        [os.path.join(ROOT, "include", "sddg.h")]  # build.py itself: flag changes rebuild
     if _mtime(obj) >= max(_mtime(d) for d in deps):
         return obj, False
     cmd = [NVCC] + ARCH + COMMON + EXTRA + flags + ["-c", src, "-o", obj]

@@ -92,7 +92,9 @@ struct RealOps<float, FAST> {
                                                     float scale, float& R, float& sn, float& cs) {
         const float v = -2.0f * ln_open(a);
         R = scale * (v * rsqrtf(v));
-        __sincosf(6.2831853f * u01_f(b), &sn, &cs);
+        // 2 pi u2 with u2 = top 24 bits 2^-24 (u01_f), one multiply
+        __sincosf(static_cast<float>(static_cast<uint32_t>(b >> 40)) * (6.2831853f * 0x1.0p-24f),
+                  &sn, &cs);
     }
     __device__ static __forceinline__ float ex(const fm::FmTables&, float v) { return __expf(v); }
     __device__ static __forceinline__ float lg(const fm::FmTables&, float v) { return __logf(v); }
