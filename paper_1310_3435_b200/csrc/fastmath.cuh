@@ -4,157 +4,45 @@
 // Why: the CUDA library's fp64 exp/log/sincos carry their polynomial
 // coefficients as 64-bit immediates, which ptxas materialises with two UMOVs
 // per coefficient inside the step loop (18% of all issued instructions in the
-// r01 profile, profiles/r01_walk_kernel_ncu_v0.txt).  Here the coefficients
-// live in __constant__ memory so each DFMA reads its operand straight from the
-// constant bank, and the argument ranges are the walk's own (no inf/nan/
-// denormal paths):
-//   fexp_neg(x)      x in [-700, 0]          (drift densities)
-//   flog_unit(u)     u in (2^-54, 1]         (Box-Muller radius)
-//   fsincos_2pi(u)   u in [0, 1)             (Box-Muller angle 2 pi u)
-//   frcp(d)          d > 0, normal
-//   fsqrt_pos(v)     v > 0, normal
-// Accuracy ~1 ulp (Taylor/atanh series to well below 2^-53 truncation).  The
+// first profile, profiles/r01_walk_kernel_ncu_v0_first.txt), and handle
+// inf/nan/denormal arguments the walk never produces.  Here:
+//   frcp(d), fsqrt_pos(v)          MUFU seed + Newton, d, v > 0 normal
+//   fexp_tab(x)                    x <= 0 (drift densities)
+//   fm2log_tab(u), flog_tab(u)     u in (2^-54, 1] (Box-Muller radius)
+//   fsincos_2pi_tab(u)             u in [0, 1)
+//   u01_open_bits, fsincos_2pi_bits  Box-Muller inputs from the raw draws
+// use shared-memory tables (glibc-style reductions) and constant-bank or
+// immediate coefficients.  Accuracy ~1 ulp (sddg_selftest_fastmath).  The
 // reference-parity kernels keep the CUDA library (walk_ref.cu).
 #pragma once
 
 namespace sddg {
 namespace fm {
 
-// 1/k!, k = 0 .. 13 (ascending)
-__constant__ double kExp[14] = {
-    1.0, 1.0, 0.5, 0.16666666666666666,
-    0.041666666666666664, 0.008333333333333333, 0.001388888888888889, 0.0001984126984126984,
-    2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07, 2.505210838544172e-08,
-    2.08767569878681e-09, 1.6059043836821613e-10};
-// 2/(2k+1), k = 0 .. 10: log1p(f) = s * sum_k 2/(2k+1) s^(2k), s = f/(2+f)
-__constant__ double kAtanh[11] = {
-    2.0, 0.6666666666666666, 0.4, 0.2857142857142857,
-    0.2222222222222222, 0.18181818181818182, 0.15384615384615385, 0.13333333333333333,
-    0.11764705882352941, 0.10526315789473684, 0.09523809523809523};
-// sin(2 pi f) = f * sum_k S_k f^(2k), k = 0 .. 9 ; |f| <= 1/8 (|2 pi f| <= pi/4:
-// next terms ~1e-19 and ~2e-18 relative)
-__constant__ double kSin[10] = {
-    6.283185307179586, -41.34170224039976, 81.60524927607506, -76.70585975306139,
-    42.058693944897655, -15.09464257682299, 3.819952584848282, -0.7181223017785006,
-    0.10422916220813984, -0.012031585942120627};
-// cos(2 pi f) = sum_k C_k f^(2k), k = 0 .. 8
-__constant__ double kCos[9] = {
-    1.0, -19.739208802178716, 64.9393940226683, -85.45681720669373,
-    60.24464137187666, -26.4262567833744, 7.903536371318469, -1.714390711088672,
-    0.28200596845579123};
 constexpr double kLn2Hi = 0.6931471805599453;
 constexpr double kLn2Lo = 2.3190468138462996e-17;
-constexpr double kLog2e = 1.4426950408889634;
 constexpr double kRound = 6755399441055744.0;  // 1.5 * 2^52
-
-// sum_{k<N} c[k] x^k as two interleaved Horner chains (even and odd
-// coefficients in x^2): half the dependency depth of plain Horner while every
-// DFMA still takes exactly one coefficient straight from the constant bank
-// (Estrin's pair products need two constant operands -> an extra LDC each).
-template <int N>
-__device__ __forceinline__ double poly2(const double* c, double x) {
-#ifdef SDDG_POLY_HORNER
-    double h = c[N - 1];
-#pragma unroll
-    for (int k = N - 2; k >= 0; --k) h = fma(h, x, c[k]);
-    return h;
-#endif
-    const double x2 = x * x;
-    constexpr int ne = (N + 1) / 2, no = N / 2;
-    double pe = c[2 * (ne - 1)];
-    double po = c[2 * (no - 1) + 1];
-#pragma unroll
-    for (int k = ne - 2; k >= 0; --k) pe = fma(pe, x2, c[2 * k]);
-#pragma unroll
-    for (int k = no - 2; k >= 0; --k) po = fma(po, x2, c[2 * k + 1]);
-    return fma(po, x, pe);
-}
 
 __device__ __forceinline__ double frcp(double d) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-#ifdef SDDG_FM_V1
-    double e = fma(-d, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-d, r, 1.0);
-    return fma(r, e, r);
-#else
     // 1/d = r / (1 - e) = r (1 + e + e^2 + ...): one cubic step (error e^3)
     const double e = fma(-d, r, 1.0);
     return fma(r, fma(e, e, e), r);
-#endif
-}
-
-// a / b with one residual correction (~0.5-1 ulp)
-__device__ __forceinline__ double fdiv(double a, double b) {
-    const double r = frcp(b);
-    const double q = a * r;
-    return fma(r, fma(-b, q, a), q);
 }
 
 // sqrt(v) for v > 0 normal: rsqrt seed + Newton, no special-case branch
 __device__ __forceinline__ double fsqrt_pos(double v) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
-    double h = 0.5 * y;
+    const double h = 0.5 * y;
     double g = v * y;                 // ~sqrt(v)
-    double r = fma(-g, h, 0.5);
+    const double r = fma(-g, h, 0.5);
     g = fma(g, r, g);
-#ifdef SDDG_FM_V1
-    h = fma(h, r, h);
-    r = fma(-g, h, 0.5);
-    g = fma(g, r, g);
-    h = fma(h, r, h);
-#endif
     // one coupled step leaves g with error ~e0^2; the residual correction
     // squares it again (h's own error only enters at second order)
     const double d = fma(-g, g, v);
     return fma(d, h, g);
-}
-
-__device__ __forceinline__ double fexp_neg(double x) {
-    x = fmax(x, -700.0);
-    const double t = fma(x, kLog2e, kRound);
-    const double n = t - kRound;
-    double r = fma(n, -kLn2Hi, x);
-    r = fma(n, -kLn2Lo, r);
-    const double p = poly2<14>(kExp, r);
-    const int ni = __double2loint(t);  // low word of t holds n (two's complement)
-    return __hiloint2double(__double2hiint(p) + (ni << 20), __double2loint(p));
-}
-
-__device__ __forceinline__ double flog_unit(double u) {
-    int hi = __double2hiint(u);
-    const int lo = __double2loint(u);
-    int k = (hi >> 20) - 1023;
-    hi = (hi & 0x000fffff) | 0x3ff00000;
-    if (hi > 0x3ff6a09e) {  // m > ~sqrt(2): use m/2, k+1
-        hi -= 0x00100000;
-        k += 1;
-    }
-    const double f = __hiloint2double(hi, lo) - 1.0;  // exact, |f| <= 0.4143
-    const double s = fdiv(f, 2.0 + f);
-    const double z = s * s;
-    const double p = poly2<11>(kAtanh, z);
-    // k -> double without the XU conversion pipe: (2^52 + 2^31 + k) - (2^52 + 2^31)
-    const double dk = __hiloint2double(0x43300000, k ^ 0x80000000) - 4503601774854144.0;
-    return fma(dk, kLn2Hi, fma(dk, kLn2Lo, s * p));
-}
-
-__device__ __forceinline__ void fsincos_2pi(double u, double& sn, double& cs) {
-    const double t = fma(4.0, u, kRound);        // quadrant in the low word of t
-    const double q = t - kRound;                  // rint(4u), 0..4
-    const double f = fma(-0.25, q, u);            // exact, |f| <= 1/8
-    const double z = f * f;
-    const double ps = poly2<10>(kSin, z);
-    const double pc = poly2<9>(kCos, z);
-    const double s0 = ps * f;
-    const int qi = __double2loint(t) & 3;
-    // angle = q pi/2 + 2 pi f
-    const double a = (qi & 1) ? pc : s0;
-    const double b = (qi & 1) ? s0 : pc;
-    sn = (qi & 2) ? -a : a;
-    cs = ((qi + 1) & 2) ? -b : b;
 }
 
 }  // namespace fm
