@@ -234,6 +234,18 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     a.box[1] = dom.xmax - sbox;
     a.box[2] = dom.ymin + sbox;
     a.box[3] = dom.ymax - sbox;
+    // integer form of the box test (performance mode): for positive doubles a
+    // strictly larger high word means a strictly larger value, so comparing
+    // high words is a conservative (slightly smaller) box.  Needs the box in
+    // the positive quadrant; otherwise it never fires and every step takes
+    // the exact path.
+    const bool pos = a.box[0] > 0.0 && a.box[2] > 0.0 && a.box[0] < a.box[1] && a.box[2] < a.box[3];
+    for (int k = 0; k < 4; ++k) {
+        int64_t bits;
+        std::memcpy(&bits, &a.box[k], 8);
+        a.box_hi[k] = static_cast<int32_t>(bits >> 32);
+    }
+    if (!pos) a.box_hi[0] = a.box_hi[2] = INT32_MAX;
     a.seed = cfg.seed;
     a.rk = make_round_keys(cfg.seed);
     a.max_steps32 = static_cast<uint32_t>(std::min<int64_t>(cfg.max_steps, 0xFFFFFFFFLL));

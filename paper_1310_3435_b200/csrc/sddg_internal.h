@@ -34,6 +34,7 @@ struct WalkArgs {
     int scheme, bridge;
     double dt, sqrt2dt, lambda, nu2, bridge_thr;
     double box[4];  // inner box x0, x1, y0, y1 (edge distances > sqrt(bridge_thr))
+    int32_t box_hi[4];  // high words of box[] for the integer test (INT32_MAX: disabled)
     uint64_t seed;
     RoundKeys rk;
     uint32_t max_steps32;  // min(max_steps, 2^32-1)

@@ -121,11 +121,20 @@ template <typename Real>
 struct Dom {
     Real xmin, xmax, ymin, ymax;
     Real bx0, bx1, by0, by1;  // inner box: every edge distance > sqrt(40 dt)
+    int hx0, hx1, hy0, hy1;   // high words of the box edges (integer test)
     __device__ __forceinline__ bool inside(Real x, Real y) const {
         return x > xmin && x < xmax && y > ymin && y < ymax;  // geometry.hpp:38-40
     }
     __device__ __forceinline__ bool in_box(Real x, Real y) const {
         return x > bx0 && x < bx1 && y > by0 && y < by1;
+    }
+    // Conservative box test on the high words (fp64 performance mode): four
+    // integer compares instead of four FP64-pipe DSETPs.  A strictly larger
+    // high word of a positive double means a strictly larger value, and a
+    // negative x has a negative high word, so a true result implies in_box.
+    __device__ __forceinline__ bool in_box_hi(double x, double y) const {
+        const int xi = __double2hiint(x), yi = __double2hiint(y);
+        return xi > hx0 && xi < hx1 && yi > hy0 && yi < hy1;
     }
     // geometry.cpp:24-32
     __device__ __forceinline__ Real dist(Real x, Real y, int e) const {
@@ -264,7 +273,13 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
     constexpr bool FAST = DV >= DV_RING_AN;
     using Ops = RealOps<Real, FAST>;
     const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax),
-                        Real(a.box[0]), Real(a.box[1]), Real(a.box[2]), Real(a.box[3])};
+                        Real(a.box[0]), Real(a.box[1]), Real(a.box[2]), Real(a.box[3]),
+                        a.box_hi[0], a.box_hi[1], a.box_hi[2], a.box_hi[3]};
+    // the inner-box test used by the step loop
+    auto box_test = [&](Real px, Real py) {
+        if constexpr (walk_uses_tables<DV, Real>()) return dom.in_box_hi(px, py);
+        else return dom.in_box(px, py);
+    };
     const DensityParams P{a.R, a.alpha, a.fd_h};
     const Real dt = Real(a.dt);
     const Real sq2dt = Real(a.sqrt2dt);
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             rng.init(a.pid[node], L.walk, 0);
         };
         start_walk(L.g);
-        bool in_box = dom.in_box(x, y);
+        bool in_box = box_test(x, y);
         uint32_t step = 0;
 #ifndef SDDG_WALK_NO_UNROLL
 #pragma unroll 2  // two step copies: x, y alternate registers (no loop-carried moves)
@@ -360,7 +375,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             if constexpr (SCHEME == 0 && BRIDGE) {
                 // inner box first: box inside the domain, so both ends in the
                 // box means no exit and no bridge draw (the common step)
-                nb = dom.in_box(nxp, nyp);
+                nb = box_test(nxp, nyp);
                 if (!(nb && in_box)) {
                     if (!dom.inside(nxp, nyp)) {
                         segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
@@ -400,7 +415,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 rng.init(a.pid[node], L.walk, epoch);
                 x = Real(a.px[node]);
                 y = Real(a.py[node]);
-                in_box = dom.in_box(x, y);
+                in_box = box_test(x, y);
                 step = 0;
                 continue;
             }
@@ -431,7 +446,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             if (gn >= a.total) break;
             L.g = gn;
             start_walk(gn);
-            in_box = dom.in_box(x, y);
+            in_box = box_test(x, y);
             step = 0;
         }
     }
