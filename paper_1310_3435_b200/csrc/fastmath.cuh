@@ -56,21 +56,24 @@ __device__ __forceinline__ double fsqrt_pos(double v) {
 //
 // Table sizes: 2^kExBits entries of 2^(j/N) for exp, 2^kLgBits of (1/c, log c)
 // for log, 2^kScBits of (sin, cos)(2 pi j/N).  The default (large) tables fill
-// 64 KB and let every polynomial drop two degrees; they need one 1024-thread
-// CTA per SM (walk_kernel.cuh).  SDDG_FM_SMALL selects the 7.9 KB set that
-// fits 8 x 128-thread CTAs per SM.
+// 96 KB and leave polynomials of degree 3 (exp), 4 (log1p) and 5/4 (sin/cos);
+// they need one 1024-thread CTA per SM (walk_kernel.cuh).  Bigger tables buy
+// no further degree (the next terms stay above 2^-53).  SDDG_FM_SMALL selects
+// the 7.9 KB set that fits 8 x 128-thread CTAs per SM.
 namespace sddg {
 namespace fm {
 
-#ifdef SDDG_FM_SMALL
-constexpr int kExBits = 6, kLgBits = 7, kScBits = 8;
+#if defined(SDDG_FM_SMALL)
+constexpr int kExBits = 6, kLgBits = 7, kScBits = 8;      // 7.9 KB
+#elif defined(SDDG_FM_MEDIUM)
+constexpr int kExBits = 10, kLgBits = 10, kScBits = 11;   // 56 KB (A/B: 2.9% slower)
 #else
-constexpr int kExBits = 10, kLgBits = 10, kScBits = 11;
+constexpr int kExBits = 12, kLgBits = 11, kScBits = 11;   // 96 KB
 #endif
 constexpr int kExN = 1 << kExBits, kLgN = 1 << kLgBits, kScN = 1 << kScBits;
 // first j with c_j = 1 + (j + 1/2)/kLgN >= sqrt 2 (log(c_j / 2) branch)
-constexpr int kLgSplit = kLgBits == 7 ? 53 : 424;
-static_assert(kLgBits == 7 || kLgBits == 10, "log split index");
+constexpr int kLgSplit = kLgBits == 7 ? 53 : (kLgBits == 10 ? 424 : 848);
+static_assert(kLgBits == 7 || kLgBits == 10 || kLgBits == 11, "log split index");
 
 struct FmTables {
     double k[32];          // polynomial / reduction constants (FmK), read with LDS so the
@@ -142,12 +145,15 @@ static __constant__ double kFmC[32] = {
 // x = -707.7 the scale exponent is clamped (one integer max instead of a
 // double fmax): the result stays a tiny positive normal instead of wrapping.
 __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
-    const double t = fma(x, kExScaleI, kRound);
+    const double t = kExBits >= 12 ? fma(x, FMK(K_EXS, kExScale), kRound) : fma(x, kExScaleI, kRound);
     const double n = t - kRound;
     double r = fma(n, -FMK(K_EXHI, kExHi), x);
     r = fma(n, -FMK(K_EXLO, kExLo), r);
     double p;
-    if constexpr (kExBits >= 10) {
+    if constexpr (kExBits >= 12) {
+        // e^r - 1 = r + r^2/2 + r^3/6  (|r| <= 8.5e-5: next term ~2e-18)
+        p = kE3i;
+    } else if constexpr (kExBits >= 10) {
         // e^r - 1 = r + r^2/2 + r^3/6 + r^4/24  (|r| <= 3.4e-4: next term ~4e-20)
         p = fma(r, kE4i, kE3i);
     } else {
@@ -184,7 +190,11 @@ __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     const double* e = T.lg[j];
     const double R = fma(m, e[0], 2.0);
     double p;
-    if constexpr (kLgBits >= 10) {
+    if constexpr (kLgBits >= 11) {
+        // log1p(r) = r - r^2/2 + r^3/3 - r^4/4 (|r| <= 2^-12: next term
+        // < 2e-19, 0.02 ulp of any |log u| >= 0.1), Horner in R = -2r
+        p = 0.03125;
+    } else if constexpr (kLgBits >= 10) {
         // log1p(r) = r - r^2/2 + r^3/3 - r^4/4 + r^5/5 (|r| <= 2^-11: next
         // term ~5e-18 relative), Horner in R = -2r
         p = fma(R, FMK(K_L5, 1.0 / 80.0), 0.03125);
