@@ -141,9 +141,11 @@ static __constant__ double kFmC[32] = {
     6.283185307179586 * 0x1.0p-53};
 #endif
 
-// exp(x), x <= 0: x = (N e + j) ln2/N + r, |r| <= ln2/(2N), N = kExN.  Below
-// x = -707.7 the scale exponent is clamped (one integer max instead of a
-// double fmax): the result stays a tiny positive normal instead of wrapping.
+// exp(x), x <= 0 (POS: x >= 0): x = (N e + j) ln2/N + r, |r| <= ln2/(2N),
+// N = kExN.  The scale exponent is clamped with integer min/max (instead of a
+// double fmax): below x = -707.7 the result stays a tiny positive normal, and
+// (POS) above 709 a huge finite one, instead of wrapping.
+template <bool POS = false>
 __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
     const double t = kExBits >= 12 ? fma(x, FMK(K_EXS, kExScale), kRound) : fma(x, kExScaleI, kRound);
     const double n = t - kRound;
@@ -165,7 +167,7 @@ __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
     p = fma(p, r, 0.5);
     p = fma(p, r, 1.0);
     p = p * r;
-    const int ni = max(__double2loint(t), -kExN * 1021);
+    const int ni = POS ? min(__double2loint(t), kExN * 1022) : max(__double2loint(t), -kExN * 1021);
     const double s = T.e2[ni & (kExN - 1)];
     const double v = fma(s, p, s);  // 2^(j/N) e^r
     return __hiloint2double(__double2hiint(v) + ((ni >> kExBits) << 20), __double2loint(v));
@@ -239,8 +241,9 @@ __device__ __forceinline__ void sincos_rotate(const FmTables& T, int j, double d
     const double cm1 = pc * d2;
     const double* e = T.sc[j];
     const double s0 = e[0], c0 = e[1];
-    sn = s0 + fma(c0, sd, s0 * cm1);
-    cs = c0 + fma(-s0, sd, c0 * cm1);
+    // big terms first: two roundings of size <= ulp/2 each (selftest <= 3 ulp)
+    sn = fma(s0, cm1, fma(c0, sd, s0));
+    cs = fma(c0, cm1, fma(-s0, sd, c0));
 }
 
 // sin, cos of 2 pi u, u in [0, 1): 2 pi u = 2 pi j/N + d, |d| <= pi/N

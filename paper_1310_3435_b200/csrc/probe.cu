@@ -91,6 +91,7 @@ __global__ void fastmath_check(int64_t n, const fm::FmTables* __restrict__ tg,
     atomicMax(&maxulp[0], ulp_diff(fm::fexp_tab(T, xe), exp(xe)));
     const double xe2 = -t * 40.0;
     atomicMax(&maxulp[0], ulp_diff(fm::fexp_tab(T, xe2), exp(xe2)));
+    atomicMax(&maxulp[0], ulp_diff(fm::fexp_tab<true>(T, -xe2), exp(-xe2)));  // ring: exp(+200 q^2)
     const double xl = exp2(-53.0 * t);
     if (xl <= 0.9) atomicMax(&maxulp[1], ulp_diff(fm::flog_tab(T, xl), log(xl)));
     if (t <= 0.9) atomicMax(&maxulp[1], ulp_diff(fm::flog_tab(T, t), log(t)));
