@@ -116,6 +116,31 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
+def pipe_fractions(steps_per_s, sm_mhz, precision):
+    """Issue-slot and FP64-pipe fractions of K1, live: the static SASS count of
+    one step (profiles/sass_walk_step.json, tools/sass_trace.py) x the measured
+    path-steps/s, over the SM's issue rate (4 warp-instructions/clk = 128
+    thread-instructions) and FP64 rate (64 lanes/clk) at the sampled clock.
+    These count useful (active-lane) work only."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "sass_walk_step.json")))
+        k = d["fp64_ring" if precision == "fp64" else "fp32_shock"]
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        hz = (sm_mhz or 0) * 1e6
+        if not hz:
+            return None
+        out = {"sass_instructions_per_step": k["instructions_per_step"],
+               "issue_frac": k["instructions_per_step"] * steps_per_s / (sms * 128 * hz),
+               "source": "profiles/sass_walk_step.json (cuobjdump trace of the hot step) x live "
+                         "path-steps/s / (SMs x 128 thread-instr/clk x sampled SM clock)"}
+        if precision == "fp64":
+            out["sass_fp64_per_step"] = k["fp64_per_step"]
+            out["fp64_pipe_frac"] = k["fp64_per_step"] * steps_per_s / (sms * 64 * hz)
+        return out
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def ncu_summary():
     """Pipe / issue utilisation of K1 from the committed ncu capture
     (profiles/ncu_walk_summary.json; measured with ncu, not in this run)."""
@@ -395,6 +420,8 @@ def main():
                          "peak_source": "measured on this GPU by sddg_probe_fma_peak (independent "
                                         "FMA chains; MEASURED_PEAKS.json has no non-tensor peak)",
                          "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64,
+                         "pipes": pipe_fractions(value / world, clk.get("sm_mhz") if clk else None,
+                                                 args.precision),
                          "ncu": ncu_summary()},
             "gpu_launches": launches,
             "clocks": clk,
