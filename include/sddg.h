@@ -222,8 +222,7 @@ typedef struct {
     int64_t max_iters; /* 0: 200 max(nx,ny)^2 */
     int32_t init_blend;
     int32_t method; /* sddg_solver_method */
-    double omega;   /* SOR factor; <= 0: start at the grid's Laplace optimum and adapt
-                       it on the device from the observed convergence rate */
+    double omega;   /* SOR factor; <= 0 picks the optimal one for the grid */
 } sddg_solver_config;
 
 typedef struct {

@@ -485,9 +485,7 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     double omega = sc.omega;
     if (sc.method == SDDG_SOLVER_RBSOR && !(omega > 0.0)) {
         const double kPi = 3.14159265358979323846;
-        // Laplace-optimal start, adapted on the device (negative = adaptive,
-        // solver.cu OmegaAdapt)
-        omega = -2.0 / (1.0 + std::sin(kPi / (max_dim_all - 1)));
+        omega = 2.0 / (1.0 + std::sin(kPi / (max_dim_all - 1)));
     }
     if (sc.method == SDDG_SOLVER_JACOBI) omega = 1.0;
     const size_t wbytes = sizeof(double) * static_cast<size_t>(gnx) * gny;

@@ -44,38 +44,6 @@ struct BlockMax {
     }
 };
 
-// Adaptive SOR factor (Hageman & Young): every 16 sweeps the decay rate lam
-// of the max update over the window gives the Jacobi spectral radius through
-// (lam + w - 1)^2 = lam w^2 mu^2, and w moves up to 2 / (1 + sqrt(1 - mu^2)).
-// The grid's Laplace-optimal w is the start: with strongly varying weights
-// the true mu is larger and the fixed w converges O(n) times slower (the
-// config-3 straggler).  Only increases; a w at or above the optimum keeps
-// lam = w - 1, which maps back to itself.  Every thread sees the same reduced
-// updates, so w stays uniform and the solve deterministic.  Enabled by a
-// negative omega (runtime.cu: the automatic choice).
-struct OmegaAdapt {
-    double w;
-    bool on;
-    int64_t mark_it;
-    double mark;
-    __device__ explicit OmegaAdapt(double omega)
-        : w(fabs(omega)), on(omega < 0.0), mark_it(0), mark(-1.0) {}
-    __device__ __forceinline__ void update(int64_t it, double upd) {
-        if (!on || (it & 15) != 0) return;
-        if (mark > 0.0 && upd > 0.0 && upd < mark) {
-            const double lam = pow(upd / mark, 1.0 / static_cast<double>(it - mark_it));
-            const double t = lam + w - 1.0;
-            const double mu2 = t * t / (lam * w * w);
-            if (mu2 < 1.0) {
-                const double wn = 2.0 / (1.0 + sqrt(1.0 - mu2));
-                if (wn > w + 1e-3) w = fmin(wn, 1.99);
-            }
-        }
-        mark = upd;
-        mark_it = it;
-    }
-};
-
 template <int METHOD, int PTS>
 __global__ void __launch_bounds__(kSolveThreads)
 solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
@@ -163,7 +131,6 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     // colour passes: METHOD 0 one pass over all interior points; METHOD 1
     // two passes (i+j even, then odd) updated in place.
     const int half = (mi + 1) / 2;
-    OmegaAdapt om(omega);
     while (iters < max_iters) {
         ++iters;
         double lupd = 0.0;
@@ -200,7 +167,7 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
                     const double xp = (cE[c] * u[c + 1] + cE[c - 1] * u[c - 1]) * ihx2;
                     const double yp = (cN[c] * u[c + nx] + cN[c - nx] * u[c - nx]) * ihy2;
                     const double gs = (xp + yp) * inv[c];
-                    const double nv = u[c] + om.w * (gs - u[c]);
+                    const double nv = u[c] + omega * (gs - u[c]);
                     const double du = fabs(nv - u[c]);
                     lupd = lupd < du ? du : lupd;
                     u[c] = nv;
@@ -209,7 +176,6 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
             }
         }
         upd = BlockMax::reduce(lupd, red);  // includes the barrier publishing u
-        if (METHOD == 1) om.update(iters, upd);
         if (upd < tol) {
             if (upd == 0.0 || upd < 1e-4 * tol) {
                 conv = true;
@@ -417,7 +383,6 @@ solve_large_kernel(const double* __restrict__ wg, int gnx, double ihx2, double i
     double* cur = u;
     double* nxt = v;
     const int half = (mi + 1) / 2;
-    OmegaAdapt om(omega);
     while (iters < max_iters) {
         ++iters;
         double lupd = 0.0;
@@ -441,7 +406,7 @@ solve_large_kernel(const double* __restrict__ wg, int gnx, double ihx2, double i
                     const double xp = (cE[c] * cur[c + 1] + cE[c - 1] * cur[c - 1]) * ihx2;
                     const double yp = (cN[c] * cur[c + nx] + cN[c - nx] * cur[c - nx]) * ihy2;
                     const double gs = (xp + yp) * inv[c];
-                    const double nv = cur[c] + om.w * (gs - cur[c]);
+                    const double nv = cur[c] + omega * (gs - cur[c]);
                     const double du = fabs(nv - cur[c]);
                     lupd = lupd < du ? du : lupd;
                     cur[c] = nv;
@@ -454,7 +419,6 @@ solve_large_kernel(const double* __restrict__ wg, int gnx, double ihx2, double i
         grid.sync();
         upd = __longlong_as_double(static_cast<long long>(slots[s]));
         if (gtid == 0) slots[(s + 2) % 3] = 0ull;  // next-but-one iteration's slot
-        if (METHOD == 1) om.update(iters, upd);
         if (METHOD == 0) {
             double* t = cur;
             cur = nxt;
