@@ -468,13 +468,16 @@ template <int DV, typename Real, int SCHEME, bool BRIDGE>
 cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
     constexpr size_t sm = walk_smem<DV, Real>();
     if constexpr (sm > 48 * 1024) {
-        static bool attr = false;  // once per process and variant (the device is fixed per ctx)
-        if (!attr) {
+        // once per device and variant (a process may drive several devices)
+        static bool attr[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64 || !attr[dev]) {
             const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(sm));
             if (e != cudaSuccess) return e;
-            attr = true;
+            if (dev >= 0 && dev < 64) attr[dev] = true;
         }
     }
     walk_kernel<DV, Real, SCHEME, BRIDGE><<<grid, walk_block<DV, Real>(), sm, s>>>(a);
