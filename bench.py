@@ -116,7 +116,7 @@ class ClockSampler:
                 "power_w_max": max(power) if power else None}
 
 
-def pipe_fractions(steps_per_s, sm_mhz, precision):
+def pipe_fractions(steps_per_s, sm_mhz, precision, sms):
     """Issue-slot and FP64-pipe fractions of K1, live: the static SASS count of
     one step (profiles/sass_walk_step.json, tools/sass_trace.py) x the measured
     path-steps/s, over the SM's issue rate (4 warp-instructions/clk = 128
@@ -125,7 +125,6 @@ def pipe_fractions(steps_per_s, sm_mhz, precision):
     try:
         d = json.load(open(os.path.join(ROOT, "profiles", "sass_walk_step.json")))
         k = d["fp64_ring" if precision == "fp64" else "fp32_shock"]
-        sms = torch.cuda.get_device_properties(0).multi_processor_count
         hz = (sm_mhz or 0) * 1e6
         if not hz:
             return None
@@ -137,7 +136,7 @@ def pipe_fractions(steps_per_s, sm_mhz, precision):
             out["sass_fp64_per_step"] = k["fp64_per_step"]
             out["fp64_pipe_frac"] = k["fp64_per_step"] * steps_per_s / (sms * 64 * hz)
         return out
-    except (OSError, KeyError, ValueError):
+    except (OSError, KeyError, ValueError, TypeError):
         return None
 
 
@@ -421,7 +420,9 @@ def main():
                                         "FMA chains; MEASURED_PEAKS.json has no non-tensor peak)",
                          "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64,
                          "pipes": pipe_fractions(value / world, clk.get("sm_mhz") if clk else None,
-                                                 args.precision),
+                                                 args.precision,
+                                                 torch.cuda.get_device_properties(
+                                                     torch.cuda.current_device()).multi_processor_count),
                          "ncu": ncu_summary()},
             "gpu_launches": launches,
             "clocks": clk,
