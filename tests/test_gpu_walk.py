@@ -316,3 +316,25 @@ def test_config3_fp32_vs_fp64_exceedances_against_null(ctx):
     assert len(z) > 20000
     assert np.sum(np.abs(z) > 4) <= 10
     assert 0.9 <= np.mean(z ** 2) <= 1.1
+
+
+def test_device_api_matches_host_api(ctx):
+    # sddg_mc_estimate_batch_device (HBM-resident inputs and records, caller's
+    # stream) must give the host-buffer call's records bit for bit
+    import torch
+    m = sdd.MonitorFunction.ring(analytic=True)
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(UNIT, 65, 65))
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=900, seed=9)
+    rng = np.random.default_rng(4)
+    pts = rng.uniform(0.05, 0.95, (37, 2))
+    pid = rng.integers(0, 1 << 47, 37).astype(np.uint64)
+    want = sdd.mc_estimate_batch(pts, pid, m, UNIT, bd, cfg, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    px = torch.tensor(pts[:, 0], dtype=torch.float64, device=dev)
+    py = torch.tensor(pts[:, 1], dtype=torch.float64, device=dev)
+    tp = torch.tensor(pid.view(np.int64), dtype=torch.int64, device=dev)
+    out = torch.zeros(37 * 128, dtype=torch.uint8, device=dev)
+    st = torch.cuda.Stream()
+    sdd.mc_estimate_batch_device(px, py, tp, out, m, UNIT, bd, cfg, ctx=ctx, stream=st)
+    st.synchronize()
+    assert out.cpu().numpy().tobytes() == want.tobytes()
