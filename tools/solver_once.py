@@ -1,0 +1,35 @@
+"""One K3 batch for ncu captures: the 2048 x 129^2 RB-SOR batch of
+tools/config_sweep.py (shock weights, tol 1e-10), working set >> L2.
+python tools/solver_once.py [n_jobs]"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1310_3435_b200 import sdd  # noqa: E402
+
+n_jobs = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+ctx = sdd.Context(0)
+g, subs_n = 1025, 8
+spec = sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), g, g)
+lay = sdd.build_layout(spec, subs_n, subs_n)
+bxy = lay.block_x + 1
+rng = np.random.default_rng(3)
+jobs, bcs = [], []
+for s in range(n_jobs):
+    q = s % lay.subdomain_count()
+    jobs.append(lay.subdomain(q % subs_n, q // subs_n))
+    v = np.sort(rng.random(4))
+    e = lambda a, b: np.linspace(a, b, bxy)  # noqa: E731
+    bcs.append(sdd.EdgeData(e(v[0], v[1]), e(v[2], v[3]), e(v[0], v[2]), e(v[1], v[3])))
+x = np.linspace(0, 1, g)
+X, Y = np.meshgrid(x, x)
+w = (1.0 + 20.0 / np.cosh(50 * (Y - 0.5 - 0.15 * np.sin(2 * np.pi * X))) ** 2).ravel()
+res = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), jobs, bcs,
+                                sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx)
+st = ctx.last_stats()
+its = np.array([r.iterations for r in res])
+upd = float(np.sum(its) * (bxy - 2) ** 2)
+print(f"{n_jobs} x {bxy}^2 rbsor: {st['kernel_ms']:.2f} ms, sweeps mean {its.mean():.1f} max {its.max()}, "
+      f"{upd / (st['kernel_ms'] / 1e3):.3e} point-updates/s, {upd * 40 / (st['kernel_ms'] / 1e3) / 1e9:.0f} GB/s at 40 B")
