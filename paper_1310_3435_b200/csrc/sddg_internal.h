@@ -56,6 +56,7 @@ struct WalkArgs {
     uint32_t* rec_meta;  // edge | epochs_used << 2
     sddg_path* dump;
     const void* fm_tables;  // fastmath.cuh FmTables in global memory (performance mode)
+    double inv_dt;          // 1/dt: performance-mode bridge exponent d0 d1 / dt as a multiply
 };
 
 // fastmath tables (host-built in long double, uploaded once per context)

@@ -230,6 +230,77 @@ __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real 
     return false;
 }
 
+// Performance-mode bridge test (SCHEME 0, fp32 walks).  pe = d0 d1 of edge
+// e, exactly the products the reference forms (sde.cpp:83-92).  Only edges
+// with ex = pe / dt <= 40 draw (here pe * (1/dt)), and the sort order matters
+// only among those: with one such edge (all but corner steps) the sort is
+// skipped.  Skipped edges draw nothing, so the stream is consumed exactly as
+// in edge_crossing.
+template <typename Real>
+__device__ __forceinline__ uint32_t sorted_edge_order(const Dom<Real>& d, Real x0, Real y0,
+                                                      Real x1, Real y1) {
+    Real s[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const Real k = d.dist(x0, y0, e), m = d.dist(x1, y1, e);
+        s[e] = m < k ? m : k;  // std::min
+    }
+    // rank of edge e in the (min(d0,d1), id) order
+    uint32_t order = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        int r = 0;
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+            if (f != e) r += (s[f] < s[e] || (s[f] == s[e] && f < e)) ? 1 : 0;
+        order |= static_cast<uint32_t>(e) << (4 * r);
+    }
+    return order;
+}
+
+// The rare path as a real subroutine: ptxas allocates the step loop's
+// registers without it (inlined, its temporaries cost the step loop
+// constant-bank operand forms or spills).  State in and out by value.
+struct BridgeRes {
+    double hx, hy;
+    uint32_t n, cw2, cw3;
+    int edge;  // -1: no exit
+};
+
+template <typename Real>
+__device__ __noinline__ BridgeRes bridge_rare(Real x0, Real y0, Real x1, Real y1, int mask,
+                                              LaneStream rng, const WalkArgs* a,
+                                              const fm::FmTables* T) {
+    const Dom<Real> d{Real(a->xmin), Real(a->xmax), Real(a->ymin), Real(a->ymax)};
+    const Real idt = Real(a->inv_dt);
+    uint32_t order = 0x3210u;
+    if (mask & (mask - 1)) order = sorted_edge_order(d, x0, y0, x1, y1);
+    BridgeRes r;
+    r.edge = -1;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i, order >>= 4) {
+        const int e = static_cast<int>(order & 15u);
+        if (!((mask >> e) & 1)) continue;
+        const Real d0 = d.dist(x0, y0, e), d1 = d.dist(x1, y1, e);
+        const Real ex = d0 * d1 * idt;
+        const Real u = RealOps<Real, true>::u(rng.next_one(a->rk));
+        if (u < RealOps<Real, true>::ex(*T, -ex)) {
+            const Real sum = d0 + d1;
+            const Real sc = sum > Real(0) ? d0 / sum : Real(0);
+            Real hx = x0 + sc * (x1 - x0), hy = y0 + sc * (y1 - y0);
+            d.project(e, hx, hy);
+            r.hx = hx;
+            r.hy = hy;
+            r.edge = e;
+            break;
+        }
+    }
+    r.n = rng.n;
+    r.cw2 = rng.cw2;
+    r.cw3 = rng.cw3;
+    return r;
+}
+
 // table_at / f_at / g_at (proj/src/boundary.cpp:10-42)
 __device__ __forceinline__ double table_at(const double* __restrict__ t, int n, double s) {
     int k = static_cast<int>(floor(s));
@@ -386,9 +457,30 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                         const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
                         const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
                         const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
-                        if (pB <= thr || pT <= thr || pL <= thr || pR <= thr)
+                        if constexpr (FAST && sizeof(Real) == 4) {
+                            // fp32: out of line (A/B +2.4%); fp64 keeps the inline test below
+                            // (out of line it costs the step loop a local-memory round trip: -0.5%)
+                            const Real idt = Real(a.inv_dt);
+                            const int mask = int(!(pB * idt > Real(40))) |
+                                             (int(!(pT * idt > Real(40))) << 1) |
+                                             (int(!(pL * idt > Real(40))) << 2) |
+                                             (int(!(pR * idt > Real(40))) << 3);
+                            if (mask) {
+                                const BridgeRes r = bridge_rare<Real>(x, y, nxp, nyp, mask, rng, &a, &T);
+                                rng.n = r.n;
+                                rng.cw2 = r.cw2;
+                                rng.cw3 = r.cw3;
+                                if (r.edge >= 0) {
+                                    hx = Real(r.hx);
+                                    hy = Real(r.hy);
+                                    edge = r.edge;
+                                    exited = true;
+                                }
+                            }
+                        } else if (pB <= thr || pT <= thr || pL <= thr || pR <= thr) {
                             exited = edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T,
                                                                   rng, hx, hy, edge);
+                        }
                     }
                 }
             } else if (!dom.inside(nxp, nyp)) {

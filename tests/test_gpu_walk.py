@@ -207,6 +207,23 @@ def test_analytic_drift_tracks_reference_fd_paths(ctx):
     assert np.max(np.abs(a["f"][same] - r["f"][same])) < 1e-6
 
 
+@pytest.mark.parametrize("start", [(0.03, 0.03), (0.5, 0.02), (0.97, 0.96), (0.02, 0.5)])
+def test_analytic_bridge_test_tracks_reference_near_edges_and_corners(ctx, start):
+    # Performance mode tests the bridge with d0 d1 * (1/dt), skips the edge
+    # sort when one edge qualifies and runs it out of line (walk_kernel.cuh
+    # bridge_rare).  Near a corner at a coarse dt two edges qualify on many
+    # steps, so the sorted order and the draw sequence are both exercised.
+    bd = sdd.make_boundary_data(sdd.MonitorFunction.ring(), sdd.GridSpec(UNIT, 65, 65))
+    cfg = sdd.WalkConfig(scheme="linear", dt=2e-4, walks=1, seed=7)
+    pid = 4242
+    a = sdd.walk_dump(start, pid, sdd.MonitorFunction.ring(True), UNIT, bd, cfg, 0, 4000, ctx=ctx)
+    r = sdd.walk_dump(start, pid, sdd.MonitorFunction.ring(False), UNIT, bd, cfg, 0, 4000, ctx=ctx)
+    same = (a["steps"] == r["steps"]) & (a["edge"] == r["edge"])
+    assert same.mean() >= 0.99
+    assert np.max(np.abs(a["ex"][same] - r["ex"][same])) < 1e-6
+    assert np.max(np.abs(a["ey"][same] - r["ey"][same])) < 1e-6
+
+
 @pytest.mark.parametrize("kind", [sdd.RING_W, sdd.SHOCK_W, sdd.TWOBUMP_W])
 def test_fp32_walks_agree_statistically_with_fp64(ctx, kind):
     m = sdd.MonitorFunction.weight(kind, analytic=True)
@@ -233,6 +250,22 @@ def test_fp32_paths_track_fp64_paths(ctx):
     b = sdd.walk_dump((0.5, 0.5), 2112, m, UNIT, bd, c32, 0, 1000, ctx=ctx)
     assert np.mean(a["edge"] == b["edge"]) >= 0.9
     assert abs(np.mean(a["f"]) - np.mean(b["f"])) < 0.05
+
+
+@pytest.mark.parametrize("start", [(0.03, 0.03), (0.97, 0.96), (0.5, 0.02)])
+def test_fp32_bridge_test_near_corners_tracks_fp64(ctx, start):
+    # fp32 runs the bridge test out of line with the sort skipped when one
+    # edge qualifies (walk_kernel.cuh bridge_rare); short walks near a corner
+    # (two qualifying edges on many steps) follow the fp64 paths step for step
+    m = sdd.MonitorFunction.ring(analytic=True)
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(UNIT, 65, 65))
+    c64 = sdd.WalkConfig(scheme="linear", dt=2e-4, walks=1, seed=3)
+    c32 = sdd.WalkConfig(scheme="linear", dt=2e-4, walks=1, seed=3, precision="fp32")
+    a = sdd.walk_dump(start, 99, m, UNIT, bd, c64, 0, 4000, ctx=ctx)
+    b = sdd.walk_dump(start, 99, m, UNIT, bd, c32, 0, 4000, ctx=ctx)
+    same = (a["edge"] == b["edge"]) & (a["steps"] == b["steps"])
+    assert same.mean() >= 0.95
+    assert np.max(np.abs(a["ex"][same] - b["ex"][same])) < 1e-3
 
 
 def test_config2_subsample_parity_with_oracle(ctx, oracle):
