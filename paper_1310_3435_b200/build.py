@@ -28,7 +28,10 @@ COMMON = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-I" + os.path.join(ROOT, "include")]
 UNITS = {
     "walk_ref.cu": ["-fmad=false"],
-    "walk_fast.cu": ["-fmad=true", "-ftz=true"],  # fp32 walks: no denormal fix-ups around SFU ops
+    # fp32 walks: no denormal fix-ups around SFU ops.  SDDG_SMEM_ABS: the
+    # fastmath tables' offset in the shared window (1 KB reserved, no static
+    # shared memory; checked at kernel entry)
+    "walk_fast.cu": ["-fmad=true", "-ftz=true", "-DSDDG_SMEM_ABS=0x400"],
     "reduce.cu": ["-fmad=false"],
     "solver.cu": ["-fmad=false"],
     "mesh.cu": ["-fmad=false"],

@@ -15,6 +15,8 @@
 // immediate coefficients.  Accuracy ~1 ulp (sddg_selftest_fastmath).  The
 // reference-parity kernels keep the CUDA library (walk_ref.cu).
 #pragma once
+#include <cstddef>
+#include <cstdint>
 
 namespace sddg {
 namespace fm {
@@ -83,6 +85,25 @@ struct FmTables {
                            // so that log(rc_j) is within 2^-8 ulp of a double (no lo part)
     double sc[kScN][2];    // sin, cos of 2 pi j / kScN
 };
+
+// Table reads.  SDDG_SMEM_ABS=<byte offset of the tables in the CTA's shared
+// window>: plain ld.shared at [index + constant], so ptxas does not rebuild
+// the dynamic-shared-memory symbol address (S2UR CgaCtaId + 3 uniform ops)
+// inside the step loop.  The kernel checks the offset at entry.
+#ifdef SDDG_SMEM_ABS
+#define SDDG_STR2(x) #x
+#define SDDG_STR(x) SDDG_STR2(x)
+__device__ __forceinline__ double tab_ld1(uint32_t off) {
+    double r;
+    asm("ld.shared.f64 %0, [%1+" SDDG_STR(SDDG_SMEM_ABS) "];" : "=d"(r) : "r"(off));
+    return r;
+}
+__device__ __forceinline__ void tab_ld2(uint32_t off, double& a, double& b) {
+    asm("ld.shared.v2.f64 {%0, %1}, [%2+" SDDG_STR(SDDG_SMEM_ABS) "];"
+        : "=d"(a), "=d"(b)
+        : "r"(off));
+}
+#endif
 
 // indices into FmTables::k (pairs adjacent in use order -> LDS.128)
 enum FmK {
@@ -168,7 +189,11 @@ __device__ __forceinline__ double fexp_tab(const FmTables& T, double x) {
     p = fma(p, r, 1.0);
     p = p * r;
     const int ni = POS ? min(__double2loint(t), kExN * 1022) : max(__double2loint(t), -kExN * 1021);
+#ifdef SDDG_SMEM_ABS
+    const double s = tab_ld1(offsetof(FmTables, e2) + 8u * static_cast<uint32_t>(ni & (kExN - 1)));
+#else
     const double s = T.e2[ni & (kExN - 1)];
+#endif
     const double v = fma(s, p, s);  // 2^(j/N) e^r
     return __hiloint2double(__double2hiint(v) + ((ni >> kExBits) << 20), __double2loint(v));
 }
@@ -189,8 +214,14 @@ __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     const int j = (hi >> (20 - kLgBits)) & (kLgN - 1);
     const int nk = (1023 - (hi >> 20)) - (j >= kLgSplit ? 1 : 0);  // -k >= 0
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+#ifdef SDDG_SMEM_ABS
+    double e0, e1;
+    tab_ld2(offsetof(FmTables, lg) + 16u * static_cast<uint32_t>(j), e0, e1);
+#else
     const double* e = T.lg[j];
-    const double R = fma(m, e[0], 2.0);
+    const double e0 = e[0], e1 = e[1];
+#endif
+    const double R = fma(m, e0, 2.0);
     double p;
     if constexpr (kLgBits >= 11) {
         // log1p(r) = r - r^2/2 + r^3/3 - r^4/4 (|r| <= 2^-12: next term
@@ -211,7 +242,7 @@ __device__ __forceinline__ double fm2log_tab(const FmTables& T, double u) {
     p = p * R;
     // -k as a double without the conversion pipe: (2^52 + nk) - 2^52
     const double dnk = __hiloint2double(0x43300000, nk) - 4503599627370496.0;
-    const double h = fma(dnk, FMK(K_LN2HI, 2.0 * kLn2Hi), e[1]);
+    const double h = fma(dnk, FMK(K_LN2HI, 2.0 * kLn2Hi), e1);
     return h + fma(dnk, FMK(K_LN2LO, 2.0 * kLn2Lo), fma(p, R, R));
 }
 
@@ -239,8 +270,13 @@ __device__ __forceinline__ void sincos_rotate(const FmTables& T, int j, double d
     }
     const double sd = fma(ps * d2, d, d);
     const double cm1 = pc * d2;
+#ifdef SDDG_SMEM_ABS
+    double s0, c0;
+    tab_ld2(offsetof(FmTables, sc) + 16u * static_cast<uint32_t>(j), s0, c0);
+#else
     const double* e = T.sc[j];
     const double s0 = e[0], c0 = e[1];
+#endif
     // big terms first: two roundings of size <= ulp/2 each (selftest <= 3 ulp)
     sn = fma(s0, cm1, fma(c0, sd, s0));
     cs = fma(c0, cm1, fma(-s0, sd, c0));

@@ -294,6 +294,9 @@ void raise_kernel_error(const Counters& hc) {
     if (hc.err_flag == 4)
         fail(SDDG_ERR_NUMERICAL, "mc_estimate: walk failed to exit after 1024 restarts (point_id " +
                                      std::to_string(hc.err_info) + ")");
+    if (hc.err_flag == 5)
+        fail(SDDG_ERR_CUDA, "walk kernel: dynamic shared memory at offset " +
+                                std::to_string(hc.err_info) + ", not the compiled SDDG_SMEM_ABS");
 }
 
 // Walks + finalize for n device-resident nodes; estimates to d_out.

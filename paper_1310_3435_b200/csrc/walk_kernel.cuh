@@ -236,6 +236,10 @@ __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real 
 // only among those: with one such edge (all but corner steps) the sort is
 // skipped.  Skipped edges draw nothing, so the stream is consumed exactly as
 // in edge_crossing.
+#ifndef SDDG_FP32_BRIDGE_OOL_SHOCK
+#define SDDG_FP32_BRIDGE_OOL_SHOCK 0  // A/B: out of line the shock kernel needs 96 registers (-3.5%)
+#endif
+
 template <typename Real>
 __device__ __forceinline__ uint32_t sorted_edge_order(const Dom<Real>& d, Real x0, Real y0,
                                                       Real x1, Real y1) {
@@ -335,8 +339,17 @@ __host__ __device__ constexpr int walk_min_blocks() {
         return SDDG_WALK_TABLE_BLOCKS_PER_SM;
 #endif
     if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return 1;
+#ifdef SDDG_SHOCK32_MIN_BLOCKS
+    if constexpr (DV == DV_SHOCK_AN && sizeof(Real) == 4) return SDDG_SHOCK32_MIN_BLOCKS;
+#endif
     return (DV == DV_SHOCK_AN || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
 }
+
+template <int DV, typename Real>
+__host__ __device__ constexpr size_t walk_table_bytes() {
+    return walk_uses_tables<DV, Real>() ? sizeof(fm::FmTables) : 0;
+}
+static_assert(sizeof(fm::FmTables) % 16 == 0, "LaneState alignment after the tables");
 
 template <int DV, typename Real, int SCHEME, bool BRIDGE>
 __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Real>())
@@ -356,9 +369,23 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);
     const uint32_t max_steps = a.max_steps32;
-    // performance mode: elementary-function tables in (dynamic) shared memory
+    // Dynamic shared memory: the fastmath tables (performance-mode fp64) then
+    // the per-lane bookkeeping.  No static shared memory, so the tables sit at
+    // a fixed offset of the CTA's shared window (SDDG_SMEM_ABS, fastmath.cuh).
     extern __shared__ double dyn_smem[];
     fm::FmTables& T = *reinterpret_cast<fm::FmTables*>(dyn_smem);
+#ifdef SDDG_SMEM_ABS
+    if constexpr (walk_uses_tables<DV, Real>()) {
+        const uint32_t at = static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem));
+        if (at != static_cast<uint32_t>(SDDG_SMEM_ABS)) {
+            if (threadIdx.x == 0) {
+                atomicCAS(a.err_flag, 0, 5);
+                atomicExch(a.err_info, static_cast<unsigned long long>(at));
+            }
+            return;
+        }
+    }
+#endif
     if constexpr (walk_uses_tables<DV, Real>()) {
         const double2* src = reinterpret_cast<const double2*>(a.fm_tables);
         double2* dst = reinterpret_cast<double2*>(dyn_smem);
@@ -370,7 +397,8 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
     // Per-walk bookkeeping that only the rare exit / restart paths touch
     // (record slot, node, walk, epoch, step total) lives in shared memory, so
     // the step loop keeps its 64 registers for the step itself.
-    __shared__ LaneState lane_state[walk_block<DV, Real>()];
+    LaneState* lane_state = reinterpret_cast<LaneState*>(
+        reinterpret_cast<char*>(dyn_smem) + walk_table_bytes<DV, Real>());
     LaneState& L = lane_state[threadIdx.x];
     L.g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     L.steps = 0;
@@ -457,7 +485,8 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                         const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
                         const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
                         const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
-                        if constexpr (FAST && sizeof(Real) == 4) {
+                        if constexpr (FAST && sizeof(Real) == 4 &&
+                                      (SDDG_FP32_BRIDGE_OOL_SHOCK || DV != DV_SHOCK_AN)) {
                             // fp32: out of line (A/B +2.4%); fp64 keeps the inline test below
                             // (out of line it costs the step loop a local-memory round trip: -0.5%)
                             const Real idt = Real(a.inv_dt);
@@ -550,10 +579,11 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
         atomicAdd(a.steps, static_cast<unsigned long long>(my_steps));
 }
 
-// All (SCHEME, BRIDGE) instantiations of one drift variant.
+// All (SCHEME, BRIDGE) instantiations of one drift variant: dynamic shared
+// memory = tables + one LaneState per thread.
 template <int DV, typename Real>
 constexpr size_t walk_smem() {
-    return walk_uses_tables<DV, Real>() ? sizeof(fm::FmTables) : 0;
+    return walk_table_bytes<DV, Real>() + sizeof(LaneState) * walk_block<DV, Real>();
 }
 
 template <int DV, typename Real, int SCHEME, bool BRIDGE>
