@@ -121,9 +121,11 @@ int drift_variant(const sddg_density& d, int precision) {
     const bool builtin = d.kind >= SDDG_DENS_CONSTANT && d.kind <= SDDG_DENS_FIVE_RING;
     if (!wkind && !builtin) fail(SDDG_ERR_VALIDATION, "unknown density kind");
     if (d.grad_mode == SDDG_GRAD_ANALYTIC) {
+        if (d.kind == SDDG_DENS_FIVE_RING) return 35;  // DV_FIVE_RING_AN
         if (!wkind)
             fail(SDDG_ERR_VALIDATION,
-                 "analytic grad(w)/w drift exists for the BASELINE densities (kinds 16-18)");
+                 "performance-mode drift exists for the BASELINE densities (kinds 16-18) and "
+                 "the five-ring (kind 4)");
         return 32 + (d.kind - SDDG_DENS_RING_W);
     }
     if (d.grad_mode != SDDG_GRAD_REFERENCE) fail(SDDG_ERR_VALIDATION, "unknown grad_mode");
@@ -466,7 +468,8 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     (void)max_n;
     (void)max_int;
     (void)max_dim;
-    const bool coef_smem = sizeof(double) * 4 * static_cast<size_t>(max_n_s) <= smem_cap;
+    const int ncoef = sc.method == SDDG_SOLVER_RBSOR ? 4 : 3;  // solver.cu launch_solve_batch
+    const bool coef_smem = sizeof(double) * ((1 + ncoef) * static_cast<size_t>(max_n_s) + 1) <= smem_cap;
     const bool jacobi_small_ok = max_int_s <= solver_max_points();
     if (sc.method == SDDG_SOLVER_JACOBI && !jacobi_small_ok) {
         // Jacobi register budget exceeded: route those jobs to K3b as well
@@ -501,7 +504,7 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     int* derr = static_cast<int*>(c->s_err.ensure(sizeof(int)));
     double* dcoef = nullptr;
     if (!small.empty() && !coef_smem)
-        dcoef = static_cast<double*>(c->s_coef.ensure(sizeof(double) * 3 * max_n_s * small.size()));
+        dcoef = static_cast<double*>(c->s_coef.ensure(sizeof(double) * ncoef * max_n_s * small.size()));
     double* dlarge = nullptr;
     if (!large.empty())
         dlarge = static_cast<double*>(c->s_large.ensure(sizeof(double) * (5 * max_n_l + 8)));

@@ -61,7 +61,7 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     double* cN;
     double* inv;
     if (coef_in_smem) {
-        cE = smem + N;
+        cE = smem + ((N + 1) & ~1);  // 16-B aligned (RB-SOR reads it as double2)
         cN = cE + N;
         inv = cN + N;
     } else {
@@ -75,15 +75,39 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     const double* Rt = L + ny;
     const int tid = threadIdx.x, nt = blockDim.x;
 
+    const int mi = nx - 2, mj = ny - 2;
+    const int half = (mi + 1) / 2;  // RB-SOR: colour slots per row
+    const int nslots = mj * half;
+    if (METHOD == 1) {
+        // RB-SOR: per colour, per slot (j-1)*half + s, the four neighbour
+        // weights of point (i, j) pre-divided by the diagonal, (aE, aW) and
+        // (aN, aS): a coalesced 32 B per update instead of five scattered
+        // reads of cE/cN/inv_den.  Same half-point weights as the reference
+        // (detsolver.cpp:88-111); the pre-division only moves the rounding of
+        // the fixed point by an ulp.
+        double2* PQ = reinterpret_cast<double2*>(cE);
+        for (int q = tid; q < 2 * nslots; q += nt) {
+            const int colour = q / nslots, r = q - colour * nslots;
+            const int j = r / half + 1, i = 2 * (r % half) + 1 + ((j + 1 + colour) & 1);
+            if (i > mi) continue;
+            const double* wr = wg + (int64_t)(J.j0 + j) * gnx + (J.i0 + i);
+            const double wc = wr[0];
+            const double ce = 0.5 * (wc + wr[1]), cw = 0.5 * (wr[-1] + wc);
+            const double cn = 0.5 * (wc + wr[gnx]), cs = 0.5 * (wr[-gnx] + wc);
+            const double id = 1.0 / ((ce + cw) * ihx2 + (cn + cs) * ihy2);
+            PQ[colour * 2 * nslots + r] = make_double2(ce * ihx2 * id, cw * ihx2 * id);
+            PQ[colour * 2 * nslots + nslots + r] = make_double2(cn * ihy2 * id, cs * ihy2 * id);
+        }
+    }
     // coefficients from the global weights (detsolver.cpp:88-111)
-    for (int c = tid; c < N; c += nt) {
+    for (int c = tid; METHOD == 0 && c < N; c += nt) {
         const int i = c % nx, j = c / nx;
         const double wc = wg[(int64_t)(J.j0 + j) * gnx + (J.i0 + i)];
         cE[c] = i + 1 < nx ? 0.5 * (wc + wg[(int64_t)(J.j0 + j) * gnx + (J.i0 + i + 1)]) : 0.0;
         cN[c] = j + 1 < ny ? 0.5 * (wc + wg[(int64_t)(J.j0 + j + 1) * gnx + (J.i0 + i)]) : 0.0;
     }
     __syncthreads();
-    for (int c = tid; c < N; c += nt) {
+    for (int c = tid; METHOD == 0 && c < N; c += nt) {
         const int i = c % nx, j = c / nx;
         inv[c] = (i > 0 && j > 0 && i + 1 < nx && j + 1 < ny)
                      ? 1.0 / ((cE[c] + cE[c - 1]) * ihx2 + (cN[c] + cN[c - nx]) * ihy2)
@@ -122,7 +146,6 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     }
     __syncthreads();
 
-    const int mi = nx - 2, mj = ny - 2;
     const int64_t max_iters =
         max_iters_cfg > 0 ? max_iters_cfg : 200LL * (nx > ny ? nx : ny) * (nx > ny ? nx : ny);
     int64_t iters = 0;
@@ -130,7 +153,10 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     bool conv = false;
     // colour passes: METHOD 0 one pass over all interior points; METHOD 1
     // two passes (i+j even, then odd) updated in place.
-    const int half = (mi + 1) / 2;
+    // this thread's first slot and the per-iteration slot step (no divisions
+    // in the sweep)
+    const int j_first = tid / half + 1, s_first = tid % half;
+    const int dj = nt / half, ds = nt % half;
     while (iters < max_iters) {
         ++iters;
         double lupd = 0.0;
@@ -159,18 +185,48 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
         } else {
 #pragma unroll 1
             for (int colour = 0; colour < 2; ++colour) {
-                for (int p = tid; p < mj * half; p += nt) {
-                    const int j = p / half + 1;
-                    const int i = 2 * (p % half) + 1 + ((j + 1 + colour) & 1);
-                    if (i > mi) continue;
-                    const int c = j * nx + i;
-                    const double xp = (cE[c] * u[c + 1] + cE[c - 1] * u[c - 1]) * ihx2;
-                    const double yp = (cN[c] * u[c + nx] + cN[c - nx] * u[c - nx]) * ihy2;
-                    const double gs = (xp + yp) * inv[c];
-                    const double nv = u[c] + omega * (gs - u[c]);
-                    const double du = fabs(nv - u[c]);
-                    lupd = lupd < du ? du : lupd;
-                    u[c] = nv;
+                const double2* P = reinterpret_cast<const double2*>(cE) + colour * 2 * nslots;
+                const double2* Q = P + nslots;
+                int j = j_first, sl = s_first;
+                // groups of G slots: all coefficient loads of a group issue
+                // before its shared-memory stores (the compiler may not move
+                // loads of the possibly-aliased coefficient pointer past a
+                // store), so G L2 round trips overlap instead of serialising
+#ifndef SDDG_SOR_GROUP
+#define SDDG_SOR_GROUP 4
+#endif
+                constexpr int G = SDDG_SOR_GROUP;
+                for (int q0 = tid; q0 < nslots; q0 += G * nt) {
+                    double2 ew[G], ns[G];
+                    int cc[G];
+#pragma unroll
+                    for (int k = 0; k < G; ++k) {
+                        const int q = q0 + k * nt;
+                        const int i = 2 * sl + 1 + ((j + 1 + colour) & 1);
+                        cc[k] = (q < nslots && i <= mi) ? j * nx + i : -1;
+                        if (cc[k] >= 0) {
+                            ew[k] = P[q];
+                            ns[k] = Q[q];
+                        }
+                        sl += ds;
+                        j += dj;
+                        if (sl >= half) {
+                            sl -= half;
+                            ++j;
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < G; ++k) {
+                        const int c = cc[k];
+                        if (c < 0) continue;
+                        const double uc = u[c];
+                        const double gs = fma(ew[k].x, u[c + 1],
+                                              fma(ew[k].y, u[c - 1], fma(ns[k].x, u[c + nx], ns[k].y * u[c - nx])));
+                        const double nv = fma(omega, gs - uc, uc);
+                        const double du = fabs(nv - uc);
+                        lupd = lupd < du ? du : lupd;
+                        u[c] = nv;
+                    }
                 }
                 __syncthreads();
             }
@@ -240,8 +296,10 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
     if (n_jobs <= 0) return cudaSuccess;
     const double ihx2 = 1.0 / (hx * hx);
     const double ihy2 = 1.0 / (hy * hy);
-    const size_t smem = sizeof(double) * static_cast<size_t>(max_n) * (coef_in_smem ? 4 : 1);
-    const int64_t cstride = 3LL * max_n;
+    // Jacobi: u + cE, cN, inv_den (3 N); RB-SOR: u + 4 packed weights per slot (<= 4 N)
+    const int ncoef = method == SDDG_SOLVER_RBSOR ? 4 : 3;
+    const size_t smem = sizeof(double) * (static_cast<size_t>(max_n) * (coef_in_smem ? 1 + ncoef : 1) + 1);
+    const int64_t cstride = static_cast<int64_t>(ncoef) * max_n;
     const int grid = static_cast<int>(n_jobs);
     const int T = kSolveThreads;
     if (method == SDDG_SOLVER_RBSOR)
