@@ -62,7 +62,9 @@ typedef enum {
      * 0-4, the user_supplied central difference of rho = 1/w with step fd_h
      * for kinds 16-18 (proj/src/monitor.cpp:206-219). */
     SDDG_GRAD_REFERENCE = 0,
-    /* Analytic drift grad(w)/w for kinds 16-18 (BASELINE.json configs). */
+    /* Performance mode: analytic drift grad(w)/w for kinds 16-18 (BASELINE.json
+     * configs), and the five-ring (kind 4) with table-driven tanh; fastmath
+     * elementary functions, fp64 or fp32, checked statistically. */
     SDDG_GRAD_ANALYTIC = 1
 } sddg_grad_mode;
 

@@ -1085,7 +1085,7 @@ void make_fm_tables(void* out) {
 }
 
 bool walk_variant_supported(int dv, int precision) {
-    if (dv >= 32 && dv <= 34) return true;
+    if (dv >= 32 && dv <= 35) return true;  // walk_fast.cu: DV_RING_AN .. DV_FIVE_RING_AN
     return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18));
 }
 

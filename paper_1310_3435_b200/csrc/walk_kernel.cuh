@@ -105,7 +105,7 @@ template <int DV, typename Real>
 __device__ __forceinline__ bool drift(const DensityParams& P, const fm::FmTables& T, Real x, Real y,
                                       Real& bx, Real& by) {
     if constexpr (DV >= DV_RING_AN) {
-        return drift_an<DV>(T, x, y, bx, by);
+        return drift_an<DV>(T, P, x, y, bx, by);
     } else {
         static_assert(sizeof(Real) == 8, "reference drifts are fp64 only");
         return drift_ref<DV>(P, x, y, bx, by);
@@ -323,26 +323,31 @@ __host__ __device__ constexpr bool walk_uses_tables() {
     return DV >= DV_RING_AN && sizeof(Real) == 8;
 }
 constexpr bool kBigTables = sizeof(fm::FmTables) > 24 * 1024;
+// drifts that need more than 64 registers in the fp64 table kernel
+template <int DV>
+__host__ __device__ constexpr bool walk_heavy_drift() {
+    return DV == DV_SHOCK_AN || DV == DV_FIVE_RING_AN;
+}
 template <int DV, typename Real>
 __host__ __device__ constexpr int walk_block() {
 #ifdef SDDG_WALK_TABLE_BLOCK
-    if constexpr (walk_uses_tables<DV, Real>() && kBigTables && DV != DV_SHOCK_AN)
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables && !walk_heavy_drift<DV>())
         return SDDG_WALK_TABLE_BLOCK;
 #endif
-    if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return DV == DV_SHOCK_AN ? 640 : 1024;
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return walk_heavy_drift<DV>() ? 640 : 1024;
     return kWalkBlock;
 }
 template <int DV, typename Real>
 __host__ __device__ constexpr int walk_min_blocks() {
 #ifdef SDDG_WALK_TABLE_BLOCKS_PER_SM
-    if constexpr (walk_uses_tables<DV, Real>() && kBigTables && DV != DV_SHOCK_AN)
+    if constexpr (walk_uses_tables<DV, Real>() && kBigTables && !walk_heavy_drift<DV>())
         return SDDG_WALK_TABLE_BLOCKS_PER_SM;
 #endif
     if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return 1;
 #ifdef SDDG_SHOCK32_MIN_BLOCKS
     if constexpr (DV == DV_SHOCK_AN && sizeof(Real) == 4) return SDDG_SHOCK32_MIN_BLOCKS;
 #endif
-    return (DV == DV_SHOCK_AN || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
+    return (walk_heavy_drift<DV>() || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
 }
 
 template <int DV, typename Real>
@@ -429,7 +434,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             if constexpr (SCHEME == 0 && FAST) {
                 // x + b dt + sqrt(2 dt) z with b dt = c v and sqrt(2 dt) z = R (cs, sn)
                 Real c, vx, vy, R, sn, cs;
-                drift_cv<DV>(T, x, y, dt, c, vx, vy);
+                drift_cv<DV>(T, P, x, y, dt, c, vx, vy);
                 ok = true;  // closed forms: finite everywhere
                 uint64_t ua, ub;
                 rng.next_pair(a.rk, ua, ub);

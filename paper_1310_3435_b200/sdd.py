@@ -272,8 +272,12 @@ class MonitorFunction:
         return MonitorFunction(MACKENZIE, R=R, alpha=alpha)
 
     @staticmethod
-    def five_ring(alpha=0.2, R=30.0):
-        return MonitorFunction(FIVE_RING, R=R, alpha=alpha, domain=RectDomain(-1.0, 1.0, -1.0, 1.0))
+    def five_ring(alpha=0.2, R=30.0, analytic=False):
+        """analytic=True: performance mode (fastmath tanh, drift as
+        -alpha J grad u / rho^2), checked statistically against the reference."""
+        return MonitorFunction(FIVE_RING, R=R, alpha=alpha,
+                               grad_mode=GRAD_ANALYTIC if analytic else GRAD_REFERENCE,
+                               domain=RectDomain(-1.0, 1.0, -1.0, 1.0))
 
     @staticmethod
     def by_name(name, R=None, alpha=None):

@@ -207,6 +207,39 @@ def test_analytic_drift_tracks_reference_fd_paths(ctx):
     assert np.max(np.abs(a["f"][same] - r["f"][same])) < 1e-6
 
 
+@pytest.mark.parametrize("scheme", ["linear", "exponential"])
+def test_five_ring_performance_mode_tracks_reference_paths(ctx, scheme):
+    # the paper's own density (monitor.cpp:16-37, 199-204) in performance mode
+    # (table tanh, drift -alpha J grad u / rho^2) vs the reference drift:
+    # same streams, paths identical except for rare near-threshold decisions
+    dom = sdd.RectDomain(-1, 1, -1, 1)
+    ref_m = sdd.MonitorFunction.five_ring()
+    bd = sdd.make_boundary_data(ref_m, sdd.GridSpec(dom, 37, 37))
+    cfg = sdd.WalkConfig(scheme=scheme, dt=1e-4, lambda_=1000.0, walks=1, seed=5)
+    for p, pid in (((0.1, -0.2), 101), ((0.6, 0.55), 202), ((-0.5, 0.05), 303)):
+        a = sdd.walk_dump(p, pid, sdd.MonitorFunction.five_ring(analytic=True), dom, bd, cfg, 0, 1500, ctx=ctx)
+        r = sdd.walk_dump(p, pid, ref_m, dom, bd, cfg, 0, 1500, ctx=ctx)
+        same = (a["steps"] == r["steps"]) & (a["edge"] == r["edge"])
+        assert same.mean() >= 0.99, (p, same.mean())
+        assert np.max(np.abs(a["f"][same] - r["f"][same])) < 1e-6
+
+
+def test_five_ring_fp32_agrees_statistically_with_fp64(ctx):
+    dom = sdd.RectDomain(-1, 1, -1, 1)
+    m = sdd.MonitorFunction.five_ring(analytic=True)
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(dom, 37, 37))
+    pts = [(x, y) for x in (-0.6, -0.1, 0.4, 0.8) for y in (-0.7, 0.2, 0.65)]
+    pids = list(range(len(pts)))
+    c64 = sdd.WalkConfig(scheme="exponential", lambda_=1000.0, walks=20000, seed=11)
+    c32 = sdd.WalkConfig(scheme="exponential", lambda_=1000.0, walks=20000, seed=12, precision="fp32")
+    a = sdd.mc_estimate_batch(pts, pids, m, dom, bd, c64, ctx=ctx)
+    b = sdd.mc_estimate_batch(pts, pids, m, dom, bd, c32, ctx=ctx)
+    z = np.concatenate([(a["xi"] - b["xi"]) / np.hypot(a["se_xi"], b["se_xi"]),
+                        (a["eta"] - b["eta"]) / np.hypot(a["se_eta"], b["se_eta"])])
+    assert np.sum(np.abs(z) > 4) <= 1
+    assert 0.3 <= np.mean(z ** 2) <= 2.0
+
+
 @pytest.mark.parametrize("start", [(0.03, 0.03), (0.5, 0.02), (0.97, 0.96), (0.02, 0.5)])
 def test_analytic_bridge_test_tracks_reference_near_edges_and_corners(ctx, start):
     # Performance mode tests the bridge with d0 d1 * (1/dt), skips the edge
