@@ -502,8 +502,21 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     double* du = static_cast<double*>(c->s_u.ensure(sizeof(double) * uoff));
     sddg_solve_info* dinfo = static_cast<sddg_solve_info*>(c->s_info.ensure(sizeof(sddg_solve_info) * n));
     int* derr = static_cast<int*>(c->s_err.ensure(sizeof(int)));
+    // RB-SOR jobs too large for one CTA's shared memory (with their weights)
+    // go to the thread-block-cluster kernel K3c when they all share one shape
+    // and the batch is latency-bound (at most one job per SM: the slowest
+    // job sets the time, and K3c runs each job on CL SMs from shared memory;
+    // A/B config 3, 128 x 129^2: 15.5 -> 7.8 ms).  Larger batches are
+    // throughput-bound, where one CTA per job wins (2048 x 129^2: 47 vs 65 ms).
+    int cluster = 0;
+    if (sc.method == SDDG_SOLVER_RBSOR && !small.empty() && !coef_smem &&
+        static_cast<int64_t>(small.size()) <= std::max(1, c->sms)) {
+        bool same = true;
+        for (const SolveJob& j : small) same = same && j.nx == small[0].nx && j.ny == small[0].ny;
+        if (same) cluster = solver_cluster_size(small[0].nx, small[0].ny);
+    }
     double* dcoef = nullptr;
-    if (!small.empty() && !coef_smem)
+    if (!small.empty() && !coef_smem && !cluster)
         dcoef = static_cast<double*>(c->s_coef.ensure(sizeof(double) * ncoef * max_n_s * small.size()));
     double* dlarge = nullptr;
     if (!large.empty())
@@ -526,10 +539,16 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     if (!small.empty()) {
         ck(cudaMemcpyAsync(dj, small.data(), sizeof(SolveJob) * small.size(), cudaMemcpyHostToDevice, st),
            "h2d jobs");
-        ck(launch_solve_batch(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
-                              sc.max_iters, sc.init_blend, sc.method, omega, du, dinfo, derr, st,
-                              max_n_s, max_int_s, dcoef, coef_smem ? 1 : 0),
-           "solver launch");
+        if (cluster)
+            ck(launch_solve_cluster(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
+                                    sc.max_iters, sc.init_blend, omega, du, dinfo, derr, st, small[0].nx,
+                                    small[0].ny, cluster),
+               "cluster solver launch");
+        else
+            ck(launch_solve_batch(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
+                                  sc.max_iters, sc.init_blend, sc.method, omega, du, dinfo, derr, st,
+                                  max_n_s, max_int_s, dcoef, coef_smem ? 1 : 0),
+               "solver launch");
         ++launches;
     }
     for (size_t q = 0; q < large.size(); ++q) {

@@ -17,6 +17,9 @@
 // inv_den (stored with row stride nx) also in smem when they fit, else read
 // through L1/L2 from a global scratch laid out the same way.
 #include <cfloat>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "sddg_internal.h"
 
@@ -43,6 +46,46 @@ struct BlockMax {
         return m;
     }
 };
+
+// Initial guess of point (i, j) (detsolver.cpp:121-148): transfinite blend of
+// the edge data clamped to the boundary range, or the range midpoint; the
+// boundary itself holds the edge data.
+__device__ __forceinline__ double initial_value(int i, int j, int nx, int ny, const double* B,
+                                                const double* T, const double* L, const double* Rt,
+                                                double bmin, double bmax, int init_blend) {
+    double v;
+    if (init_blend) {
+        const double ty = static_cast<double>(j) / (ny - 1);
+        const double tx = static_cast<double>(i) / (nx - 1);
+        const double xb = (1.0 - tx) * L[j] + tx * Rt[j];
+        const double yb = (1.0 - ty) * B[i] + ty * T[i];
+        const double bil = ((1.0 - tx) * (1.0 - ty) * B[0] + tx * ty * T[nx - 1]) +
+                           (tx * (1.0 - ty) * B[nx - 1] + (1.0 - tx) * ty * T[0]);
+        v = xb + yb - bil;
+        v = v < bmin ? bmin : (bmax < v ? bmax : v);
+    } else {
+        v = 0.5 * (bmin + bmax);
+    }
+    if (j == 0) v = B[i];
+    if (j == ny - 1) v = T[i];
+    if (i == 0) v = L[j];
+    if (i == nx - 1) v = Rt[j];
+    return v;
+}
+
+// RB-SOR neighbour weights of interior point (i, j) of a job, divided by the
+// diagonal: (aE, aW), (aN, aS) (half-point weights of detsolver.cpp:88-111)
+__device__ __forceinline__ void sor_weights(const double* __restrict__ wg, int gnx, const SolveJob& J,
+                                            int i, int j, double ihx2, double ihy2, double2& ew,
+                                            double2& ns) {
+    const double* wr = wg + (int64_t)(J.j0 + j) * gnx + (J.i0 + i);
+    const double wc = wr[0];
+    const double ce = 0.5 * (wc + wr[1]), cw = 0.5 * (wr[-1] + wc);
+    const double cn = 0.5 * (wc + wr[gnx]), cs = 0.5 * (wr[-gnx] + wc);
+    const double id = 1.0 / ((ce + cw) * ihx2 + (cn + cs) * ihy2);
+    ew = make_double2(ce * ihx2 * id, cw * ihx2 * id);
+    ns = make_double2(cn * ihy2 * id, cs * ihy2 * id);
+}
 
 template <int METHOD, int PTS>
 __global__ void __launch_bounds__(kSolveThreads)
@@ -90,13 +133,8 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
             const int colour = q / nslots, r = q - colour * nslots;
             const int j = r / half + 1, i = 2 * (r % half) + 1 + ((j + 1 + colour) & 1);
             if (i > mi) continue;
-            const double* wr = wg + (int64_t)(J.j0 + j) * gnx + (J.i0 + i);
-            const double wc = wr[0];
-            const double ce = 0.5 * (wc + wr[1]), cw = 0.5 * (wr[-1] + wc);
-            const double cn = 0.5 * (wc + wr[gnx]), cs = 0.5 * (wr[-gnx] + wc);
-            const double id = 1.0 / ((ce + cw) * ihx2 + (cn + cs) * ihy2);
-            PQ[colour * 2 * nslots + r] = make_double2(ce * ihx2 * id, cw * ihx2 * id);
-            PQ[colour * 2 * nslots + nslots + r] = make_double2(cn * ihy2 * id, cs * ihy2 * id);
+            sor_weights(wg, gnx, J, i, j, ihx2, ihy2, PQ[colour * 2 * nslots + r],
+                        PQ[colour * 2 * nslots + nslots + r]);
         }
     }
     // coefficients from the global weights (detsolver.cpp:88-111)
@@ -123,27 +161,8 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     const double bmax = BlockMax::reduce(lmax, red);
     const double bmin = -BlockMax::reduce(-lmin, red);
     // initial guess (detsolver.cpp:121-148)
-    for (int c = tid; c < N; c += nt) {
-        const int i = c % nx, j = c / nx;
-        double v;
-        if (init_blend) {
-            const double ty = static_cast<double>(j) / (ny - 1);
-            const double tx = static_cast<double>(i) / (nx - 1);
-            const double xb = (1.0 - tx) * L[j] + tx * Rt[j];
-            const double yb = (1.0 - ty) * B[i] + ty * T[i];
-            const double bil = ((1.0 - tx) * (1.0 - ty) * B[0] + tx * ty * T[nx - 1]) +
-                               (tx * (1.0 - ty) * B[nx - 1] + (1.0 - tx) * ty * T[0]);
-            v = xb + yb - bil;
-            v = v < bmin ? bmin : (bmax < v ? bmax : v);
-        } else {
-            v = 0.5 * (bmin + bmax);
-        }
-        if (j == 0) v = B[i];
-        if (j == ny - 1) v = T[i];
-        if (i == 0) v = L[j];
-        if (i == nx - 1) v = Rt[j];
-        u[c] = v;
-    }
+    for (int c = tid; c < N; c += nt)
+        u[c] = initial_value(c % nx, c / nx, nx, ny, B, T, L, Rt, bmin, bmax, init_blend);
     __syncthreads();
 
     const int64_t max_iters =
@@ -283,9 +302,221 @@ cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, cons
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// K3c: RB-SOR for jobs whose weights do not fit next to u in one SM's shared
+// memory (129^2 blocks of configs 3 and 4): one thread-block cluster of CL
+// CTAs per job ("one subdomain per thread block group").  CTA r owns a strip
+// of interior rows with one halo row on each side; its u strip and the
+// packed weights of its rows live in its own shared memory for the whole
+// solve, so the sweeps never touch L2.  After each colour the strip's edge
+// rows (that colour's points only) are stored into the neighbours' halo rows
+// through distributed shared memory, and a cluster barrier publishes them.
+// The per-sweep maximum update is all-gathered the same way, so every CTA
+// takes the same convergence decision (the K3 stopping rule).
+constexpr int kClusterThreads = 256;
+
+// shared-memory doubles of one CTA: u strip (per + 2 rows), the packed weights
+// (2 colours x 2 double2 per slot, per * half slots), CL maximum slots
+__host__ __device__ inline int64_t cluster_smem_doubles(int nx, int ny, int cl) {
+    const int mj = ny - 2, half = (nx - 1) / 2;
+    const int per = (mj + cl - 1) / cl;
+    return ((static_cast<int64_t>(per + 2) * nx + 1) & ~1LL) + 8LL * per * half + 8;
+}
+
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kClusterThreads)
+solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
+                     const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
+                     int64_t max_iters_cfg, int init_blend, double omega, double* __restrict__ uout,
+                     sddg_solve_info* __restrict__ info, int per_cap, int* err) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = static_cast<int>(cluster.block_rank());
+    extern __shared__ double smem[];
+    __shared__ double red[kClusterThreads / 32];
+    const SolveJob J = jobs[blockIdx.x / CL];
+    const int nx = J.nx, ny = J.ny, mi = nx - 2, mj = ny - 2;
+    const int half = (mi + 1) / 2;
+    const int per = (mj + CL - 1) / CL;
+    const int ra = 1 + rank * per;                     // first interior row of the strip
+    const int rb = min(1 + (rank + 1) * per, ny - 1);  // one past the last
+    const int rows = rb > ra ? rb - ra : 0;
+    const int nsl = rows * half;                       // slots per colour
+    const int cap = per_cap * half;
+    double* us = smem;  // local row lr = j - (ra - 1), rows ra-1 .. rb
+    double2* PQ = reinterpret_cast<double2*>(smem + (((per_cap + 2) * nx + 1) & ~1));
+    double* slots = reinterpret_cast<double*>(PQ + 4 * cap);
+    const double* B = bc + J.bc_off;
+    const double* T = B + nx;
+    const double* L = T + nx;
+    const double* Rt = L + ny;
+    const int tid = threadIdx.x, nt = blockDim.x;
+
+    for (int q = tid; q < 2 * nsl; q += nt) {
+        const int colour = q / nsl, r = q - colour * nsl;
+        const int j = ra + r / half, i = 2 * (r % half) + 1 + ((j + 1 + colour) & 1);
+        if (i > mi) continue;
+        sor_weights(wg, gnx, J, i, j, ihx2, ihy2, PQ[colour * 2 * cap + r], PQ[colour * 2 * cap + cap + r]);
+    }
+    double lmin = DBL_MAX, lmax = -DBL_MAX;
+    for (int k = tid; k < 2 * (nx + ny); k += nt) {
+        const double v = B[k];
+        lmin = v < lmin ? v : lmin;
+        lmax = lmax < v ? v : lmax;
+    }
+    const double bmax = BlockMax::reduce(lmax, red);
+    const double bmin = -BlockMax::reduce(-lmin, red);
+    for (int c = tid; c < (rows + 2) * nx; c += nt) {
+        const int j = ra - 1 + c / nx, i = c % nx;
+        us[c] = initial_value(i, j, nx, ny, B, T, L, Rt, bmin, bmax, init_blend);
+    }
+    // neighbours' strips: my first row is rank-1's top halo, my last row
+    // rank+1's bottom halo (same shared-memory layout in every CTA)
+    double* below = rank > 0 ? cluster.map_shared_rank(us, rank - 1) : nullptr;
+    double* above = (rank + 1 < CL && rb < ny - 1) ? cluster.map_shared_rank(us, rank + 1) : nullptr;
+    const int below_row = per + 1;  // local index of row ra in rank-1's strip
+    cluster.sync();
+
+    const int64_t max_iters =
+        max_iters_cfg > 0 ? max_iters_cfg : 200LL * (nx > ny ? nx : ny) * (nx > ny ? nx : ny);
+    int64_t iters = 0;
+    double upd = 0.0, prev = -1.0;
+    bool conv = false;
+    const int l_first = tid / half, s_first = tid % half;
+    const int dl = nt / half, ds = nt % half;
+    while (iters < max_iters) {
+        ++iters;
+        double lupd = 0.0;
+#pragma unroll 1
+        for (int colour = 0; colour < 2; ++colour) {
+            const double2* P = PQ + colour * 2 * cap;
+            const double2* Q = P + cap;
+            int lr = l_first, sl = s_first;
+            for (int q = tid; q < nsl; q += nt) {
+                const int j = ra + lr;
+                const int i = 2 * sl + 1 + ((j + 1 + colour) & 1);
+                if (i <= mi) {
+                    const int c = (lr + 1) * nx + i;
+                    const double2 ew = P[q], ns = Q[q];
+                    const double uc = us[c];
+                    const double gs =
+                        fma(ew.x, us[c + 1], fma(ew.y, us[c - 1], fma(ns.x, us[c + nx], ns.y * us[c - nx])));
+                    const double nv = fma(omega, gs - uc, uc);
+                    const double du = fabs(nv - uc);
+                    lupd = lupd < du ? du : lupd;
+                    us[c] = nv;
+                }
+                sl += ds;
+                lr += dl;
+                if (sl >= half) {
+                    sl -= half;
+                    ++lr;
+                }
+            }
+            __syncthreads();
+            // this colour's points of the edge rows into the neighbours' halos
+            for (int i = 1 + tid; i <= mi; i += nt) {
+                if (below && ((ra + 1 + colour + i) & 1) == 1)
+                    below[below_row * nx + i] = us[nx + i];
+                if (above && ((rb - 1 + 1 + colour + i) & 1) == 1)
+                    above[i] = us[rows * nx + i];
+            }
+            if (colour == 1) {
+                const double m = BlockMax::reduce(lupd, red);
+                if (tid < CL) cluster.map_shared_rank(slots, tid)[rank] = m;
+            }
+            cluster.sync();
+        }
+        upd = slots[0];
+#pragma unroll
+        for (int r = 1; r < CL; ++r) upd = upd < slots[r] ? slots[r] : upd;
+        if (upd < tol) {
+            if (upd == 0.0 || upd < 1e-4 * tol) {
+                conv = true;
+                break;
+            }
+            if (prev > 0.0 && upd < prev) {
+                const double rho = upd / prev;
+                if (upd * rho / (1.0 - rho) < tol) {
+                    conv = true;
+                    break;
+                }
+            }
+        }
+        prev = upd;
+    }
+    // maximum principle (detsolver.cpp:191-198) and write-out of my rows
+    // (rank 0 adds boundary row 0, the last strip row ny-1)
+    const double slack = 1e-12 * (1.0 + fabs(bmin) + fabs(bmax));
+    double* U = uout + J.u_off;
+    const int lo = rank == 0 ? 0 : 1, hi = rb == ny - 1 ? rows + 2 : rows + 1;
+    for (int c = lo * nx + tid; c < hi * nx; c += nt) {
+        const int lr = c / nx, i = c % nx, j = ra - 1 + lr;
+        const double v = us[c];
+        if (i > 0 && j > 0 && i + 1 < nx && j + 1 < ny && (v < bmin - slack || v > bmax + slack))
+            atomicCAS(err, 0, 4);
+        U[static_cast<int64_t>(j) * nx + i] = v;
+    }
+    if (rank == 0 && tid == 0) {
+        sddg_solve_info r;
+        r.iterations = iters;
+        r.final_update = upd;
+        r.converged = conv ? 1 : 0;
+        r.reserved = 0;
+        info[blockIdx.x / CL] = r;
+    }
+    cluster.sync();  // no CTA leaves while a neighbour may still store into it
+}
+
+template <int CL>
+cudaError_t launch_cluster(int64_t n_jobs, int max_nx, int max_ny, cudaStream_t st, const double* wg,
+                           int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
+                           double tol, int64_t mi, int init_blend, double omega, double* u,
+                           sddg_solve_info* info, int* err) {
+    const size_t smem = sizeof(double) * static_cast<size_t>(cluster_smem_doubles(max_nx, max_ny, CL));
+    auto k = solve_cluster_kernel<CL>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const int per_cap = (max_ny - 2 + CL - 1) / CL;
+    k<<<static_cast<unsigned>(n_jobs * CL), kClusterThreads, smem, st>>>(
+        wg, gnx, ihx2, ihy2, jobs, bc, tol, mi, init_blend, omega, u, info, per_cap, err);
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 int solver_max_points() { return kSolveThreads * 32; }
+
+int solver_cluster_size(int max_nx, int max_ny) {
+    if (std::getenv("SDDG_NO_CLUSTER_SOLVER")) return 0;
+    const int mj = max_ny - 2;
+    for (int cl : {2, 4, 8}) {
+        const int per = (mj + cl - 1) / cl;
+        if (sizeof(double) * cluster_smem_doubles(max_nx, max_ny, cl) <= 227 * 1024 &&
+            (cl - 1) * per < mj && per >= 2)  // every strip non-empty
+            return cl;
+    }
+    return 0;
+}
+
+cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, double hy,
+                                 int64_t n_jobs, const SolveJob* jobs, const double* bc, double tol,
+                                 int64_t max_iters_cfg, int init_blend, double omega, double* u,
+                                 sddg_solve_info* info, int* err, cudaStream_t s, int max_nx,
+                                 int max_ny, int cl) {
+    if (n_jobs <= 0) return cudaSuccess;
+    const double ihx2 = 1.0 / (hx * hx), ihy2 = 1.0 / (hy * hy);
+    switch (cl) {
+        case 2: return launch_cluster<2>(n_jobs, max_nx, max_ny, s, w_global, gnx, ihx2, ihy2, jobs, bc,
+                                         tol, max_iters_cfg, init_blend, omega, u, info, err);
+        case 4: return launch_cluster<4>(n_jobs, max_nx, max_ny, s, w_global, gnx, ihx2, ihy2, jobs, bc,
+                                         tol, max_iters_cfg, init_blend, omega, u, info, err);
+        case 8: return launch_cluster<8>(n_jobs, max_nx, max_ny, s, w_global, gnx, ihx2, ihy2, jobs, bc,
+                                         tol, max_iters_cfg, init_blend, omega, u, info, err);
+    }
+    return cudaErrorInvalidValue;
+}
 
 cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
                                int64_t n_jobs, const SolveJob* jobs, const double* bc,

@@ -173,6 +173,32 @@ def test_config3_batch_rbsor_against_reference_jacobi_sample(oracle, ctx):
         assert np.max(np.abs(res[k].values - u_ref)) <= 1e-10
 
 
+@pytest.mark.parametrize("nx,ny", [(129, 129), (129, 97), (160, 130)])
+def test_cluster_solver_matches_single_cta_solver(oracle, ctx, monkeypatch, nx, ny):
+    # K3c (one thread-block cluster per job, strips + DSMEM halos) performs
+    # the single-CTA K3's red-black iteration (same weights, same update
+    # expression, exact max): identical iterates, bit for bit; shapes cover
+    # odd/even row lengths and a short last strip
+    g = 257
+    w = oracle.weight_values(B.density(B.SHOCK_W), UNIT, g, g)
+    rng = np.random.default_rng(nx * ny)
+    subs, bcs = [], []
+    for k in range(6):
+        v0, v1, v2, v3 = np.sort(rng.random(4))
+        ex = lambda lo, hi: np.linspace(lo, hi, nx)  # noqa: E731
+        ey = lambda lo, hi: np.linspace(lo, hi, ny)  # noqa: E731
+        bcs.append(sdd.EdgeData(ex(v0, v1), ex(v2, v3), ey(v0, v2), ey(v1, v3)))
+        subs.append(((k * 17) % (g - nx), (k * 29) % (g - ny), nx, ny))
+    cfg = sdd.SolverConfig(tol=1e-13, method="rbsor")
+    a = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), subs, bcs, cfg, ctx=ctx)
+    monkeypatch.setenv("SDDG_NO_CLUSTER_SOLVER", "1")
+    b = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), subs, bcs, cfg, ctx=ctx)
+    for ra, rb in zip(a, b):
+        assert ra.converged and rb.converged
+        assert np.array_equal(ra.values, rb.values)
+        assert ra.iterations == rb.iterations and ra.final_update == rb.final_update
+
+
 def test_large_grid_path_jacobi_bit_identical(golden, oracle, ctx, monkeypatch):
     # K3b (cooperative, global memory) runs the same reference iteration
     monkeypatch.setenv("SDDG_FORCE_LARGE_SOLVER", "1")
