@@ -148,6 +148,12 @@ def test_errors(ctx):
                             ctx=ctx)
 
 
+def test_empty_batch_is_a_no_op(ctx):
+    for method in ("jacobi", "rbsor"):
+        assert sdd.solve_dirichlet_batch(np.ones(9 * 9), 9, 9, 0.125, 0.125, [], [],
+                                         sdd.SolverConfig(method=method), ctx=ctx) == []
+
+
 def test_config3_batch_rbsor_against_reference_jacobi_sample(oracle, ctx):
     # BASELINE config 3: 64 subdomains x 2 fields of 129^2 in one launch;
     # two of them against the reference iteration at tol 1e-13

@@ -184,6 +184,7 @@ def test_validation_errors(ctx):
                         sdd.WalkConfig(walks=10, precision="fp32"), ctx=ctx)
     # an empty batch is a no-op
     assert len(sdd.mc_estimate_batch(np.zeros((0, 2)), [], m, UNIT, bd, sdd.WalkConfig(), ctx=ctx)) == 0
+    assert len(sdd.walk_dump((0.5, 0.5), 0, m, UNIT, bd, sdd.WalkConfig(), 0, 0, ctx=ctx)) == 0
 
 
 def test_numerical_error_after_1024_epochs(ctx):
