@@ -348,6 +348,39 @@ def test_config3_scale_properties_fp32(ctx):
     assert np.corrcoef(x, e["xi"])[0, 1] > 0.9
 
 
+def test_config2_full_size_properties_fp64(ctx):
+    # BASELINE config 2 at full size (all 753 nodes x 1e5 paths, dt 2e-5,
+    # performance-mode fp64: the bench workload): size-independent properties.
+    # The ring density and the reference boundary tables are symmetric under
+    # x -> 1-x, so xi(x, y) + xi(1-x, y) = 1 in expectation; mirror nodes use
+    # independent streams (different point ids), so the sum is a z-test.
+    m = sdd.MonitorFunction.ring(analytic=True)
+    spec = sdd.GridSpec(UNIT, 129, 129)
+    bd = sdd.make_boundary_data(m, spec)
+    lay = sdd.build_layout(spec, 4, 4)
+    px, py, pid = sdd.interface_nodes(m, lay, sdd.plan_interface_points("all", 0, m, lay))
+    assert len(px) == 753
+    cfg = sdd.WalkConfig(scheme="linear", dt=2e-5, walks=100_000, seed=1)
+    e = sdd.mc_estimate_batch(np.stack([px, py], 1), pid, m, UNIT, bd, cfg, ctx=ctx)
+    assert (e["edge_hits"].sum(axis=1) == 100_000).all() and (e["restarts"] == 0).all()
+    assert (e["xi"] > 0).all() and (e["xi"] < 1).all() and (e["eta"] > 0).all() and (e["eta"] < 1).all()
+    assert ctx.last_stats()["path_steps"] > 6e11
+    ij = {(int(round(x * 128)), int(round(y * 128))): k for k, (x, y) in enumerate(zip(px, py))}
+    z = []
+    for (i, j), k in ij.items():
+        q = ij.get((128 - i, j))
+        if q is not None and q > k:
+            z.append((e["xi"][k] + e["xi"][q] - 1.0) / np.hypot(e["se_xi"][k], e["se_xi"][q]))
+    z = np.array(z)
+    assert len(z) > 300
+    assert np.sum(np.abs(z) > 4) <= 1
+    assert 0.5 <= np.mean(z ** 2) <= 1.6  # chi^2 / dof of independent estimates
+    # xi increases with x along every horizontal interface line
+    for j in (32, 64, 96):
+        row = sorted((i, e["xi"][k]) for (i, jj), k in ij.items() if jj == j)
+        assert np.all(np.diff([v for _, v in row]) > -4 * 0.5 / np.sqrt(1e5) * np.sqrt(2))
+
+
 def test_fastmath_accuracy(ctx):
     # performance-mode elementary functions (fastmath.cuh) vs the CUDA library
     import ctypes as C
