@@ -87,7 +87,18 @@ __device__ __forceinline__ void sor_weights(const double* __restrict__ wg, int g
     ns = make_double2(cn * ihy2 * id, cs * ihy2 * id);
 }
 
-template <int METHOD, int PTS>
+// G (RB-SOR): slots per group of coefficient loads issued ahead of the
+// updates -- 4 when the weights stream from L2, 1 when they are in shared memory
+// One RB-SOR point update (K3 and K3c share it, so their iterates agree bit
+// for bit): Gauss-Seidel value from the pre-divided weights as two
+// independent products pairs (dependency depth 3), then over-relaxation.
+__device__ __forceinline__ double sor_point(const double2 ew, const double2 ns, double uE, double uW,
+                                            double uN, double uS, double uc, double omega) {
+    const double gs = fma(ew.x, uE, ew.y * uW) + fma(ns.x, uN, ns.y * uS);
+    return fma(omega, gs - uc, uc);
+}
+
+template <int METHOD, int PTS, int G = 1>
 __global__ void __launch_bounds__(kSolveThreads)
 solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
              const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
@@ -211,10 +222,6 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
                 // before its shared-memory stores (the compiler may not move
                 // loads of the possibly-aliased coefficient pointer past a
                 // store), so G L2 round trips overlap instead of serialising
-#ifndef SDDG_SOR_GROUP
-#define SDDG_SOR_GROUP 4
-#endif
-                constexpr int G = SDDG_SOR_GROUP;
                 for (int q0 = tid; q0 < nslots; q0 += G * nt) {
                     double2 ew[G], ns[G];
                     int cc[G];
@@ -239,9 +246,8 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
                         const int c = cc[k];
                         if (c < 0) continue;
                         const double uc = u[c];
-                        const double gs = fma(ew[k].x, u[c + 1],
-                                              fma(ew[k].y, u[c - 1], fma(ns[k].x, u[c + nx], ns[k].y * u[c - nx])));
-                        const double nv = fma(omega, gs - uc, uc);
+                        const double nv =
+                            sor_point(ew[k], ns[k], u[c + 1], u[c - 1], u[c + nx], u[c - nx], uc, omega);
                         const double du = fabs(nv - uc);
                         lupd = lupd < du ? du : lupd;
                         u[c] = nv;
@@ -287,13 +293,13 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     }
 }
 
-template <int METHOD, int PTS>
+template <int METHOD, int PTS, int G = 1>
 cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, const double* wg,
                        int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
                        double tol, int64_t mi, int init_blend, double omega, double* u,
                        sddg_solve_info* info, double* scratch, int64_t cstride, int cin,
                        int* err) {
-    auto k = solve_kernel<METHOD, PTS>;
+    auto k = solve_kernel<METHOD, PTS, G>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -399,9 +405,8 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
                     const int c = (lr + 1) * nx + i;
                     const double2 ew = P[q], ns = Q[q];
                     const double uc = us[c];
-                    const double gs =
-                        fma(ew.x, us[c + 1], fma(ew.y, us[c - 1], fma(ns.x, us[c + nx], ns.y * us[c - nx])));
-                    const double nv = fma(omega, gs - uc, uc);
+                    const double nv =
+                        sor_point(ew, ns, us[c + 1], us[c - 1], us[c + nx], us[c - nx], uc, omega);
                     const double du = fabs(nv - uc);
                     lupd = lupd < du ? du : lupd;
                     us[c] = nv;
@@ -534,9 +539,13 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
     const int grid = static_cast<int>(n_jobs);
     const int T = kSolveThreads;
     if (method == SDDG_SOLVER_RBSOR)
-        return launch_one<1, 1>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
-                                max_iters_cfg, init_blend, omega, u, info, coef_scratch, cstride,
-                                coef_in_smem, err);
+        return coef_in_smem
+                   ? launch_one<1, 1, 1>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
+                                         max_iters_cfg, init_blend, omega, u, info, coef_scratch,
+                                         cstride, coef_in_smem, err)
+                   : launch_one<1, 1, 4>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
+                                         max_iters_cfg, init_blend, omega, u, info, coef_scratch,
+                                         cstride, coef_in_smem, err);
     const int pts = (max_interior + T - 1) / T;
 #define SDDG_J(P)                                                                             \
     if (pts <= P)                                                                             \

@@ -1,6 +1,6 @@
 """One K3 batch for ncu captures: the 2048 x 129^2 RB-SOR batch of
 tools/config_sweep.py (shock weights, tol 1e-10), working set >> L2.
-python tools/solver_once.py [n_jobs]"""
+python tools/solver_once.py [n_jobs] [grid] [subdomains per side]   (default 2048 1025 8)"""
 import os
 import sys
 
@@ -11,7 +11,8 @@ from paper_1310_3435_b200 import sdd  # noqa: E402
 
 n_jobs = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 ctx = sdd.Context(0)
-g, subs_n = 1025, 8
+g = int(sys.argv[2]) if len(sys.argv) > 2 else 1025
+subs_n = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 spec = sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), g, g)
 lay = sdd.build_layout(spec, subs_n, subs_n)
 bxy = lay.block_x + 1
