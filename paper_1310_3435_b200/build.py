@@ -77,7 +77,32 @@ def build(verbose=False, force=False):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
+    if not _TAG:
+        build_examples()
     return LIB
+
+
+EXAMPLES = os.path.join(ROOT, "examples")
+EXAMPLE_BIN = os.path.join(EXAMPLES, "_bin")
+
+
+def build_examples():
+    """Plain C callers of the C-ABI (examples/*.c), linked against the
+    in-tree library with an rpath relative to the binary."""
+    if not os.path.isdir(EXAMPLES):
+        return
+    os.makedirs(EXAMPLE_BIN, exist_ok=True)
+    for src in sorted(f for f in os.listdir(EXAMPLES) if f.endswith(".c")):
+        out = os.path.join(EXAMPLE_BIN, src[:-2])
+        deps = [os.path.join(EXAMPLES, src), LIB, os.path.join(ROOT, "include", "sddg.h")]
+        if _mtime(out) >= max(_mtime(d) for d in deps):
+            continue
+        cmd = ["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
+               os.path.join(EXAMPLES, src), "-o", out, "-L" + OUT_DIR, "-lsddg",
+               "-Wl,-rpath,$ORIGIN/../../paper_1310_3435_b200/_lib"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"gcc failed for {src}:\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -142,3 +142,23 @@ def test_write_mesh_is_byte_identical_to_reference(golden, tmp_path, refimpl):
     assert ours.read_bytes().startswith(b"sddmesh v1 33 33\n")
     with pytest.raises(sdd.ValidationError):
         sdd.write_mesh(mesh, xi, eta, sdd.GridSpec(spec.domain, 33, 17), str(ours))
+
+
+def test_plain_c_caller_builds_links_and_fails_loudly_without_a_gpu():
+    # examples/sdd_config1.c: a C99 program against include/sddg.h only,
+    # built by build() and linked to the in-tree library; with no usable GPU
+    # the first call reports SDDG_ERR_CUDA (status 6) -- no CPU fallback
+    exe = os.path.join(ROOT, "examples", "_bin", "sdd_config1")
+    if not os.path.exists(exe):
+        from paper_1310_3435_b200 import build as bld
+        bld.build()
+    ldd = subprocess.run(["ldd", exe], capture_output=True, text=True).stdout
+    assert "paper_1310_3435_b200/_lib/libsddg.so" in ldd
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present: tests/test_gpu_sdd.py runs the program")
+    except ImportError:
+        pass
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 1 and "status 6" in r.stderr

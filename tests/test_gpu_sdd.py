@@ -1,6 +1,9 @@
 """GPU end-to-end: solve_interfaces and solve_sdd through the C-ABI against
 the reference's golden outputs and the reference test_decomposition.cpp
 properties."""
+import os
+import subprocess
+
 import numpy as np
 import pytest
 
@@ -167,3 +170,26 @@ def test_stochastic_full_matches_reference_estimates(ctx, oracle):
                                  [p[0] for p in pts], [p[1] for p in pts], pid, threads=8)
     assert np.max(np.abs(xi[pid] - o["xi"])) <= 1e-10 and np.max(np.abs(eta[pid] - o["eta"])) <= 1e-10
     assert np.array_equal(xi.reshape(9, 9)[0], t.f[0]) and np.array_equal(eta.reshape(9, 9)[:, 0], t.g[2])
+
+
+@pytest.mark.parametrize("mode", ["reference", "analytic"])
+def test_plain_c_caller_matches_python_mirror(ctx, mode):
+    # examples/sdd_config1.c runs BASELINE config 1 end to end through the
+    # C-ABI alone; the Python mirror's solve_sdd on the same inputs gives the
+    # same mesh bit for bit (checksums in index order) and the same counts
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([os.path.join(root, "examples", "_bin", "sdd_config1"), mode, "1"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    mc, steps, _, _, sx, se, qmax, qmean = out.stdout.split()
+    m = sdd.MonitorFunction.ring(analytic=mode == "analytic")
+    spec = sdd.GridSpec(UNIT, 65, 65)
+    lay = sdd.build_layout(spec, 2, 2)
+    r = sdd.solve_sdd(m, lay, sdd.plan_interface_points("equispaced", 31, m, lay),
+                      sdd.WalkConfig(scheme="linear", dt=1e-4, walks=10_000, seed=1),
+                      sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx)
+    assert int(mc) == r.mc_points == 61 and int(steps) == r.path_steps
+    # the C program sums in index order (np.cumsum is sequential; np.sum is pairwise)
+    assert float(sx) == float(np.cumsum(r.xi)[-1]) and float(se) == float(np.cumsum(r.eta)[-1])
+    q = sdd.quality_report(sdd.invert_mesh(r.xi, r.eta, spec, 65, 65, ctx=ctx), ctx=ctx)
+    assert float(qmax) == q.q_max and float(qmean) == q.q_mean
