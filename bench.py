@@ -229,6 +229,52 @@ def run_reference(args):
     return 0
 
 
+def hbm_peak_gbs():
+    """Measured HBM copy bandwidth (driver-written MEASURED_PEAKS.json), else
+    the profiling recipe's B200 figure."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 7700.0, "fallback: B200 nominal 7.7 TB/s"
+
+
+def solver_rooflines(sdd, ctx):
+    g, subs_n = 1025, 8
+    spec = sdd.GridSpec(sdd.RectDomain(0.0, 1.0, 0.0, 1.0), g, g)
+    lay = sdd.build_layout(spec, subs_n, subs_n)
+    bxy = lay.block_x + 1
+    x = np.linspace(0.0, 1.0, g)
+    X, Y = np.meshgrid(x, x)
+    w = (1.0 + 20.0 / np.cosh(50 * (Y - 0.5 - 0.15 * np.sin(2 * np.pi * X))) ** 2).ravel()
+    peak, src = hbm_peak_gbs()
+    out = {"bytes_per_point_update": 40, "peak_GBps": peak, "peak_source": src}
+    for name, n_jobs in (("config3_batch", 128), ("batch_2048", 2048)):
+        rng = np.random.default_rng(3)
+        jobs, bcs = [], []
+        for s_ in range(n_jobs):
+            q = s_ % lay.subdomain_count()
+            jobs.append(lay.subdomain(q % subs_n, q // subs_n))
+            v = np.sort(rng.random(4))
+            e = lambda a, b: np.linspace(a, b, bxy)  # noqa: E731
+            bcs.append(sdd.EdgeData(e(v[0], v[1]), e(v[2], v[3]), e(v[0], v[2]), e(v[1], v[3])))
+        cfg = sdd.SolverConfig(tol=1e-10, method="rbsor")
+        best = None
+        for _ in range(3):
+            res = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), jobs, bcs, cfg, ctx=ctx)
+            ms = ctx.last_stats()["kernel_ms"]
+            best = ms if best is None else min(best, ms)
+        its = np.array([r.iterations for r in res])
+        upd = float(its.sum()) * (bxy - 2) ** 2
+        gbs = upd * 40 / (best / 1e3) / 1e9
+        out[name] = {"solves": n_jobs, "grid": f"{bxy}^2", "kernel": "K3c (cluster per solve)" if n_jobs <= 148
+                     else "K3 (CTA per solve)", "ms": best, "sweeps_mean": float(its.mean()),
+                     "sweeps_max": int(its.max()), "point_updates_per_s": upd / (best / 1e3),
+                     "effective_GBps": gbs, "frac_of_hbm_peak": gbs / peak,
+                     "converged": bool(all(r.converged for r in res))}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -241,6 +287,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-mesh", action="store_true", help="skip the end-to-end mesh-gen timings")
+    ap.add_argument("--no-solver", action="store_true", help="skip the subdomain-solver roofline")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -370,6 +417,15 @@ def main():
                           "path_steps": r.path_steps, "subdomain_solves": r.subdomain_solves,
                           "solver": "rbsor tol 1e-10"}
 
+    # ---- subdomain solver (K3/K3c), measured live: BASELINE config 3's batch
+    # (128 x 129^2, shock weights, RB-SOR to 1e-10; one thread-block cluster per
+    # solve) and a 2048-solve batch of the same blocks (working set 1 GB >> L2).
+    # Roofline: algorithmic 40 B per point-update against the
+    # measured HBM copy bandwidth; the data stays on chip, so it can exceed 1.
+    solver = None
+    if rank == 0 and world == 1 and not args.no_solver:
+        solver = solver_rooflines(sdd, ctx)
+
     # ---- CPU baseline: the reference on this host, rank 0 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -429,6 +485,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "mesh_gen_seconds": mesh,
+            "solver": solver,
             "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value * world,
         }
         print(json.dumps(line))
