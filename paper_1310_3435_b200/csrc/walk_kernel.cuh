@@ -27,6 +27,12 @@
 #include "philox.cuh"
 #include "sddg_internal.h"
 
+#ifndef SDDG_WALK_UNROLL
+#define SDDG_WALK_UNROLL 2  // step-loop copies (A/B: tools/ab.sh with -DSDDG_WALK_UNROLL=n)
+#endif
+#define SDDG_PRAGMA_STR(x) _Pragma(#x)
+#define SDDG_UNROLL(n) SDDG_PRAGMA_STR(unroll n)
+
 namespace sddg {
 
 // Elementary functions per mode: FAST (analytic fp64) uses fastmath.cuh;
@@ -424,9 +430,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
         start_walk(L.g);
         bool in_box = box_test(x, y);
         uint32_t step = 0;
-#ifndef SDDG_WALK_NO_UNROLL
-#pragma unroll 2  // two step copies: x, y alternate registers (no loop-carried moves)
-#endif
+        SDDG_UNROLL(SDDG_WALK_UNROLL)  // 2: step copies alternate x, y registers (no loop-carried moves)
         for (;;) {
             // ---- one step
             Real bx, by, nxp, nyp, z0, z1;
