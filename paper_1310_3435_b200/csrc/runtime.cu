@@ -227,6 +227,7 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     a.dt = cfg.dt;
     a.sqrt2dt = std::sqrt(2.0 * cfg.dt);  // step_linear (sde.cpp:27)
     a.inv_dt = 1.0 / cfg.dt;
+    a.half_inv_lambda = 0.5 / cfg.lambda;
     a.lambda = cfg.lambda;
     a.nu2 = 2.0 * std::sqrt(cfg.lambda);  // step_exponential (sde.cpp:135)
     a.bridge_thr = 40.0 * cfg.dt * (1.0 + (cfg.precision == SDDG_FP32 ? 1e-5 : 1e-12));

@@ -57,6 +57,7 @@ struct WalkArgs {
     sddg_path* dump;
     const void* fm_tables;  // fastmath.cuh FmTables in global memory (performance mode)
     double inv_dt;          // 1/dt: performance-mode bridge exponent d0 d1 / dt as a multiply
+    double half_inv_lambda; // 1/(2 lambda): performance-mode Exp(lambda) step from -2 ln u
 };
 
 // fastmath tables (host-built in long double, uploaded once per context)

@@ -63,6 +63,17 @@ struct RealOps<double, FAST> {
         R = scale * fm::fsqrt_pos(fm::fm2log_tab(T, fm::u01_open_bits(T, a)));
         fm::fsincos_2pi_bits(T, b, sn, cs);
     }
+    // the same with the squared scale inside the root: R = sqrt(-2 ln u1 * scale2)
+    __device__ static __forceinline__ void bm_polar_sq(const fm::FmTables& T, uint64_t a, uint64_t b,
+                                                       double scale2, double& R, double& sn,
+                                                       double& cs) {
+        R = fm::fsqrt_pos(fm::fm2log_tab(T, fm::u01_open_bits(T, a)) * scale2);
+        fm::fsincos_2pi_bits(T, b, sn, cs);
+    }
+    // -2 ln u_open(a) (rng.hpp:61-63) from the raw bits: Exp(lambda) = that * 1/(2 lambda)
+    __device__ static __forceinline__ double m2ln_open(const fm::FmTables& T, uint64_t a) {
+        return fm::fm2log_tab(T, fm::u01_open_bits(T, a));
+    }
     __device__ static __forceinline__ double ex(const fm::FmTables& T, double v) {
         if constexpr (FAST) return fm::fexp_tab(T, v);
         else return exp(v);
@@ -311,6 +322,45 @@ __device__ __noinline__ BridgeRes bridge_rare(Real x0, Real y0, Real x1, Real y1
     return r;
 }
 
+// Performance-mode exit test of the exponential scheme (edge_crossing_test
+// with exponent nu2 min(d0, d1), sde.cpp:72-109,131-140).  With large
+// exponential steps most edges qualify (ex <= 40 within 40/nu2 of an edge),
+// so this runs on nearly every step: the qualifying set is a bitmask, the
+// edge sort runs only when two or more edges qualify, and the draws share one
+// rolled loop.  Skipped edges draw nothing, as in edge_crossing.
+template <typename Real>
+__device__ __forceinline__ bool bridge_exp_fast(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
+                                                Real nu2, const RoundKeys& rk, const fm::FmTables& T,
+                                                LaneStream& rng, Real& hx, Real& hy, int& edge) {
+    int mask = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const Real k = d.dist(x0, y0, e), m = d.dist(x1, y1, e);
+        mask |= int(!(nu2 * (m < k ? m : k) > Real(40))) << e;
+    }
+    if (mask == 0) return false;
+    uint32_t order = 0x3210u;
+    if (mask & (mask - 1)) order = sorted_edge_order(d, x0, y0, x1, y1);
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i, order >>= 4) {
+        const int e = static_cast<int>(order & 15u);
+        if (!((mask >> e) & 1)) continue;
+        const Real d0 = d.dist(x0, y0, e), d1 = d.dist(x1, y1, e);
+        const Real ex = nu2 * (d1 < d0 ? d1 : d0);
+        const Real u = RealOps<Real, true>::u(rng.next_one(rk));
+        if (u < RealOps<Real, true>::ex(T, -ex)) {
+            const Real sum = d0 + d1;
+            const Real sc = sum > Real(0) ? d0 / sum : Real(0);
+            hx = x0 + sc * (x1 - x0);
+            hy = y0 + sc * (y1 - y0);
+            d.project(e, hx, hy);
+            edge = e;
+            return true;
+        }
+    }
+    return false;
+}
+
 // table_at / f_at / g_at (proj/src/boundary.cpp:10-42)
 __device__ __forceinline__ double table_at(const double* __restrict__ t, int n, double s) {
     int k = static_cast<int>(floor(s));
@@ -452,6 +502,18 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 Ops::box_muller(T, ua, ub, z0, z1);
                 nxp = x + bx * dt + sq2dt * z0;
                 nyp = y + by * dt + sq2dt * z1;
+            } else if constexpr (FAST && sizeof(Real) == 8) {
+                // step_exponential (sde.cpp:123-140), fp64 performance mode: edt =
+                // -ln u / lambda from the raw bits, one root for the radius
+                // sqrt(-2 ln u1) * sqrt(2 edt) = sqrt(-2 ln u1 * 2 edt)
+                const Real edt = Ops::m2ln_open(T, rng.next_one(a.rk)) * Real(a.half_inv_lambda);
+                ok = drift<DV, Real>(P, T, x, y, bx, by);
+                uint64_t ua, ub;
+                rng.next_pair(a.rk, ua, ub);
+                Real R, sn, cs;
+                Ops::bm_polar_sq(T, ua, ub, Real(2) * edt, R, sn, cs);
+                nxp = fma(R, cs, fma(bx, edt, x));
+                nyp = fma(R, sn, fma(by, edt, y));
             } else {
                 // step_exponential (sde.cpp:123-140): dt ~ Exp(lambda) first
                 const Real edt = -Ops::lg(T, Ops::u_open(rng.next_one(a.rk))) / Real(a.lambda);
@@ -459,7 +521,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 uint64_t ua, ub;
                 rng.next_pair(a.rk, ua, ub);
                 const Real s = Ops::sq(Real(2) * edt);
-                if constexpr (FAST) {
+                if constexpr (FAST) {  // fp32 (A/B: the fp64 form above is 10-18% slower here)
                     Real R, sn, cs;
                     Ops::bm_polar(T, ua, ub, s, R, sn, cs);
                     nxp = x + bx * edt + R * cs;
@@ -524,6 +586,9 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             } else if (!dom.inside(nxp, nyp)) {
                 segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
                 exited = true;
+            } else if constexpr (SCHEME == 1 && FAST && sizeof(Real) == 8) {
+                exited = bridge_exp_fast<Real>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx,
+                                               hy, edge);
             } else if constexpr (SCHEME == 1) {
                 exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T,
                                                       rng, hx, hy, edge);

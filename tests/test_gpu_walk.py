@@ -196,11 +196,14 @@ def test_numerical_error_after_1024_epochs(ctx):
         sdd.mc_estimate((0.5, 0.5), 0, m, UNIT, bd, cfg, ctx=ctx)
 
 
-def test_analytic_drift_tracks_reference_fd_paths(ctx):
+@pytest.mark.parametrize("scheme", ["linear", "exponential"])
+def test_analytic_drift_tracks_reference_fd_paths(ctx, scheme):
     # analytic grad(w)/w vs the reference's FD drift: same streams, paths
-    # structurally identical except for rare near-threshold decisions
+    # structurally identical except for rare near-threshold decisions (the
+    # exponential scheme's performance mode also takes Exp(lambda) from the
+    # raw bits, one root for the radius and the masked exit test)
     bd = sdd.make_boundary_data(sdd.MonitorFunction.ring(), sdd.GridSpec(UNIT, 65, 65))
-    cfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=1, seed=1)
+    cfg = sdd.WalkConfig(scheme=scheme, dt=1e-4, lambda_=1000.0, walks=1, seed=1)
     a = sdd.walk_dump((0.5, 0.5), 2112, sdd.MonitorFunction.ring(True), UNIT, bd, cfg, 0, 2000, ctx=ctx)
     r = sdd.walk_dump((0.5, 0.5), 2112, sdd.MonitorFunction.ring(False), UNIT, bd, cfg, 0, 2000, ctx=ctx)
     same = (a["steps"] == r["steps"]) & (a["edge"] == r["edge"])
