@@ -20,6 +20,7 @@
 // Template parameters: DV drift variant (density.cuh), Real (double/float),
 // SCHEME (0 linear, 1 exponential), BRIDGE (linear bridge test on/off).
 #pragma once
+#include <atomic>
 #include <cstdint>
 
 #include "density.cuh"
@@ -664,16 +665,17 @@ template <int DV, typename Real, int SCHEME, bool BRIDGE>
 cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
     constexpr size_t sm = walk_smem<DV, Real>();
     if constexpr (sm > 48 * 1024) {
-        // once per device and variant (a process may drive several devices)
-        static bool attr[64] = {};
+        // once per device and variant (a process may drive several devices
+        // from several host threads: setting it twice is harmless)
+        static std::atomic<bool> attr[64];
         int dev = 0;
         cudaGetDevice(&dev);
-        if (dev < 0 || dev >= 64 || !attr[dev]) {
+        if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_relaxed)) {
             const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(sm));
             if (e != cudaSuccess) return e;
-            if (dev >= 0 && dev < 64) attr[dev] = true;
+            if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_relaxed);
         }
     }
     walk_kernel<DV, Real, SCHEME, BRIDGE><<<grid, walk_block<DV, Real>(), sm, s>>>(a);
