@@ -1,4 +1,4 @@
-"""Where T_stoc goes in the paper-table workload (tools/paper_table.py):
+"""Where T_stoc goes in the paper-table workload (bench.py --paper-table):
 kernel time vs wall of the interface walk batch."""
 import os
 import sys
