@@ -8,6 +8,7 @@
 // (layout, placement, interface fill, assembly).  No compute path runs on the
 // CPU: every Monte Carlo walk and every subdomain iteration is a kernel.
 #include <cuda_runtime.h>
+#include <nvtx3/nvtx3.hpp>
 
 #include <algorithm>
 #include <chrono>
@@ -18,6 +19,7 @@
 #include <fstream>
 #include <sstream>
 #include <map>
+#include <optional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -1009,11 +1011,14 @@ sddg_status finish(sddg_ctx* c, const Fail& f) {
     return f.st;
 }
 
+// Every context entry point is an NVTX range named after the C-ABI function
+// (host-side phases in nsys / ncu --nvtx; a few ns when no tool is attached).
 #define API_BEGIN(ctx)                                   \
     if (!(ctx)) {                                        \
         g_free_err = "NULL context";                     \
         return SDDG_ERR_VALIDATION;                      \
     }                                                    \
+    const nvtx3::scoped_range _nvtx{__func__};           \
     std::lock_guard<std::mutex> _lk((ctx)->mu);          \
     try {                                                \
         ck(cudaSetDevice((ctx)->device), "cudaSetDevice");
@@ -1385,11 +1390,13 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
     // solve_sdd (proj/src/decomposition.cpp:262-385)
     const Layout L = build_layout(*dom, nx, ny, sx, sy);
     const double tb0 = now_s();
+    std::optional<nvtx3::scoped_range> phase{std::in_place, "solve_sdd: boundary data"};
     const auto tabs = boundary_tables(*dens, *dom, nx, ny, bc_mode);
     const double t_bd = now_s() - tb0;
     const sddg_boundary bd = make_boundary_view(*dom, nx, ny, tabs);
     const auto pl = plan(*dens, L, placement, k);
     const double t0 = now_s();
+    phase.emplace("solve_sdd: interface walks (T_stoc)");
     IfcResult ifc = solve_interfaces(ctx, *dens, L, pl, bd, *cfg, opts ? opts->interp : SDDG_INTERP_LINEAR);
     const double t_stoc = ifc.mc_points > 0 ? now_s() - t0 : 0.0;
     // optional interface pre-smoothing (decomposition.cpp:274-282)
@@ -1405,6 +1412,7 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
     const int64_t steps = ifc.path_steps;
 
     const double ts0 = now_s();
+    phase.emplace("solve_sdd: subdomain solves + assembly (T_sub)");
     const int n_sub = sx * sy;
     std::vector<double> u;
     std::vector<sddg_solve_info> info;
