@@ -502,6 +502,19 @@ def main():
                           "path_steps": r.path_steps, "subdomain_solves": r.subdomain_solves,
                           "solver": "rbsor tol 1e-10"}
 
+    # ---- like-for-like with the reference arm: the same walk phase with the
+    # reference's own drift (user_supplied central difference of rho = 1/w,
+    # monitor.cpp:206-219; the bit-faithful parity mode), on a 1e4-path sample
+    parity_mode = None
+    if rank == 0 and world == 1 and not args.no_mesh and args.drift == "analytic":
+        m_ref = sdd.MonitorFunction.ring(analytic=False)
+        cfg_ref = sdd.WalkConfig(scheme="linear", dt=DT, walks=10_000, seed=7, precision="fp64")
+        sdd.mc_estimate_batch_device(d_px, d_py, d_pid, d_out, m_ref, dom, bd, cfg_ref, ctx=ctx, stream=stream)
+        st = ctx.last_stats()
+        parity_mode = {"value": st["path_steps"] / (st["kernel_ms"] / 1e3), "unit": "path-steps/s",
+                       "paths_per_node": 10_000, "drift": "reference (user_supplied FD of 1/w, h = 1e-6)",
+                       "note": "same config-2 walk phase as `value`, bit-faithful parity mode, K1 time"}
+
     # ---- subdomain solver (K3/K3c), measured live: BASELINE config 3's batch
     # (128 x 129^2, shock weights, RB-SOR to 1e-10; one thread-block cluster per
     # solve) and a 2048-solve batch of the same blocks (working set 1 GB >> L2).
@@ -571,6 +584,7 @@ def main():
             "cpu_baseline": cpu,
             "mesh_gen_seconds": mesh,
             "solver": solver,
+            "parity_mode_walks": parity_mode,
             "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value * world,
         }
         print(json.dumps(line))
