@@ -329,6 +329,72 @@ def _paper_reference(n, threads, with_t1):
     return xi, eta, out
 
 
+# ------------------------------------------------------------ CPU configs
+# `python bench.py --cpu-configs`: the reference CPU build's walk rate on every
+# BASELINE config: config 1 in full, configs 2-5 on a fixed
+# deterministic node subsample with the config's dt and density (the
+# reference's user_supplied FD drift, its only route for these densities), all
+# host threads.  Reports path-steps/s, mean steps per path and the CPU seconds
+# the full config would take at that rate.  One JSON object
+# (profiles/r01_cpu_configs.json); the GPU side of each row is measured by
+# tools/config_sweep.py / tools/config3_full.py and this bench.
+CPU_CONFIGS = (
+    # name, density, grid, layout, placement, k, dt, paths per node, node stride, sample paths
+    ("config1", "ring", 65, 2, "equispaced", 31, 1e-4, 10_000, 1, 10_000),
+    ("config2", "ring", 129, 4, "all", 0, 2e-5, 100_000, 24, 2_000),
+    ("config3", "shock", 1025, 8, "all", 0, 1e-5, 1_000_000, 476, 2_000),
+    ("config4", "two-bump", 513, 4, "equidistributed", 32, 1e-5, 200_000, 8, 1_000),
+    ("config5", "ring", 0, 0, "", 0, 1e-5, 1_000_000, 128, 1_000),
+)
+
+
+def cpu_configs(args):
+    from oracle import bindings as B  # this mode is a CPU-baseline leg
+    from paper_1310_3435_b200 import sdd
+    B.ensure_built()
+    ref, orc = B.Ref(), B.Oracle()
+    threads = ref.hardware_threads()
+    kinds = {"ring": (B.RING_W, sdd.RING_W), "shock": (B.SHOCK_W, sdd.SHOCK_W),
+             "two-bump": (B.TWOBUMP_W, sdd.TWOBUMP_W)}
+    out = {"threads": threads, "drift": "reference user_supplied FD of rho = 1/w (h = 1e-6)",
+           "configs": {}}
+    for name, dens, grid, subs, place, k, dt, paths, stride, sample_paths in CPU_CONFIGS:
+        bk, sk = kinds[dens]
+        m = sdd.MonitorFunction.weight(sk)
+        dom = B.Domain(0, 1, 0, 1)
+        if name == "config5":
+            pts = np.clip(np.random.default_rng(1).uniform(0.0, 1.0, (4096, 2)), 1e-9, 1 - 1e-9)
+            px, py, pid = pts[:, 0].copy(), pts[:, 1].copy(), np.arange(4096, dtype=np.uint64)
+            grid = 129
+        else:
+            lay = sdd.build_layout(sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), grid, grid), subs, subs)
+            px, py, pid = sdd.interface_nodes(m, lay, sdd.plan_interface_points(place, k, m, lay))
+        n_nodes = len(px)
+        sel = slice(0, None, stride)
+        d = B.density(bk)
+        tabs = ref.make_boundary(d, dom, grid, grid)
+        cfg = B.walk_cfg(dt=dt, walks=sample_paths, seed=1)
+        t0 = time.perf_counter()
+        ref.mc_estimate_batch(d, dom, tabs, cfg, px[sel], py[sel], pid[sel], threads=threads)
+        sec = time.perf_counter() - t0
+        # path-steps of the same walks, counted by the bit-identical C restatement
+        steps = int(orc.mc_estimate_batch(d, dom, tabs, cfg, px[sel], py[sel], pid[sel],
+                                          threads=threads)["path_steps"].sum())
+        n_sel = len(px[sel])
+        per_path = steps / (n_sel * sample_paths)
+        rate = steps / sec
+        out["configs"][name] = {
+            "nodes": n_nodes, "paths_per_node": paths, "dt": dt, "density": dens,
+            "sample": f"every {stride}th node ({n_sel}) x {sample_paths} paths",
+            "sample_path_steps": steps, "sample_seconds": sec, "path_steps_per_s": rate,
+            "mean_steps_per_path": per_path,
+            "full_config_path_steps_est": per_path * n_nodes * paths,
+            "full_config_cpu_seconds_est": per_path * n_nodes * paths / rate}
+        print(name, json.dumps(out["configs"][name]), file=sys.stderr, flush=True)
+    print(json.dumps(out, indent=1))
+    return 0
+
+
 def paper_table(args):
     from paper_1310_3435_b200 import sdd
     ctx = sdd.Context(0)
@@ -369,6 +435,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-mesh", action="store_true", help="skip the end-to-end mesh-gen timings")
     ap.add_argument("--no-solver", action="store_true", help="skip the subdomain-solver roofline")
+    ap.add_argument("--cpu-configs", action="store_true",
+                    help="the reference CPU walk rate on every BASELINE config (CPU only)")
     ap.add_argument("--paper-table", action="store_true",
                     help="the reference's own workload (paper table / acceptance c11) vs the reference CPU")
     args = ap.parse_args()
@@ -376,6 +444,8 @@ def main():
         return run_reference(args)
     if args.paper_table:
         return paper_table(args)
+    if args.cpu_configs:
+        return cpu_configs(args)
 
     import torch
     import torch.distributed as dist
