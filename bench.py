@@ -416,10 +416,62 @@ def paper_table(args):
             rows[n]["t_total_speedup"] = rr["t_total_s"] / row["t_total_s"]
             rows[n]["t_total_speedup_fast"] = rr["t_total_s"] / row_fast["t_total_s"]
         print(n, json.dumps(rows[n]), file=sys.stderr, flush=True)
+    readme = readme_workloads(sdd, ctx, threads, not args.no_cpu_baseline)
     print(json.dumps({"workload": "paper table / acceptance c11: five-ring on [-1,1]^2, 4x4, optimal placement, "
                       "exponential lambda 1000, N 5000, seed 1, tol 1e-8", "host_threads": threads,
-                      "grids": rows}, indent=1))
+                      "grids": rows, "readme_workloads": readme}, indent=1))
     return 0
+
+
+def readme_workloads(sdd, ctx, threads, with_ref):
+    """The reference README's CLI examples (proj/README.md:68-79) on the
+    running-example density, 29^2 grid, seed 1: `stochastic-full` (every
+    interior node, N = 10000, exponential:1000) and `sdd` (2x2, optimal
+    placement, N = 10000, exponential:10000); ours on the GPU (reference-mode
+    drift, the reference Jacobi) vs the reference CPU build."""
+    m = sdd.MonitorFunction.running_example()
+    spec = sdd.GridSpec(sdd.RectDomain(0, 1, 0, 1), 29, 29)
+    out = {}
+    cfg = sdd.WalkConfig(scheme="exponential", lambda_=1000.0, walks=10_000, seed=1)
+    sdd.stochastic_full(m, spec, cfg, ctx=ctx)
+    t0 = time.perf_counter()
+    xi, eta, st = sdd.stochastic_full(m, spec, cfg, ctx=ctx)
+    row = {"gpu_s": time.perf_counter() - t0, "mc_points": st["mc_points"]}
+    if with_ref:
+        from oracle import bindings as B  # CPU-baseline leg
+        ref = B.Ref()
+        dom = B.Domain(0, 1, 0, 1)
+        d = B.density(B.RUNNING)
+        tabs = ref.make_boundary(d, dom, 29, 29)
+        ids = [(i, j) for j in range(1, 28) for i in range(1, 28)]
+        t0 = time.perf_counter()
+        e = ref.mc_estimate_batch(d, dom, tabs, B.walk_cfg(scheme="exponential", lam=1000.0, walks=10_000, seed=1),
+                                  [0.0 + i * (1.0 / 28) for i, _ in ids], [0.0 + j * (1.0 / 28) for _, j in ids],
+                                  [j * 29 + i for i, j in ids],  # GridSpec::node = min + i h
+                                  threads=threads)
+        row["reference_cpu_s"] = time.perf_counter() - t0
+        row["speedup"] = row["reference_cpu_s"] / row["gpu_s"]
+        pid = np.array([j * 29 + i for i, j in ids])
+        row["max_abs_diff_xi"] = float(np.max(np.abs(xi[pid] - e["xi"])))
+    out["stochastic_full_running_29"] = row
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("optimal", 0, m, lay)
+    wc = sdd.WalkConfig(scheme="exponential", lambda_=10_000.0, walks=10_000, seed=1)
+    sc = sdd.SolverConfig(tol=1e-8)
+    sdd.solve_sdd(m, lay, plan, wc, sc, ctx=ctx)
+    t0 = time.perf_counter()
+    r = sdd.solve_sdd(m, lay, plan, wc, sc, ctx=ctx)
+    row = {"gpu_s": time.perf_counter() - t0, "t_stoc_s": r.t_stoc, "t_sub_s": r.t_sub, "mc_points": r.mc_points}
+    if with_ref:
+        t0 = time.perf_counter()
+        rxi, reta, rt = ref.solve_sdd(d, dom, 29, 29, 2, 2, 2, 0,
+                                      B.walk_cfg(scheme="exponential", lam=10_000.0, walks=10_000, seed=1),
+                                      tol=1e-8, threads=threads)
+        row["reference_cpu_s"] = time.perf_counter() - t0
+        row["speedup"] = row["reference_cpu_s"] / row["gpu_s"]
+        row["max_abs_mesh_diff"] = float(max(np.max(np.abs(rxi - r.xi)), np.max(np.abs(reta - r.eta))))
+    out["sdd_running_29_2x2"] = row
+    return out
 
 
 def main():
