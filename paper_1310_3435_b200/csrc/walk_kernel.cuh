@@ -77,7 +77,7 @@ struct RealOps<double, FAST> {
     }
     __device__ static __forceinline__ double ex(const fm::FmTables& T, double v) {
         if constexpr (FAST) return fm::fexp_tab(T, v);
-        else return exp(v);
+        else return exp_cuda_cb(v);
     }
     __device__ static __forceinline__ double lg(const fm::FmTables& T, double v) {
         if constexpr (FAST) return fm::flog_tab(T, v);
