@@ -51,8 +51,8 @@ struct RealOps<double, FAST> {
         const double u1 = u01_open_d(a);
         const double u2 = u01_d(b);
         double s, c;
-        const double r = sqrt(-2.0 * log(u1));
-        sincos(6.283185307179586476925286766559 * u2, &s, &c);
+        const double r = sqrt(-2.0 * log_cuda_cb(u1));
+        sincos_cuda_cb(6.283185307179586476925286766559 * u2, &s, &c);
         z0 = r * c;
         z1 = r * s;
     }
@@ -81,7 +81,7 @@ struct RealOps<double, FAST> {
     }
     __device__ static __forceinline__ double lg(const fm::FmTables& T, double v) {
         if constexpr (FAST) return fm::flog_tab(T, v);
-        else return log(v);
+        else return log_cuda_cb(v);
     }
     __device__ static __forceinline__ double sq(double v) { return sqrt(v); }
 };
