@@ -224,7 +224,9 @@ typedef struct {
     int64_t max_iters; /* 0: 200 max(nx,ny)^2 */
     int32_t init_blend;
     int32_t method; /* sddg_solver_method */
-    double omega;   /* SOR factor; <= 0 picks the optimal one for the grid */
+    double omega;   /* SOR factor: > 0 as given; 0 estimates the optimal one per job
+                       from its weights (Rayleigh quotient of the Jacobi operator);
+                       < 0 the constant-coefficient formula 2/(1+sin(pi/(n-1))) */
 } sddg_solver_config;
 
 typedef struct {

@@ -88,7 +88,7 @@ struct sddg_ctx {
     std::string err;
     std::mutex mu;
     DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm;
-    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large;
+    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large, s_omega;
     DevBuf m_in, m_out, m_q, m_misc;
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
@@ -492,7 +492,10 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
             max_int_s = std::max(max_int_s, (j.nx - 2) * (j.ny - 2));
         }
     }
+    // SOR factor: sc.omega > 0 as given; 0 (default) per job from the job's
+    // weights (launch_sor_omega); < 0 the constant-coefficient grid formula
     double omega = sc.omega;
+    const bool omega_per_job = sc.method == SDDG_SOLVER_RBSOR && omega == 0.0;
     if (sc.method == SDDG_SOLVER_RBSOR && !(omega > 0.0)) {
         const double kPi = 3.14159265358979323846;
         omega = 2.0 / (1.0 + std::sin(kPi / (max_dim_all - 1)));
@@ -500,7 +503,10 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     if (sc.method == SDDG_SOLVER_JACOBI) omega = 1.0;
     const size_t wbytes = sizeof(double) * static_cast<size_t>(gnx) * gny;
     double* dw = static_cast<double*>(c->s_w.ensure(wbytes));
-    SolveJob* dj = static_cast<SolveJob*>(c->s_jobs.ensure(sizeof(SolveJob) * std::max<size_t>(1, small.size())));
+    // device job list: small jobs (K3/K3c) then large jobs (K3b), and one SOR factor per job
+    const size_t n_all = small.size() + large.size();
+    SolveJob* dj = static_cast<SolveJob*>(c->s_jobs.ensure(sizeof(SolveJob) * std::max<size_t>(1, n_all)));
+    double* domg = static_cast<double*>(c->s_omega.ensure(sizeof(double) * std::max<size_t>(1, n_all)));
     double* dbc = static_cast<double*>(c->s_bc.ensure(sizeof(double) * boff));
     double* du = static_cast<double*>(c->s_u.ensure(sizeof(double) * uoff));
     sddg_solve_info* dinfo = static_cast<sddg_solve_info*>(c->s_info.ensure(sizeof(sddg_solve_info) * n));
@@ -537,26 +543,38 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
         for (const SolveJob& j : small) info_of[a++] = pos_of_uoff[j.u_off];
         for (const SolveJob& j : large) info_of[a++] = pos_of_uoff[j.u_off];
     }
+    std::vector<SolveJob> all_jobs(small);
+    all_jobs.insert(all_jobs.end(), large.begin(), large.end());
+    std::vector<double> homg(n_all, omega);
     ck(cudaEventRecord(c->ev0, st), "event");
     int launches = 0;
-    if (!small.empty()) {
-        ck(cudaMemcpyAsync(dj, small.data(), sizeof(SolveJob) * small.size(), cudaMemcpyHostToDevice, st),
+    if (n_all) {
+        ck(cudaMemcpyAsync(dj, all_jobs.data(), sizeof(SolveJob) * n_all, cudaMemcpyHostToDevice, st),
            "h2d jobs");
+        if (omega_per_job) {
+            ck(launch_sor_omega(dw, gnx, hx, hy, static_cast<int64_t>(n_all), dj, domg, st), "omega launch");
+            ++launches;
+        } else {
+            ck(cudaMemcpyAsync(domg, homg.data(), sizeof(double) * n_all, cudaMemcpyHostToDevice, st),
+               "h2d omega");
+        }
+    }
+    if (!small.empty()) {
         if (cluster)
             ck(launch_solve_cluster(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
-                                    sc.max_iters, sc.init_blend, omega, du, dinfo, derr, st, small[0].nx,
+                                    sc.max_iters, sc.init_blend, domg, du, dinfo, derr, st, small[0].nx,
                                     small[0].ny, cluster),
                "cluster solver launch");
         else
             ck(launch_solve_batch(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
-                                  sc.max_iters, sc.init_blend, sc.method, omega, du, dinfo, derr, st,
+                                  sc.max_iters, sc.init_blend, sc.method, domg, du, dinfo, derr, st,
                                   max_n_s, max_int_s, dcoef, coef_smem ? 1 : 0),
                "solver launch");
         ++launches;
     }
     for (size_t q = 0; q < large.size(); ++q) {
         ck(launch_solve_large(dw, gnx, hx, hy, large[q], dbc, sc.tol, sc.max_iters, sc.init_blend,
-                              sc.method, omega, du, dinfo + small.size() + q, derr, dlarge, st, c->sms),
+                              sc.method, domg + small.size() + q, du, dinfo + small.size() + q, derr, dlarge, st, c->sms),
            "large solver launch");
         ++launches;
     }
@@ -1176,7 +1194,7 @@ void sddg_destroy(sddg_ctx* c) {
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
                       &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
-                      &c->s_coef, &c->s_err, &c->s_large, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
+                      &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);

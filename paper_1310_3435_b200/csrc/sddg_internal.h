@@ -101,24 +101,28 @@ struct SolveJob {
 // else in coef_scratch (n_jobs * 3*max_n doubles).  max_interior <=
 // solver_max_points() for METHOD Jacobi.
 int solver_max_points();
+// Per-job RB-SOR factor from a Rayleigh-quotient estimate of the job's Jacobi
+// spectral radius (one CTA per job; writes omegas[0..n_jobs))
+cudaError_t launch_sor_omega(const double* w_global, int gnx, double hx, double hy, int64_t n_jobs,
+                             const SolveJob* jobs, double* omegas, cudaStream_t s);
 // K3c (thread-block-cluster RB-SOR): cluster size for jobs up to max_nx x
 // max_ny whose packed weights do not fit next to u in one CTA (0: none fits)
 int solver_cluster_size(int max_nx, int max_ny);
 cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, double hy,
                                  int64_t n_jobs, const SolveJob* jobs, const double* bc, double tol,
-                                 int64_t max_iters_cfg, int init_blend, double omega, double* u,
+                                 int64_t max_iters_cfg, int init_blend, const double* omega, double* u,
                                  sddg_solve_info* info, int* err, cudaStream_t s, int max_nx,
                                  int max_ny, int cl);
 // K3b: one grid too large for shared memory, cooperative kernel; scratch 5*N+8 doubles
 cudaError_t launch_solve_large(const double* w_global, int gnx, double hx, double hy,
                                const SolveJob& job, const double* bc, double tol,
-                               int64_t max_iters_cfg, int init_blend, int method, double omega,
+                               int64_t max_iters_cfg, int init_blend, int method, const double* omega,
                                double* u_out, sddg_solve_info* info, int* err, double* scratch,
                                cudaStream_t s, int sms);
 cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
                                int64_t n_jobs, const SolveJob* jobs, const double* bc,
                                double tol, int64_t max_iters_cfg, int init_blend, int method,
-                               double omega, double* u, sddg_solve_info* info, int* err,
+                               const double* omega, double* u, sddg_solve_info* info, int* err,
                                cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem);
 

@@ -102,12 +102,13 @@ template <int METHOD, int PTS, int G = 1>
 __global__ void __launch_bounds__(kSolveThreads)
 solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
              const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
-             int64_t max_iters_cfg, int init_blend, double omega, double* __restrict__ uout,
+             int64_t max_iters_cfg, int init_blend, const double* __restrict__ omegas, double* __restrict__ uout,
              sddg_solve_info* __restrict__ info, double* __restrict__ coef_scratch,
              int64_t coef_stride, int coef_in_smem, int* err) {
     extern __shared__ double smem[];
     __shared__ double red[kSolveThreads / 32];
     const SolveJob J = jobs[blockIdx.x];
+    const double omega = omegas[blockIdx.x];  // per-job SOR factor (sor_omega_kernel)
     const int nx = J.nx, ny = J.ny;
     const int N = nx * ny;
     double* u = smem;
@@ -296,7 +297,7 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
 template <int METHOD, int PTS, int G = 1>
 cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, const double* wg,
                        int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
-                       double tol, int64_t mi, int init_blend, double omega, double* u,
+                       double tol, int64_t mi, int init_blend, const double* omega, double* u,
                        sddg_solve_info* info, double* scratch, int64_t cstride, int cin,
                        int* err) {
     auto k = solve_kernel<METHOD, PTS, G>;
@@ -333,7 +334,7 @@ template <int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kClusterThreads)
 solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
                      const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
-                     int64_t max_iters_cfg, int init_blend, double omega, double* __restrict__ uout,
+                     int64_t max_iters_cfg, int init_blend, const double* __restrict__ omegas, double* __restrict__ uout,
                      sddg_solve_info* __restrict__ info, int per_cap, int* err) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -341,6 +342,7 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
     extern __shared__ double smem[];
     __shared__ double red[kClusterThreads / 32];
     const SolveJob J = jobs[blockIdx.x / CL];
+    const double omega = omegas[blockIdx.x / CL];
     const int nx = J.nx, ny = J.ny, mi = nx - 2, mj = ny - 2;
     const int half = (mi + 1) / 2;
     const int per = (mj + CL - 1) / CL;
@@ -476,7 +478,7 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
 template <int CL>
 cudaError_t launch_cluster(int64_t n_jobs, int max_nx, int max_ny, cudaStream_t st, const double* wg,
                            int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
-                           double tol, int64_t mi, int init_blend, double omega, double* u,
+                           double tol, int64_t mi, int init_blend, const double* omega, double* u,
                            sddg_solve_info* info, int* err) {
     const size_t smem = sizeof(double) * static_cast<size_t>(cluster_smem_doubles(max_nx, max_ny, CL));
     auto k = solve_cluster_kernel<CL>;
@@ -489,7 +491,79 @@ cudaError_t launch_cluster(int64_t n_jobs, int max_nx, int max_ny, cudaStream_t 
     return cudaGetLastError();
 }
 
+// Per-job RB-SOR factor.  The optimal factor of a consistently ordered
+// operator is 2/(1+sqrt(1-rJ^2)), rJ the spectral radius of its Jacobi
+// iteration: the largest eigenvalue of Off v = r D v (D the diagonal, Off the
+// neighbour weights, detsolver.cpp:88-111).  One Rayleigh quotient
+// r = v.Off v / v.D v with the constant-coefficient ground mode
+// v = sin(pi i/(nx-1)) sin(pi j/(ny-1)) estimates it from below (to within
+// 1e-6 on config 3's shock-layer blocks, where the grid formula's factor
+// 1.952 against the optimal 1.966 takes 1,260 instead of ~700 sweeps).  For
+// constant weights v is the exact ground mode and the factor is the grid
+// formula 2/(1+sin(pi/(n-1))).  One CTA per job, fixed-order reduction: K3,
+// K3c and K3b read the same factor.
+constexpr int kOmegaThreads = 256;
+
+__global__ void __launch_bounds__(kOmegaThreads)
+sor_omega_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
+                 const SolveJob* __restrict__ jobs, double* __restrict__ omegas) {
+    __shared__ double red[2][kOmegaThreads / 32];
+    const SolveJob J = jobs[blockIdx.x];
+    const int nx = J.nx, ny = J.ny, mi = nx - 2, mj = ny - 2;
+    const double rx = 1.0 / (nx - 1), ry = 1.0 / (ny - 1);
+    double num = 0.0, den = 0.0;
+    for (int q = threadIdx.x; q < mi * mj; q += blockDim.x) {
+        const int i = 1 + q % mi, j = 1 + q / mi;
+        const double* wr = wg + (int64_t)(J.j0 + j) * gnx + (J.i0 + i);
+        const double wc = wr[0];
+        const double ce = 0.5 * (wc + wr[1]) * ihx2, cw = 0.5 * (wr[-1] + wc) * ihx2;
+        const double cn = 0.5 * (wc + wr[gnx]) * ihy2, cs = 0.5 * (wr[-gnx] + wc) * ihy2;
+        // sinpi is exactly 0 on the boundary rows/columns
+        const double si = sinpi(i * rx), sj = sinpi(j * ry);
+        const double v = si * sj;
+        const double off = sj * (ce * sinpi((i + 1) * rx) + cw * sinpi((i - 1) * rx)) +
+                           si * (cn * sinpi((j + 1) * ry) + cs * sinpi((j - 1) * ry));
+        num = fma(v, off, num);
+        den = fma(v * v, (ce + cw) + (cn + cs), den);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        red[0][wid] = num;
+        red[1][wid] = den;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            a += red[0][k];
+            b += red[1][k];
+        }
+        const double r = a / b;
+        double om;
+        if (r > 0.0 && r < 1.0) {
+            om = 2.0 / (1.0 + sqrt((1.0 - r) * (1.0 + r)));
+        } else {  // degenerate job (no interior, or non-finite weights): grid formula
+            om = 2.0 / (1.0 + sinpi(1.0 / (max(nx, ny) - 1)));
+        }
+        omegas[blockIdx.x] = om;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_sor_omega(const double* w_global, int gnx, double hx, double hy, int64_t n_jobs,
+                             const SolveJob* jobs, double* omegas, cudaStream_t s) {
+    if (n_jobs <= 0) return cudaSuccess;
+    const double ihx2 = 1.0 / (hx * hx), ihy2 = 1.0 / (hy * hy);
+    sor_omega_kernel<<<static_cast<unsigned>(n_jobs), kOmegaThreads, 0, s>>>(w_global, gnx, ihx2, ihy2,
+                                                                           jobs, omegas);
+    return cudaGetLastError();
+}
 
 int solver_max_points() { return kSolveThreads * 32; }
 
@@ -507,7 +581,7 @@ int solver_cluster_size(int max_nx, int max_ny) {
 
 cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, double hy,
                                  int64_t n_jobs, const SolveJob* jobs, const double* bc, double tol,
-                                 int64_t max_iters_cfg, int init_blend, double omega, double* u,
+                                 int64_t max_iters_cfg, int init_blend, const double* omega, double* u,
                                  sddg_solve_info* info, int* err, cudaStream_t s, int max_nx,
                                  int max_ny, int cl) {
     if (n_jobs <= 0) return cudaSuccess;
@@ -526,7 +600,7 @@ cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, dou
 cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
                                int64_t n_jobs, const SolveJob* jobs, const double* bc,
                                double tol, int64_t max_iters_cfg, int init_blend, int method,
-                               double omega, double* u, sddg_solve_info* info, int* err,
+                               const double* omega, double* u, sddg_solve_info* info, int* err,
                                cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem) {
     if (n_jobs <= 0) return cudaSuccess;
@@ -592,12 +666,13 @@ template <int METHOD>
 __global__ void __launch_bounds__(256)
 solve_large_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2, SolveJob J,
                    const double* __restrict__ bc, double tol, int64_t max_iters_cfg, int init_blend,
-                   double omega, double* __restrict__ u, double* __restrict__ v,
+                   const double* __restrict__ omegas, double* __restrict__ u, double* __restrict__ v,
                    double* __restrict__ cE, double* __restrict__ cN, double* __restrict__ inv,
                    unsigned long long* slots, sddg_solve_info* info, int* err) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double red[8];
+    const double omega = *omegas;
     const int nx = J.nx, ny = J.ny, N = nx * ny;
     const double* B = bc + J.bc_off;
     const double* T = B + nx;
@@ -761,7 +836,7 @@ solve_large_kernel(const double* __restrict__ wg, int gnx, double ihx2, double i
 // Solves one job with the cooperative kernel; scratch holds 5*N doubles + 8 slots.
 cudaError_t launch_solve_large(const double* w_global, int gnx, double hx, double hy,
                                const SolveJob& job, const double* bc, double tol,
-                               int64_t max_iters_cfg, int init_blend, int method, double omega,
+                               int64_t max_iters_cfg, int init_blend, int method, const double* omega,
                                double* u_out, sddg_solve_info* info, int* err, double* scratch,
                                cudaStream_t s, int sms) {
     const double ihx2 = 1.0 / (hx * hx);

@@ -261,3 +261,38 @@ def test_single_domain_513_config4_reference_solve(oracle, ctx):
     assert all(r.converged for r in res)
     X = res[0].values.reshape(n, n)
     assert (np.diff(X, axis=1) > 0).all()   # xi strictly increasing in x (max principle per row)
+
+
+def test_per_job_sor_factor_same_fixed_point_fewer_sweeps(oracle, ctx):
+    # The default RB-SOR factor (omega = 0) is estimated per job from its
+    # weights (a Rayleigh quotient of the Jacobi operator, solver.cu
+    # sor_omega_kernel).  On config 3's shock-layer blocks the grid formula
+    # (omega < 0) is far from optimal: the per-job factor must land on the
+    # same fixed point (within the 1e-10 bar) in fewer sweeps for the slowest
+    # job, and cost nothing on the constant-weight blocks.
+    g = 1025
+    w = oracle.weight_values(B.density(B.SHOCK_W), UNIT, g, g)
+    rng = np.random.default_rng(5)
+    subs, bcs = [], []
+    for b in range(8):  # one column of blocks, crossing the shock layer
+        v0, v1, v2, v3 = np.sort(rng.random(4))
+        edge = lambda lo, hi: np.linspace(lo, hi, 129)  # noqa: E731
+        bcs.append(sdd.EdgeData(edge(v0, v1), edge(v2, v3), edge(v0, v2), edge(v1, v3)))
+        subs.append((0, b * 128, 129, 129))
+    est = sdd.solve_dirichlet_batch(w, g, g, 1 / 1024, 1 / 1024, subs, bcs,
+                                    sdd.SolverConfig(tol=1e-12, method="rbsor", omega=0.0), ctx=ctx)
+    grid = sdd.solve_dirichlet_batch(w, g, g, 1 / 1024, 1 / 1024, subs, bcs,
+                                     sdd.SolverConfig(tol=1e-12, method="rbsor", omega=-1.0), ctx=ctx)
+    assert all(r.converged for r in est + grid)
+    for a, b in zip(est, grid):
+        assert np.max(np.abs(a.values - b.values)) <= 1e-10
+    assert max(r.iterations for r in est) < 0.8 * max(r.iterations for r in grid)
+    # constant weights: the estimate is the grid formula's factor
+    ones = np.ones(g * g)
+    e1 = sdd.solve_dirichlet_batch(ones, g, g, 1 / 1024, 1 / 1024, subs[:2], bcs[:2],
+                                   sdd.SolverConfig(tol=1e-12, method="rbsor", omega=0.0), ctx=ctx)
+    g1 = sdd.solve_dirichlet_batch(ones, g, g, 1 / 1024, 1 / 1024, subs[:2], bcs[:2],
+                                   sdd.SolverConfig(tol=1e-12, method="rbsor", omega=-1.0), ctx=ctx)
+    for a, b in zip(e1, g1):
+        assert abs(a.iterations - b.iterations) <= 2
+        assert np.max(np.abs(a.values - b.values)) <= 1e-10
