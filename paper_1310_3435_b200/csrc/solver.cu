@@ -320,14 +320,43 @@ cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, cons
 // through distributed shared memory, and a cluster barrier publishes them.
 // The per-sweep maximum update is all-gathered the same way, so every CTA
 // takes the same convergence decision (the K3 stopping rule).
-constexpr int kClusterThreads = 256;
+#ifndef SDDG_K3C_THREADS
+#define SDDG_K3C_THREADS 256
+#endif
+#ifndef SDDG_K3C_G
+#define SDDG_K3C_G 1
+#endif
+constexpr int kClusterThreads = SDDG_K3C_THREADS;
+// slots per thread whose loads (weights and the five u values) are all issued
+// before their updates: points of one colour never read one another, so a
+// group's loads overlap instead of serialising on each update's store
+constexpr int kClusterG = SDDG_K3C_G;
+// per-sweep maximum slots: one per (rank, warp), up to 8 ranks x 32 warps
+constexpr int kClusterSlots = 8 * 32;
 
 // shared-memory doubles of one CTA: u strip (per + 2 rows), the packed weights
 // (2 colours x 2 double2 per slot, per * half slots), CL maximum slots
 __host__ __device__ inline int64_t cluster_smem_doubles(int nx, int ny, int cl) {
     const int mj = ny - 2, half = (nx - 1) / 2;
     const int per = (mj + cl - 1) / cl;
-    return ((static_cast<int64_t>(per + 2) * nx + 1) & ~1LL) + 8LL * per * half + 8;
+    return ((static_cast<int64_t>(per + 2) * nx + 1) & ~1LL) + 8LL * per * half + kClusterSlots;
+}
+
+// Distributed shared memory through explicit shared::cluster addresses: a
+// generic store into a peer CTA forces the cluster barrier's release to a
+// GPU-scope fence (MEMBAR.ALL.GPU); these keep it at cluster scope.
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(r)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_st_f64(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 template <int CL>
@@ -380,9 +409,13 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
     }
     // neighbours' strips: my first row is rank-1's top halo, my last row
     // rank+1's bottom halo (same shared-memory layout in every CTA)
-    double* below = rank > 0 ? cluster.map_shared_rank(us, rank - 1) : nullptr;
-    double* above = (rank + 1 < CL && rb < ny - 1) ? cluster.map_shared_rank(us, rank + 1) : nullptr;
+    const bool has_below = rank > 0, has_above = rank + 1 < CL && rb < ny - 1;
     const int below_row = per + 1;  // local index of row ra in rank-1's strip
+    // the neighbours' u strips in the cluster window: my local point c of
+    // strip row 0 is rank-1's point c + (below_row - 1) nx, of strip row
+    // rows-1 rank+1's point c - rows nx (its halo row 0)
+    const uint32_t below_us = has_below ? cluster_addr(us, rank - 1) : 0u;
+    const uint32_t above_us = has_above ? cluster_addr(us, rank + 1) : 0u;
     cluster.sync();
 
     const int64_t max_iters =
@@ -392,6 +425,12 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
     bool conv = false;
     const int l_first = tid / half, s_first = tid % half;
     const int dl = nt / half, ds = nt % half;
+    // per-sweep maximum update: every warp stores its maximum into its own
+    // slot (rank, warp) of every CTA; after the barrier each thread takes the
+    // exact maximum of the CL * nwarps slots.  A slot is rewritten only after
+    // the next sweep's first barrier, which every reader passes after reading.
+    const int nwarps = nt >> 5;
+    double* wslot = slots + rank * nwarps + (tid >> 5);
     while (iters < max_iters) {
         ++iters;
         double lupd = 0.0;
@@ -400,43 +439,66 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
             const double2* P = PQ + colour * 2 * cap;
             const double2* Q = P + cap;
             int lr = l_first, sl = s_first;
-            for (int q = tid; q < nsl; q += nt) {
-                const int j = ra + lr;
-                const int i = 2 * sl + 1 + ((j + 1 + colour) & 1);
-                if (i <= mi) {
-                    const int c = (lr + 1) * nx + i;
-                    const double2 ew = P[q], ns = Q[q];
-                    const double uc = us[c];
-                    const double nv =
-                        sor_point(ew, ns, us[c + 1], us[c - 1], us[c + nx], us[c - nx], uc, omega);
-                    const double du = fabs(nv - uc);
+            for (int q0 = tid; q0 < nsl; q0 += kClusterG * nt) {
+                double2 ew[kClusterG], ns[kClusterG];
+                double ue[kClusterG], uw[kClusterG], un[kClusterG], usn[kClusterG], uc[kClusterG];
+                int cc[kClusterG], ll[kClusterG];
+#pragma unroll
+                for (int k = 0; k < kClusterG; ++k) {
+                    const int q = q0 + k * nt;
+                    const int j = ra + lr;
+                    const int i = 2 * sl + 1 + ((j + 1 + colour) & 1);
+                    cc[k] = (q < nsl && i <= mi) ? (lr + 1) * nx + i : -1;
+                    ll[k] = lr;
+                    if (cc[k] >= 0) {
+                        const int c = cc[k];
+                        ew[k] = P[q];
+                        ns[k] = Q[q];
+                        uc[k] = us[c];
+                        ue[k] = us[c + 1];
+                        uw[k] = us[c - 1];
+                        un[k] = us[c + nx];
+                        usn[k] = us[c - nx];
+                    }
+                    sl += ds;
+                    lr += dl;
+                    if (sl >= half) {
+                        sl -= half;
+                        ++lr;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kClusterG; ++k) {
+                    if (cc[k] < 0) continue;
+                    const double nv = sor_point(ew[k], ns[k], ue[k], uw[k], un[k], usn[k], uc[k], omega);
+                    const double du = fabs(nv - uc[k]);
                     lupd = lupd < du ? du : lupd;
-                    us[c] = nv;
+                    us[cc[k]] = nv;
+                    // an edge row's point also into the neighbour's halo row: the
+                    // neighbour reads only the other colour's halo points during
+                    // this colour, and the cluster barrier publishes it
+                    if (ll[k] == 0 && has_below)
+                        cluster_st_f64(below_us + 8u * static_cast<uint32_t>(cc[k] + (below_row - 1) * nx), nv);
+                    if (ll[k] == rows - 1 && has_above)
+                        cluster_st_f64(above_us + 8u * static_cast<uint32_t>(cc[k] - rows * nx), nv);
                 }
-                sl += ds;
-                lr += dl;
-                if (sl >= half) {
-                    sl -= half;
-                    ++lr;
-                }
-            }
-            __syncthreads();
-            // this colour's points of the edge rows into the neighbours' halos
-            for (int i = 1 + tid; i <= mi; i += nt) {
-                if (below && ((ra + 1 + colour + i) & 1) == 1)
-                    below[below_row * nx + i] = us[nx + i];
-                if (above && ((rb - 1 + 1 + colour + i) & 1) == 1)
-                    above[i] = us[rows * nx + i];
             }
             if (colour == 1) {
-                const double m = BlockMax::reduce(lupd, red);
-                if (tid < CL) cluster.map_shared_rank(slots, tid)[rank] = m;
+                double m = lupd;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double v = __shfl_xor_sync(0xffffffffu, m, o);
+                    m = m < v ? v : m;
+                }
+                if ((tid & 31) == 0) {
+#pragma unroll
+                    for (int r = 0; r < CL; ++r) cluster_st_f64(cluster_addr(wslot, r), m);
+                }
             }
-            cluster.sync();
+            cluster_barrier();
         }
         upd = slots[0];
-#pragma unroll
-        for (int r = 1; r < CL; ++r) upd = upd < slots[r] ? slots[r] : upd;
+        for (int k = 1; k < CL * nwarps; ++k) upd = upd < slots[k] ? slots[k] : upd;
         if (upd < tol) {
             if (upd == 0.0 || upd < 1e-4 * tol) {
                 conv = true;
@@ -570,7 +632,10 @@ int solver_max_points() { return kSolveThreads * 32; }
 int solver_cluster_size(int max_nx, int max_ny) {
     if (std::getenv("SDDG_NO_CLUSTER_SOLVER")) return 0;
     const int mj = max_ny - 2;
+    const char* force = std::getenv("SDDG_CLUSTER_SIZE");  // A/B: smallest allowed size at least this
+    const int cl_min = force ? std::atoi(force) : 2;
     for (int cl : {2, 4, 8}) {
+        if (cl < cl_min) continue;
         const int per = (mj + cl - 1) / cl;
         if (sizeof(double) * cluster_smem_doubles(max_nx, max_ny, cl) <= 227 * 1024 &&
             (cl - 1) * per < mj && per >= 2)  // every strip non-empty

@@ -27,9 +27,14 @@ for s in range(n_jobs):
 x = np.linspace(0, 1, g)
 X, Y = np.meshgrid(x, x)
 w = (1.0 + 20.0 / np.cosh(50 * (Y - 0.5 - 0.15 * np.sin(2 * np.pi * X))) ** 2).ravel()
-res = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), jobs, bcs,
-                                sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx)
-st = ctx.last_stats()
+reps = int(os.environ.get("SOLVER_REPS", "1"))  # > 1: best of reps (timing); 1 for ncu
+best = None
+for _ in range(reps):
+    res = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), jobs, bcs,
+                                    sdd.SolverConfig(tol=1e-10, method="rbsor"), ctx=ctx)
+    if best is None or ctx.last_stats()["kernel_ms"] < best["kernel_ms"]:
+        best = ctx.last_stats()
+st = best
 its = np.array([r.iterations for r in res])
 upd = float(np.sum(its) * (bxy - 2) ** 2)
 print(f"{n_jobs} x {bxy}^2 rbsor: {st['kernel_ms']:.2f} ms, sweeps mean {its.mean():.1f} max {its.max()}, "
