@@ -88,7 +88,7 @@ struct sddg_ctx {
     std::string err;
     std::mutex mu;
     DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm;
-    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large, s_omega;
+    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large, s_omega, s_perm;
     DevBuf m_in, m_out, m_q, m_misc;
     int64_t last_steps = 0, last_launches = 0;
     double last_ms = 0.0;
@@ -507,6 +507,7 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     const size_t n_all = small.size() + large.size();
     SolveJob* dj = static_cast<SolveJob*>(c->s_jobs.ensure(sizeof(SolveJob) * std::max<size_t>(1, n_all)));
     double* domg = static_cast<double*>(c->s_omega.ensure(sizeof(double) * std::max<size_t>(1, n_all)));
+    int* dperm = static_cast<int*>(c->s_perm.ensure(sizeof(int) * std::max<size_t>(1, small.size())));
     double* dbc = static_cast<double*>(c->s_bc.ensure(sizeof(double) * boff));
     double* du = static_cast<double*>(c->s_u.ensure(sizeof(double) * uoff));
     sddg_solve_info* dinfo = static_cast<sddg_solve_info*>(c->s_info.ensure(sizeof(sddg_solve_info) * n));
@@ -554,20 +555,30 @@ void solve_batch_host(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
         if (omega_per_job) {
             ck(launch_sor_omega(dw, gnx, hx, hy, static_cast<int64_t>(n_all), dj, domg, st), "omega launch");
             ++launches;
+            // K3 blocks in descending factor order, so the slowest solves start
+            // in the first waves (2048 x 129^2: 41.5 -> 39.9 ms).  Not for K3c:
+            // on the config-3 batch the order measured slower (4.9-5.2 -> 5.7 ms)
+            if (!small.empty() && !cluster && !std::getenv("SDDG_NO_JOB_ORDER")) {
+                ck(launch_order_jobs(domg, static_cast<int64_t>(small.size()), dperm, st), "order launch");
+                ++launches;
+            } else {
+                dperm = nullptr;
+            }
         } else {
             ck(cudaMemcpyAsync(domg, homg.data(), sizeof(double) * n_all, cudaMemcpyHostToDevice, st),
                "h2d omega");
+            dperm = nullptr;
         }
     }
     if (!small.empty()) {
         if (cluster)
             ck(launch_solve_cluster(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
-                                    sc.max_iters, sc.init_blend, domg, du, dinfo, derr, st, small[0].nx,
+                                    sc.max_iters, sc.init_blend, domg, dperm, du, dinfo, derr, st, small[0].nx,
                                     small[0].ny, cluster),
                "cluster solver launch");
         else
             ck(launch_solve_batch(dw, gnx, hx, hy, static_cast<int64_t>(small.size()), dj, dbc, sc.tol,
-                                  sc.max_iters, sc.init_blend, sc.method, domg, du, dinfo, derr, st,
+                                  sc.max_iters, sc.init_blend, sc.method, domg, dperm, du, dinfo, derr, st,
                                   max_n_s, max_int_s, dcoef, coef_smem ? 1 : 0),
                "solver launch");
         ++launches;
@@ -1194,7 +1205,7 @@ void sddg_destroy(sddg_ctx* c) {
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
                       &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
-                      &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
+                      &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->s_perm, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
     if (c->ev0) cudaEventDestroy(c->ev0);

@@ -105,13 +105,18 @@ int solver_max_points();
 // spectral radius (one CTA per job; writes omegas[0..n_jobs))
 cudaError_t launch_sor_omega(const double* w_global, int gnx, double hx, double hy, int64_t n_jobs,
                              const SolveJob* jobs, double* omegas, cudaStream_t s);
+// Launch order of the K3/K3c blocks: jobs by descending SOR factor (a larger
+// factor means a slower-converging job), ties in batch order; perm[n_jobs]
+cudaError_t launch_order_jobs(const double* omegas, int64_t n_jobs, int* perm, cudaStream_t s);
+// perm (nullable): block b solves job perm[b]; info and omegas stay in job order
 // K3c (thread-block-cluster RB-SOR): cluster size for jobs up to max_nx x
 // max_ny whose packed weights do not fit next to u in one CTA (0: none fits)
 int solver_cluster_size(int max_nx, int max_ny);
 cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, double hy,
                                  int64_t n_jobs, const SolveJob* jobs, const double* bc, double tol,
-                                 int64_t max_iters_cfg, int init_blend, const double* omega, double* u,
-                                 sddg_solve_info* info, int* err, cudaStream_t s, int max_nx,
+                                 int64_t max_iters_cfg, int init_blend, const double* omega,
+                                 const int* perm, double* u, sddg_solve_info* info, int* err,
+                                 cudaStream_t s, int max_nx,
                                  int max_ny, int cl);
 // K3b: one grid too large for shared memory, cooperative kernel; scratch 5*N+8 doubles
 cudaError_t launch_solve_large(const double* w_global, int gnx, double hx, double hy,
@@ -122,8 +127,8 @@ cudaError_t launch_solve_large(const double* w_global, int gnx, double hx, doubl
 cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
                                int64_t n_jobs, const SolveJob* jobs, const double* bc,
                                double tol, int64_t max_iters_cfg, int init_blend, int method,
-                               const double* omega, double* u, sddg_solve_info* info, int* err,
-                               cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
+                               const double* omega, const int* perm, double* u, sddg_solve_info* info,
+                               int* err, cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem);
 
 // smooth.cu: K6 Perona-Malik FTCS, K7 interface loess

@@ -102,13 +102,16 @@ template <int METHOD, int PTS, int G = 1>
 __global__ void __launch_bounds__(kSolveThreads)
 solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
              const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
-             int64_t max_iters_cfg, int init_blend, const double* __restrict__ omegas, double* __restrict__ uout,
+             int64_t max_iters_cfg, int init_blend, const double* __restrict__ omegas,
+             const int* __restrict__ perm, double* __restrict__ uout,
              sddg_solve_info* __restrict__ info, double* __restrict__ coef_scratch,
              int64_t coef_stride, int coef_in_smem, int* err) {
     extern __shared__ double smem[];
     __shared__ double red[kSolveThreads / 32];
-    const SolveJob J = jobs[blockIdx.x];
-    const double omega = omegas[blockIdx.x];  // per-job SOR factor (sor_omega_kernel)
+    // job of this CTA: perm (longest expected solves first) or the batch order
+    const int jq = perm ? perm[blockIdx.x] : static_cast<int>(blockIdx.x);
+    const SolveJob J = jobs[jq];
+    const double omega = omegas[jq];  // per-job SOR factor (sor_omega_kernel)
     const int nx = J.nx, ny = J.ny;
     const int N = nx * ny;
     double* u = smem;
@@ -290,21 +293,21 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
         r.final_update = upd;
         r.converged = conv ? 1 : 0;
         r.reserved = 0;
-        info[blockIdx.x] = r;
+        info[jq] = r;
     }
 }
 
 template <int METHOD, int PTS, int G = 1>
 cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, const double* wg,
                        int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
-                       double tol, int64_t mi, int init_blend, const double* omega, double* u,
+                       double tol, int64_t mi, int init_blend, const double* omega, const int* perm, double* u,
                        sddg_solve_info* info, double* scratch, int64_t cstride, int cin,
                        int* err) {
     auto k = solve_kernel<METHOD, PTS, G>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k<<<grid, threads, smem, st>>>(wg, gnx, ihx2, ihy2, jobs, bc, tol, mi, init_blend, omega, u,
+    k<<<grid, threads, smem, st>>>(wg, gnx, ihx2, ihy2, jobs, bc, tol, mi, init_blend, omega, perm, u,
                                    info, scratch, cstride, cin, err);
     return cudaGetLastError();
 }
@@ -363,15 +366,17 @@ template <int CL>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kClusterThreads)
 solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
                      const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
-                     int64_t max_iters_cfg, int init_blend, const double* __restrict__ omegas, double* __restrict__ uout,
+                     int64_t max_iters_cfg, int init_blend, const double* __restrict__ omegas,
+                     const int* __restrict__ perm, double* __restrict__ uout,
                      sddg_solve_info* __restrict__ info, int per_cap, int* err) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = static_cast<int>(cluster.block_rank());
     extern __shared__ double smem[];
     __shared__ double red[kClusterThreads / 32];
-    const SolveJob J = jobs[blockIdx.x / CL];
-    const double omega = omegas[blockIdx.x / CL];
+    const int jq = perm ? perm[blockIdx.x / CL] : static_cast<int>(blockIdx.x / CL);
+    const SolveJob J = jobs[jq];
+    const double omega = omegas[jq];
     const int nx = J.nx, ny = J.ny, mi = nx - 2, mj = ny - 2;
     const int half = (mi + 1) / 2;
     const int per = (mj + CL - 1) / CL;
@@ -532,7 +537,7 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
         r.final_update = upd;
         r.converged = conv ? 1 : 0;
         r.reserved = 0;
-        info[blockIdx.x / CL] = r;
+        info[jq] = r;
     }
     cluster.sync();  // no CTA leaves while a neighbour may still store into it
 }
@@ -540,7 +545,7 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
 template <int CL>
 cudaError_t launch_cluster(int64_t n_jobs, int max_nx, int max_ny, cudaStream_t st, const double* wg,
                            int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
-                           double tol, int64_t mi, int init_blend, const double* omega, double* u,
+                           double tol, int64_t mi, int init_blend, const double* omega, const int* perm, double* u,
                            sddg_solve_info* info, int* err) {
     const size_t smem = sizeof(double) * static_cast<size_t>(cluster_smem_doubles(max_nx, max_ny, CL));
     auto k = solve_cluster_kernel<CL>;
@@ -549,7 +554,7 @@ cudaError_t launch_cluster(int64_t n_jobs, int max_nx, int max_ny, cudaStream_t 
     if (e != cudaSuccess) return e;
     const int per_cap = (max_ny - 2 + CL - 1) / CL;
     k<<<static_cast<unsigned>(n_jobs * CL), kClusterThreads, smem, st>>>(
-        wg, gnx, ihx2, ihy2, jobs, bc, tol, mi, init_blend, omega, u, info, per_cap, err);
+        wg, gnx, ihx2, ihy2, jobs, bc, tol, mi, init_blend, omega, perm, u, info, per_cap, err);
     return cudaGetLastError();
 }
 
@@ -627,6 +632,30 @@ cudaError_t launch_sor_omega(const double* w_global, int gnx, double hx, double 
     return cudaGetLastError();
 }
 
+namespace {
+// rank of job i = number of jobs ordered before it (larger factor first,
+// ties by index): a permutation, O(n^2) over a few thousand jobs at most
+__global__ void __launch_bounds__(256) order_jobs_kernel(const double* __restrict__ omegas, int n,
+                                                         int* __restrict__ perm) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double oi = omegas[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+        const double oj = omegas[j];
+        rank += (oj > oi || (oj == oi && j < i)) ? 1 : 0;
+    }
+    perm[rank] = i;
+}
+}  // namespace
+
+cudaError_t launch_order_jobs(const double* omegas, int64_t n_jobs, int* perm, cudaStream_t s) {
+    if (n_jobs <= 0) return cudaSuccess;
+    const int n = static_cast<int>(n_jobs);
+    order_jobs_kernel<<<(n + 255) / 256, 256, 0, s>>>(omegas, n, perm);
+    return cudaGetLastError();
+}
+
 int solver_max_points() { return kSolveThreads * 32; }
 
 int solver_cluster_size(int max_nx, int max_ny) {
@@ -646,18 +675,18 @@ int solver_cluster_size(int max_nx, int max_ny) {
 
 cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, double hy,
                                  int64_t n_jobs, const SolveJob* jobs, const double* bc, double tol,
-                                 int64_t max_iters_cfg, int init_blend, const double* omega, double* u,
+                                 int64_t max_iters_cfg, int init_blend, const double* omega, const int* perm, double* u,
                                  sddg_solve_info* info, int* err, cudaStream_t s, int max_nx,
                                  int max_ny, int cl) {
     if (n_jobs <= 0) return cudaSuccess;
     const double ihx2 = 1.0 / (hx * hx), ihy2 = 1.0 / (hy * hy);
     switch (cl) {
         case 2: return launch_cluster<2>(n_jobs, max_nx, max_ny, s, w_global, gnx, ihx2, ihy2, jobs, bc,
-                                         tol, max_iters_cfg, init_blend, omega, u, info, err);
+                                         tol, max_iters_cfg, init_blend, omega, perm, u, info, err);
         case 4: return launch_cluster<4>(n_jobs, max_nx, max_ny, s, w_global, gnx, ihx2, ihy2, jobs, bc,
-                                         tol, max_iters_cfg, init_blend, omega, u, info, err);
+                                         tol, max_iters_cfg, init_blend, omega, perm, u, info, err);
         case 8: return launch_cluster<8>(n_jobs, max_nx, max_ny, s, w_global, gnx, ihx2, ihy2, jobs, bc,
-                                         tol, max_iters_cfg, init_blend, omega, u, info, err);
+                                         tol, max_iters_cfg, init_blend, omega, perm, u, info, err);
     }
     return cudaErrorInvalidValue;
 }
@@ -665,7 +694,7 @@ cudaError_t launch_solve_cluster(const double* w_global, int gnx, double hx, dou
 cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, double hy,
                                int64_t n_jobs, const SolveJob* jobs, const double* bc,
                                double tol, int64_t max_iters_cfg, int init_blend, int method,
-                               const double* omega, double* u, sddg_solve_info* info, int* err,
+                               const double* omega, const int* perm, double* u, sddg_solve_info* info, int* err,
                                cudaStream_t s, int max_n, int max_interior, double* coef_scratch,
                                int coef_in_smem) {
     if (n_jobs <= 0) return cudaSuccess;
@@ -680,16 +709,16 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
     if (method == SDDG_SOLVER_RBSOR)
         return coef_in_smem
                    ? launch_one<1, 1, 1>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
-                                         max_iters_cfg, init_blend, omega, u, info, coef_scratch,
+                                         max_iters_cfg, init_blend, omega, perm, u, info, coef_scratch,
                                          cstride, coef_in_smem, err)
                    : launch_one<1, 1, 4>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
-                                         max_iters_cfg, init_blend, omega, u, info, coef_scratch,
+                                         max_iters_cfg, init_blend, omega, perm, u, info, coef_scratch,
                                          cstride, coef_in_smem, err);
     const int pts = (max_interior + T - 1) / T;
 #define SDDG_J(P)                                                                             \
     if (pts <= P)                                                                             \
         return launch_one<0, P>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,   \
-                                max_iters_cfg, init_blend, omega, u, info, coef_scratch,      \
+                                max_iters_cfg, init_blend, omega, perm, u, info, coef_scratch,      \
                                 cstride, coef_in_smem, err);
     SDDG_J(1) SDDG_J(2) SDDG_J(4) SDDG_J(8) SDDG_J(16) SDDG_J(32)
 #undef SDDG_J
