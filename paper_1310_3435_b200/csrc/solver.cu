@@ -359,7 +359,11 @@ __device__ __forceinline__ void cluster_st_f64(uint32_t addr, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
 __device__ __forceinline__ void cluster_barrier() {
+#ifdef SDDG_K3C_RELAXED_BARRIER  // A/B measurement of the fence cost only: not a valid ordering
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+#else
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+#endif
 }
 
 template <int CL>
