@@ -334,6 +334,14 @@ constexpr int kClusterThreads = SDDG_K3C_THREADS;
 // before their updates: points of one colour never read one another, so a
 // group's loads overlap instead of serialising on each update's store
 constexpr int kClusterG = SDDG_K3C_G;
+#ifndef SDDG_K3C_MAXK
+#define SDDG_K3C_MAXK 8
+#endif
+constexpr int kK3cMaxK = SDDG_K3C_MAXK;  // K3c fast path: slots per thread and colour
+#ifndef SDDG_K3C_FAST_G
+#define SDDG_K3C_FAST_G 1
+#endif
+constexpr int kK3cFastG = SDDG_K3C_FAST_G;  // points per load group (divides kK3cMaxK)
 // per-sweep maximum slots: one per (rank, warp), up to 8 ranks x 32 warps
 constexpr int kClusterSlots = 8 * 32;
 
@@ -440,7 +448,101 @@ solve_cluster_kernel(const double* __restrict__ wg, int gnx, double ihx2, double
     // the next sweep's first barrier, which every reader passes after reading.
     const int nwarps = nt >> 5;
     double* wslot = slots + rank * nwarps + (tid >> 5);
-    while (iters < max_iters) {
+    // Fast path (every thread owns at most kK3cMaxK slots per colour, e.g.
+    // 129^2 in 4 strips of 256 threads: 8): the shared-memory offset of each
+    // owned point and its edge-row flags are computed once, so a point update
+    // is its loads, the stencil, one store and no index arithmetic.
+    const int kslots = (nsl + nt - 1) / nt;
+    if (kslots <= kK3cMaxK) {
+        int cof[2][kK3cMaxK];
+        unsigned edge_lo = 0u, edge_hi = 0u;  // bit colour*kK3cMaxK + k: store to below / above
+#pragma unroll
+        for (int colour = 0; colour < 2; ++colour) {
+#pragma unroll
+            for (int k = 0; k < kK3cMaxK; ++k) {
+                const int q = tid + k * nt;
+                const int lr = q / half, sl = q - lr * half;
+                const int i = 2 * sl + 1 + ((ra + lr + 1 + colour) & 1);
+                const bool ok = k < kslots && q < nsl && i <= mi;
+                cof[colour][k] = ok ? (lr + 1) * nx + i : -1;
+                if (ok && lr == 0 && has_below) edge_lo |= 1u << (colour * kK3cMaxK + k);
+                if (ok && lr == rows - 1 && has_above) edge_hi |= 1u << (colour * kK3cMaxK + k);
+            }
+        }
+        while (iters < max_iters) {
+            ++iters;
+            double lupd = 0.0;
+#pragma unroll
+            for (int colour = 0; colour < 2; ++colour) {
+                const double2* P = PQ + colour * 2 * cap;
+                const double2* Q = P + cap;
+                // groups of kK3cFastG points: all their loads first (points of
+                // one colour never read one another), then the updates
+#pragma unroll
+                for (int k0 = 0; k0 < kK3cMaxK; k0 += kK3cFastG) {
+                    double2 ew[kK3cFastG], ns[kK3cFastG];
+                    double ue[kK3cFastG], uw[kK3cFastG], un[kK3cFastG], usn[kK3cFastG], uc[kK3cFastG];
+#pragma unroll
+                    for (int g = 0; g < kK3cFastG; ++g) {
+                        const int c = cof[colour][k0 + g];
+                        if (c < 0) continue;
+                        const int q = tid + (k0 + g) * nt;
+                        ew[g] = P[q];
+                        ns[g] = Q[q];
+                        uc[g] = us[c];
+                        ue[g] = us[c + 1];
+                        uw[g] = us[c - 1];
+                        un[g] = us[c + nx];
+                        usn[g] = us[c - nx];
+                    }
+#pragma unroll
+                    for (int g = 0; g < kK3cFastG; ++g) {
+                        const int c = cof[colour][k0 + g];
+                        if (c < 0) continue;
+                        const double nv = sor_point(ew[g], ns[g], ue[g], uw[g], un[g], usn[g], uc[g], omega);
+                        const double du = fabs(nv - uc[g]);
+                        lupd = lupd < du ? du : lupd;
+                        us[c] = nv;
+                        const unsigned bit = 1u << (colour * kK3cMaxK + k0 + g);
+                        if (edge_lo & bit)
+                            cluster_st_f64(below_us + 8u * static_cast<uint32_t>(c + (below_row - 1) * nx), nv);
+                        if (edge_hi & bit)
+                            cluster_st_f64(above_us + 8u * static_cast<uint32_t>(c - rows * nx), nv);
+                    }
+                }
+                if (colour == 1) {
+                    double m = lupd;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const double v = __shfl_xor_sync(0xffffffffu, m, o);
+                        m = m < v ? v : m;
+                    }
+                    if ((tid & 31) == 0) {
+#pragma unroll
+                        for (int r = 0; r < CL; ++r) cluster_st_f64(cluster_addr(wslot, r), m);
+                    }
+                }
+                cluster_barrier();
+            }
+            upd = slots[0];
+            for (int k = 1; k < CL * nwarps; ++k) upd = upd < slots[k] ? slots[k] : upd;
+            if (upd < tol) {
+                if (upd == 0.0 || upd < 1e-4 * tol) {
+                    conv = true;
+                    break;
+                }
+                if (prev > 0.0 && upd < prev) {
+                    const double rho = upd / prev;
+                    if (upd * rho / (1.0 - rho) < tol) {
+                        conv = true;
+                        break;
+                    }
+                }
+            }
+            prev = upd;
+        }
+    }
+    while (!conv && kslots > kK3cMaxK && iters < max_iters) {
         ++iters;
         double lupd = 0.0;
 #pragma unroll 1
