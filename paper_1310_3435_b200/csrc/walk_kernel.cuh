@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
         if constexpr (walk_uses_tables<DV, Real>()) return dom.in_box_hi(px, py);
         else return dom.in_box(px, py);
     };
-    const DensityParams P{a.R, a.alpha, a.fd_h};
+    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h)};
     const Real dt = Real(a.dt);
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);
