@@ -630,9 +630,15 @@ def main():
     parity_mode = None
     if rank == 0 and world == 1 and not args.no_mesh and args.drift == "analytic":
         m_ref = sdd.MonitorFunction.ring(analytic=False)
+        # through the host API on the same nodes, best of two launches (the
+        # first also loads the parity-mode kernel's module)
         cfg_ref = sdd.WalkConfig(scheme="linear", dt=DT, walks=10_000, seed=7, precision="fp64")
-        sdd.mc_estimate_batch_device(d_px, d_py, d_pid, d_out, m_ref, dom, bd, cfg_ref, ctx=ctx, stream=stream)
-        st = ctx.last_stats()
+        st = None
+        for _ in range(2):
+            sdd.mc_estimate_batch(np.stack([px, py], axis=1), pid, m_ref, dom, bd, cfg_ref, ctx=ctx)
+            s_ = ctx.last_stats()
+            if st is None or s_["kernel_ms"] < st["kernel_ms"]:
+                st = s_
         parity_mode = {"value": st["path_steps"] / (st["kernel_ms"] / 1e3), "unit": "path-steps/s",
                        "paths_per_node": 10_000, "drift": "reference (user_supplied FD of 1/w, h = 1e-6)",
                        "note": "same config-2 walk phase as `value`, bit-faithful parity mode, K1 time"}
