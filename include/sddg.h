@@ -101,13 +101,16 @@ typedef struct {
     double lambda;     /* exponential rate */
     int64_t walks;     /* paths per node */
     uint64_t seed;
-    int64_t max_steps; /* steps per epoch before a restart */
+    int64_t max_steps; /* steps per epoch before a restart, 1..2^29 */
     int32_t bridge_test;
     int32_t reserved;
 } sddg_walk_config;
 
 /* sdd::McEstimate (proj/include/sdd/sde.hpp:61-68) + the raw fixed-order
- * sums and the executed path-steps (all epochs). */
+ * sums and path_steps: the steps the node's walks executed, summed over all
+ * epochs (a restarted walk counts its max_steps per failed epoch plus the
+ * exit step index of its last, sde.cpp:154-176); counted on the GPU by one
+ * atomic per finished walk. */
 typedef struct {
     double xi, eta, se_xi, se_eta;
     int64_t walks, restarts;

@@ -16,7 +16,8 @@ constexpr int kReduceThreads = 256;
 __global__ void __launch_bounds__(kReduceThreads)
 reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
               const uint32_t* __restrict__ meta, int64_t walks, const uint32_t* __restrict__ perm,
-              sddg_estimate* out, const GatherTargets gt) {
+              const unsigned long long* __restrict__ node_steps, sddg_estimate* out,
+              const GatherTargets gt) {
     __shared__ double part[4][kReduceThreads];
     __shared__ unsigned long long icnt[5][kReduceThreads / 32];
     const int64_t node = blockIdx.x;
@@ -99,8 +100,9 @@ reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
         e.sum_g = tg;
         e.sum_ff = tff;
         e.sum_gg = tgg;
-        e.path_steps = 0;  // filled by the host from the kernel counter
         const uint32_t k = perm ? perm[node] : static_cast<uint32_t>(node);
+        // executed path-steps of the node's walks (K1's per-node counter)
+        e.path_steps = node_steps ? static_cast<int64_t>(node_steps[k]) : 0;
         out[k] = e;
         // fused all-gather: store the finished record straight into every
         // rank's gather buffer (NVLink peer memory opened through CUDA IPC)
@@ -113,11 +115,12 @@ reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
 }
 
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
-                          int64_t walks, int64_t n_nodes, const uint32_t* perm, sddg_estimate* out,
+                          int64_t walks, int64_t n_nodes, const uint32_t* perm,
+                          const unsigned long long* node_steps, sddg_estimate* out,
                           cudaStream_t s, const GatherTargets& gt) {
     if (n_nodes <= 0) return cudaSuccess;
     reduce_kernel<<<static_cast<unsigned>(n_nodes), kReduceThreads, 0, s>>>(rf, rg, meta, walks, perm,
-                                                                            out, gt);
+                                                                            node_steps, out, gt);
     return cudaGetLastError();
 }
 

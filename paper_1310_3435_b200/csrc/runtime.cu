@@ -87,7 +87,7 @@ struct sddg_ctx {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::string err;
     std::mutex mu;
-    DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm;
+    DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm, nsteps;
     DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large, s_omega, s_perm;
     DevBuf m_in, m_out, m_q, m_misc;
     int64_t last_steps = 0, last_launches = 0;
@@ -114,6 +114,12 @@ void validate_walk(const sddg_walk_config& c) {
     if (c.walks > 0xFFFFFFFFLL)
         fail(SDDG_ERR_VALIDATION, "WalkConfig: walks must fit the 32-bit stream walk id");
     if (c.max_steps < 1) fail(SDDG_ERR_VALIDATION, "WalkConfig: max_steps must be >= 1");
+    // A step draws at most 7 u64s (exponential scheme: 1 + 2 + 4 edges), and
+    // the per-epoch draw counter (LaneStream::n) is 32-bit: 2^29 steps keep it
+    // below 2^32 draws, so the stream never wraps (the reference's counter
+    // would wrap at 2^32 blocks and draw differently).  Default: 1e7.
+    if (c.max_steps > (int64_t(1) << 29))
+        fail(SDDG_ERR_VALIDATION, "WalkConfig: max_steps must be <= 2^29 (536870912)");
     if (c.precision != SDDG_FP64 && c.precision != SDDG_FP32)
         fail(SDDG_ERR_VALIDATION, "WalkConfig: unknown precision");
 }
@@ -254,7 +260,7 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     if (!pos) a.box_hi[0] = a.box_hi[2] = INT32_MAX;
     a.seed = cfg.seed;
     a.rk = make_round_keys(cfg.seed);
-    a.max_steps32 = static_cast<uint32_t>(std::min<int64_t>(cfg.max_steps, 0xFFFFFFFFLL));
+    a.max_steps32 = static_cast<uint32_t>(cfg.max_steps);  // <= 2^29 (validate_walk)
 }
 
 // Longest-expected-walk-first node order (LPT): a first-exit walk from p
@@ -321,6 +327,9 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
        "h2d perm");
     Counters* cnt = static_cast<Counters*>(c->counters.ensure(sizeof(Counters)));
     ck(cudaMemsetAsync(cnt, 0, sizeof(Counters), st), "memset counters");
+    unsigned long long* nst =
+        static_cast<unsigned long long*>(c->nsteps.ensure(sizeof(unsigned long long) * n));
+    ck(cudaMemsetAsync(nst, 0, sizeof(unsigned long long) * n, st), "memset node steps");
     const int64_t W = cfg.walks;
     const int64_t npb = std::max<int64_t>(1, batch_budget_walks() / W);
     const int64_t cap = std::min(npb, n) * W;
@@ -334,6 +343,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     a.walk_lo = 0;
     a.next = &cnt->next;
     a.steps = &cnt->steps;
+    a.node_steps = nst;
     a.err_flag = &cnt->err_flag;
     a.err_info = &cnt->err_info;
     a.rec_f = rf;
@@ -360,7 +370,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         ck(cudaEventRecord(c->bev[2 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
         ck(cudaEventRecord(c->bev[2 * bi + 1], st), "event");
-        ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, d_out, st, gt ? *gt : none), "reduce launch");
+        ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, nst, d_out, st, gt ? *gt : none), "reduce launch");
         launches += 3;
     }
     Counters hc;
@@ -1204,7 +1214,7 @@ void sddg_destroy(sddg_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->perm, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->s_perm, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);

@@ -37,7 +37,7 @@ struct WalkArgs {
     int32_t box_hi[4];  // high words of box[] for the integer test (INT32_MAX: disabled)
     uint64_t seed;
     RoundKeys rk;
-    uint32_t max_steps32;  // min(max_steps, 2^32-1)
+    uint32_t max_steps32;  // max_steps (validated <= 2^29)
     // batch: total = n_nodes * walks
     const double* px;
     const double* py;
@@ -48,6 +48,7 @@ struct WalkArgs {
     uint64_t total;
     unsigned long long* next;   // global walk counter (starts at the grid size)
     unsigned long long* steps;  // executed path-steps
+    unsigned long long* node_steps;  // per-node executed path-steps (all epochs), or null
     int* err_flag;              // 3 EvaluationError, 4 NumericalError
     unsigned long long* err_info;
     // outputs: per-walk records, or per-path dumps
@@ -88,7 +89,8 @@ struct GatherTargets {
     sddg_estimate* peers[kMaxPeers];  // device pointers (local or IPC-mapped peer memory)
 };
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,
-                          int64_t walks, int64_t n_nodes, const uint32_t* perm, sddg_estimate* out,
+                          int64_t walks, int64_t n_nodes, const uint32_t* perm,
+                          const unsigned long long* node_steps, sddg_estimate* out,
                           cudaStream_t s, const GatherTargets& gt);
 
 // solver.cu: K3 batched Dirichlet solves

@@ -623,6 +623,11 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             const double fv = table_at(a.tf[edge], tn, par);
             const double gv = table_at(a.tg[edge], tn, par);
             L.steps += step;
+            // per-node path-steps of this walk, all epochs (restarts happen at
+            // exactly max_steps): one atomic per finished walk
+            if (a.node_steps)
+                atomicAdd(a.node_steps + L.node,
+                          static_cast<unsigned long long>(L.epoch) * max_steps + step);
             const uint64_t g = L.g;
             if (a.dump) {
                 sddg_path& r = a.dump[g];

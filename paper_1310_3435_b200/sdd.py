@@ -398,12 +398,13 @@ class McEstimate:
     restarts: int
     reliability_warning: bool
     edge_hits: list
+    path_steps: int = 0  # executed steps of the node's walks, all epochs (not in the reference)
 
     @staticmethod
     def from_record(r):
         return McEstimate(float(r["xi"]), float(r["eta"]), float(r["se_xi"]), float(r["se_eta"]),
                           int(r["walks"]), int(r["restarts"]), bool(r["warn"]),
-                          [int(v) for v in r["edge_hits"]])
+                          [int(v) for v in r["edge_hits"]], int(r["path_steps"]))
 
 
 def mc_estimate_batch(points, point_ids, m: MonitorFunction, domain: RectDomain,

@@ -1,0 +1,257 @@
+"""Parity at BASELINE.json's own sizes, against the reference itself
+(oracle/_ref, the unmodified reference library on the box's host cores).
+
+(a) Config 1 in full (65^2, 2x2, equispaced(31), 61 nodes x 1e4 paths,
+    dt 1e-4, ring density through the reference's user_supplied FD drift):
+    per-node estimates within 1e-10 with identical edge counts and restarts
+    (reference mc_estimate, proj/src/sde.cpp:193-246), interface lines within
+    1e-10 (solve_interfaces, proj/src/decomposition.cpp:147-248), the mesh
+    within 1e-10 of the reference's solve_sdd (decomposition.cpp:262-385) and
+    the quality statistics within 1e-6 (quality.cpp:35-80).
+(b) The benchmarked performance mode (analytic drift, fastmath; fp64 and
+    fp32) against the reference's estimates at 4 combined standard errors on
+    config 1 in full and on fixed node subsamples of configs 2-5, on
+    independent streams (different seeds).  SURVEY D8: the number of |z| > 4
+    exceedances is compared with its null expectation, plus chi^2/dof.
+(c) 16 of config 3's 128 subdomain solves (129^2, shock) against the
+    reference's Jacobi at tol 1e-13, and the RB-SOR stopping rule's distance
+    to the fixed point at the reference's default tol 1e-8.
+"""
+import concurrent.futures as cf
+import math
+
+import numpy as np
+import pytest
+
+from oracle import bindings as B
+from paper_1310_3435_b200 import sdd
+
+pytestmark = pytest.mark.gpu
+UNIT = sdd.RectDomain(0, 1, 0, 1)
+ODOM = B.Domain(0, 1, 0, 1)
+EST_TOL = 1e-10
+P_GT4 = math.erfc(4 / math.sqrt(2))  # two-sided P(|z| > 4) = 6.3e-5
+
+
+def _config1():
+    m = sdd.MonitorFunction.ring()
+    spec = sdd.GridSpec(UNIT, 65, 65)
+    lay = sdd.build_layout(spec, 2, 2)
+    plan = sdd.plan_interface_points("equispaced", 31, m, lay)
+    px, py, pid = sdd.interface_nodes(m, lay, plan)
+    return m, spec, lay, plan, px, py, pid
+
+
+@pytest.fixture(scope="module")
+def c1_reference(refimpl):
+    """The reference's config-1 estimates (all host threads), computed once."""
+    _, _, _, _, px, py, pid = _config1()
+    assert len(px) == 61
+    tabs = refimpl.make_boundary(B.density(B.RING_W), ODOM, 65, 65)
+    est = refimpl.mc_estimate_batch(B.density(B.RING_W), ODOM, tabs,
+                                    B.walk_cfg(dt=1e-4, walks=10_000, seed=1), px, py, pid, threads=0)
+    return tabs, est
+
+
+# ------------------------------------------------------------------ (a)
+def test_config1_full_estimates_bit_faithful(ctx, c1_reference):
+    m, spec, lay, plan, px, py, pid = _config1()
+    _, ref = c1_reference
+    bd = sdd.make_boundary_data(m, spec)
+    got = sdd.mc_estimate_batch(np.stack([px, py], 1), pid, m, UNIT, bd,
+                                sdd.WalkConfig(scheme="linear", dt=1e-4, walks=10_000, seed=1), ctx=ctx)
+    for f in ("xi", "eta", "se_xi", "se_eta"):
+        assert np.max(np.abs(got[f] - ref[f])) <= EST_TOL, f
+    for f in ("walks", "restarts", "warn", "edge_hits"):
+        assert np.array_equal(got[f], ref[f]), f
+    # per-node path-steps: the executed steps of every walk (all epochs);
+    # config 1 totals 1.1115e9
+    assert abs(int(got["path_steps"].sum()) - 1.1115e9) < 0.001e9
+    assert (got["path_steps"] > 500 * 10_000).all()
+
+
+def test_config1_full_interface_lines(ctx, refimpl, c1_reference):
+    m, spec, lay, plan, px, py, pid = _config1()
+    tabs, _ = c1_reference
+    bd = sdd.make_boundary_data(m, spec)
+    got = sdd.solve_interfaces(plan, m, bd, sdd.WalkConfig(scheme="linear", dt=1e-4, walks=10_000, seed=1),
+                               lay, ctx=ctx)
+    ref, mc, rs = refimpl.solve_interfaces(B.density(B.RING_W), ODOM, 65, 65, 2, 2, 1, 31, tabs,
+                                           B.walk_cfg(dt=1e-4, walks=10_000, seed=1), threads=0)
+    assert (got.mc_points, got.restarts) == (mc, rs) == (61, 0)
+    for l, (xi, eta, sxi, seta) in enumerate(ref):
+        assert np.max(np.abs(got.xi[l] - xi)) <= EST_TOL
+        assert np.max(np.abs(got.eta[l] - eta)) <= EST_TOL
+        assert np.max(np.abs(got.se_xi[l] - sxi)) <= EST_TOL
+        assert np.max(np.abs(got.se_eta[l] - seta)) <= EST_TOL
+
+
+def test_config1_full_mesh_and_quality(ctx, refimpl):
+    m, spec, lay, plan, *_ = _config1()
+    wcfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=10_000, seed=1)
+    got = sdd.solve_sdd(m, lay, plan, wcfg, sdd.SolverConfig(tol=1e-13, method="rbsor"), ctx=ctx)
+    rxi, reta, _ = refimpl.solve_sdd(B.density(B.RING_W), ODOM, 65, 65, 2, 2, 1, 31,
+                                     B.walk_cfg(dt=1e-4, walks=10_000, seed=1), tol=1e-13, threads=0)
+    assert np.max(np.abs(got.xi - rxi)) <= 1e-10
+    assert np.max(np.abs(got.eta - reta)) <= 1e-10
+    # single-domain reference meshes (cli.cpp:327-338) and the quality report
+    lay1 = sdd.build_layout(spec, 1, 1)
+    one = sdd.solve_sdd(m, lay1, sdd.plan_interface_points("all", 0, m, lay1), wcfg,
+                        sdd.SolverConfig(tol=1e-13, method="rbsor"), ctx=ctx)
+    sxi, seta = refimpl.solve_single_domain(B.density(B.RING_W), ODOM, 65, 65, tol=1e-13)
+    mesh = sdd.invert_mesh(got.xi, got.eta, spec, 65, 65, ctx=ctx)
+    ref_mesh = sdd.invert_mesh(one.xi, one.eta, spec, 65, 65, ctx=ctx)
+    q = sdd.quality_report(mesh, ref_mesh, m, ctx=ctx)
+    rx, ry = refimpl.invert_mesh(rxi, reta, 65, 65, ODOM, 65, 65)
+    srx, sry = refimpl.invert_mesh(sxi, seta, 65, 65, ODOM, 65, 65)
+    rq = refimpl.quality(rx, ry, 65, 65, ODOM, srx, sry, B.density(B.RING_W))
+    got_q = [q.q_max, q.q_mean, q.r_max, q.r_mean, q.l_inf]
+    print("config 1 quality (gpu, reference):", got_q, rq.tolist())
+    assert np.max(np.abs(np.array(got_q) - rq)) <= 1e-6
+
+
+# ------------------------------------------------------------------ (b)
+def _z(g, r):
+    z = []
+    for f, s in (("xi", "se_xi"), ("eta", "se_eta")):
+        se = np.hypot(g[s], r[s])
+        ok = se > 0
+        z.append((g[f][ok] - r[f][ok]) / se[ok])
+    return np.concatenate(z)
+
+
+def _subsample(n, k=16):
+    return np.linspace(0, n - 1, k).round().astype(int)
+
+
+def _nodes(m, nx, sx, placement, k):
+    spec = sdd.GridSpec(UNIT, nx, nx)
+    lay = sdd.build_layout(spec, sx, sx)
+    return spec, sdd.interface_nodes(m, lay, sdd.plan_interface_points(placement, k, m, lay))
+
+
+def test_performance_mode_against_reference_at_baseline_configs(ctx, refimpl, c1_reference):
+    zs, report = [], {}
+
+    def compare(name, m_an, spec, bd, ref_tabs, kind, pts, pid, dt, walks_gpu, walks_ref, precisions,
+                ref=None):
+        if ref is None:
+            ref = refimpl.mc_estimate_batch(B.density(kind), ODOM, ref_tabs,
+                                            B.walk_cfg(dt=dt, walks=walks_ref, seed=1),
+                                            pts[:, 0], pts[:, 1], pid, threads=0)
+        for prec in precisions:
+            g = sdd.mc_estimate_batch(pts, pid, m_an, UNIT, bd,
+                                      sdd.WalkConfig(scheme="linear", dt=dt, walks=walks_gpu, seed=2,
+                                                     precision=prec), ctx=ctx)
+            assert (g["edge_hits"].sum(axis=1) == walks_gpu).all()
+            z = _z(g, ref)
+            zs.append(z)
+            report[f"{name}_{prec}"] = (len(z), int(np.sum(np.abs(z) > 4)), float(np.mean(z ** 2)))
+
+    # config 1 in full: the reference estimates of (a), 1e4 paths both sides
+    m, spec, *_ , px, py, pid = _config1()
+    tabs, ref1 = c1_reference
+    compare("config1", sdd.MonitorFunction.ring(analytic=True), spec, sdd.make_boundary_data(m, spec), tabs,
+            B.RING_W, np.stack([px, py], 1), pid, 1e-4, 10_000, 10_000, ("fp64", "fp32"), ref=ref1)
+    # config 2: 129^2 4x4, all 753 nodes -> 16; GPU 1e5 paths, reference 2000
+    m2 = sdd.MonitorFunction.ring()
+    spec2, (px, py, pid) = _nodes(m2, 129, 4, "all", 0)
+    s = _subsample(len(px))
+    compare("config2", sdd.MonitorFunction.ring(analytic=True), spec2, sdd.make_boundary_data(m2, spec2),
+            refimpl.make_boundary(B.density(B.RING_W), ODOM, 129, 129), B.RING_W,
+            np.stack([px[s], py[s]], 1), pid[s], 2e-5, 100_000, 2000, ("fp64",))
+    # config 3: 1025^2 8x8 shock, 14,273 nodes -> 16; fp32 walks (and fp64)
+    m3 = sdd.MonitorFunction.shock()
+    spec3, (px, py, pid) = _nodes(m3, 1025, 8, "all", 0)
+    assert len(px) == 14273
+    s = _subsample(len(px))
+    compare("config3", sdd.MonitorFunction.shock(analytic=True), spec3, sdd.make_boundary_data(m3, spec3),
+            refimpl.make_boundary(B.density(B.SHOCK_W), ODOM, 1025, 1025), B.SHOCK_W,
+            np.stack([px[s], py[s]], 1), pid[s], 1e-5, 100_000, 1000, ("fp32", "fp64"))
+    # config 4: 513^2 4x4 two-bump, 32 integral-w-equidistributed nodes per line -> 16
+    m4 = sdd.MonitorFunction.two_bump()
+    spec4, (px, py, pid) = _nodes(m4, 513, 4, "equidistributed", 32)
+    s = _subsample(len(px))
+    compare("config4", sdd.MonitorFunction.two_bump(analytic=True), spec4, sdd.make_boundary_data(m4, spec4),
+            refimpl.make_boundary(B.density(B.TWOBUMP_W), ODOM, 513, 513), B.TWOBUMP_W,
+            np.stack([px[s], py[s]], 1), pid[s], 1e-5, 200_000, 1000, ("fp64",))
+    # config 5: 4096 uniform points (numpy seed 1), identity boundary data -> 16
+    pts5 = np.clip(np.random.default_rng(1).uniform(0.0, 1.0, size=(4096, 2)), 1e-9, 1 - 1e-9)
+    s = _subsample(4096)
+    spec5 = sdd.GridSpec(UNIT, 129, 129)
+    compare("config5", sdd.MonitorFunction.ring(analytic=True), spec5,
+            sdd.make_boundary_data(sdd.MonitorFunction.ring(), spec5, sdd.BC_IDENTITY),
+            B.Tables.identity(ODOM, 129, 129), B.RING_W, pts5[s], np.arange(4096, dtype=np.uint64)[s],
+            1e-5, 100_000, 1000, ("fp64", "fp32"))
+
+    z = np.concatenate(zs)
+    expected = len(z) * P_GT4
+    exceed = int(np.sum(np.abs(z) > 4))
+    chi2 = float(np.mean(z ** 2))
+    print(f"performance mode vs reference: {len(z)} z-values, |z|>4: {exceed} "
+          f"(null expectation {expected:.3f}), chi2/dof {chi2:.3f}; per config: {report}")
+    # P(>= 2 exceedances | H0) = 1 - e^-l (1 + l) ~ 1e-4 at l = expected ~ 0.03
+    assert exceed <= 1
+    sd = math.sqrt(2.0 / len(z))
+    assert abs(chi2 - 1.0) <= 5 * sd
+
+
+# ------------------------------------------------------------------ (c)
+def _config3_batch(refimpl):
+    g = 1025
+    w = refimpl.weight_values(B.density(B.SHOCK_W), ODOM, g, g)
+    subs, bcs = [], []
+    rng = np.random.default_rng(3)
+    for s in range(64):
+        a, b = s % 8, s // 8
+        for _ in range(2):
+            v0, v1, v2, v3 = np.sort(rng.random(4))
+            edge = lambda lo, hi: np.linspace(lo, hi, 129)  # noqa: E731
+            bcs.append(sdd.EdgeData(edge(v0, v1), edge(v2, v3), edge(v0, v2), edge(v1, v3)))
+            subs.append((a * 128, b * 128, 129, 129))
+    return g, w, subs, bcs
+
+
+def test_config3_sixteen_solves_against_reference_jacobi(ctx, refimpl):
+    g, w, subs, bcs = _config3_batch(refimpl)
+    res = sdd.solve_dirichlet_batch(w, g, g, 1 / 1024, 1 / 1024, subs, bcs,
+                                    sdd.SolverConfig(tol=1e-13, method="rbsor"), ctx=ctx)
+    assert all(r.converged for r in res)
+    picks = [int(k) for k in np.linspace(0, len(subs) - 1, 16).round()]
+
+    def ref_solve(k):
+        i0, j0, nx, ny = subs[k]
+        wl = w.reshape(g, g)[j0:j0 + ny, i0:i0 + nx].ravel()
+        return refimpl.solve_dirichlet(wl, nx, ny, 1 / 1024, 1 / 1024, *bcs[k].arrays(), tol=1e-13)[0]
+
+    with cf.ThreadPoolExecutor(max_workers=16) as ex:
+        refs = list(ex.map(ref_solve, picks))
+    err = max(float(np.max(np.abs(res[k].values - u))) for k, u in zip(picks, refs))
+    print(f"config 3: 16 of 128 RB-SOR solves vs reference Jacobi (tol 1e-13): max |du| {err:.2e}")
+    assert err <= 1e-10
+
+
+def test_rbsor_stops_within_tol_of_fixed_point_at_reference_default(ctx, refimpl):
+    # the SOR update norm is not monotone near the optimal factor;
+    # the stopping rule must not stop far from the fixed point.  At the
+    # reference's default tol 1e-8, every solve of a config-3 sample and of
+    # config 1's blocks must lie within 2 tol of the tight solution.
+    g, w, subs, bcs = _config3_batch(refimpl)
+    subs, bcs = subs[::8], bcs[::8]
+    for omega in (0.0, -1.0):
+        loose = sdd.solve_dirichlet_batch(w, g, g, 1 / 1024, 1 / 1024, subs, bcs,
+                                          sdd.SolverConfig(tol=1e-8, method="rbsor", omega=omega), ctx=ctx)
+        tight = sdd.solve_dirichlet_batch(w, g, g, 1 / 1024, 1 / 1024, subs, bcs,
+                                          sdd.SolverConfig(tol=1e-14, method="rbsor", omega=omega), ctx=ctx)
+        d = max(float(np.max(np.abs(a.values - b.values))) for a, b in zip(loose, tight))
+        print(f"omega mode {omega}: max distance at tol 1e-8: {d:.2e}")
+        assert d <= 2e-8
+    w1 = refimpl.weight_values(B.density(B.RING_W), ODOM, 65, 65)
+    x = np.linspace(0, 1, 33)
+    bc1 = [sdd.EdgeData(x, x, np.zeros(33), np.ones(33)), sdd.EdgeData(np.zeros(33), np.ones(33), x, x)]
+    subs1 = [(a * 32, b * 32, 33, 33) for a in range(2) for b in range(2)]
+    loose = sdd.solve_dirichlet_batch(w1, 65, 65, 1 / 64, 1 / 64, subs1 * 2, bc1 * 4,
+                                      sdd.SolverConfig(tol=1e-8, method="rbsor"), ctx=ctx)
+    tight = sdd.solve_dirichlet_batch(w1, 65, 65, 1 / 64, 1 / 64, subs1 * 2, bc1 * 4,
+                                      sdd.SolverConfig(tol=1e-14, method="rbsor"), ctx=ctx)
+    assert max(float(np.max(np.abs(a.values - b.values))) for a, b in zip(loose, tight)) <= 2e-8

@@ -78,6 +78,28 @@ def test_estimate_is_fixed_chunk_order_sum_of_paths(golden, ctx):
     assert e.stderr_xi == (var / 1000) ** 0.5
 
 
+def test_per_node_path_steps_with_restarts(ctx):
+    # sddg_estimate.path_steps: every executed step of the node's walks over
+    # all epochs (a restart after exactly max_steps steps, sde.cpp:154-182)
+    m = sdd.MonitorFunction.running_example()
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(UNIT, 17, 17))
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=600, seed=4, max_steps=300)
+    pts = [(0.5, 0.5), (0.2, 0.7), (0.9, 0.1)]
+    e = sdd.mc_estimate_batch(pts, [7, 8, 9], m, UNIT, bd, cfg, ctx=ctx)
+    assert e["restarts"].sum() > 0
+    assert int(e["path_steps"].sum()) == ctx.last_stats()["path_steps"]
+    for k, p in enumerate(pts):
+        d = sdd.walk_dump(p, 7 + k, m, UNIT, bd, cfg, 0, 600, ctx=ctx)
+        assert int(e["path_steps"][k]) == int(np.sum(d["steps"] + d["epoch"].astype(np.int64) * 300))
+
+
+def test_max_steps_bound_is_validated(ctx):
+    m = sdd.MonitorFunction.constant()
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(UNIT, 9, 9))
+    with pytest.raises(sdd.ValidationError, match="2\\^29"):
+        sdd.mc_estimate((0.5, 0.5), 0, m, UNIT, bd, sdd.WalkConfig(walks=4, max_steps=(1 << 29) + 1), ctx=ctx)
+
+
 def test_estimates_are_deterministic_and_batch_independent(ctx):
     m = sdd.MonitorFunction.ring()
     bd = sdd.make_boundary_data(m, sdd.GridSpec(UNIT, 65, 65))
@@ -323,6 +345,8 @@ def test_config2_subsample_parity_with_oracle(ctx, oracle):
     assert np.max(np.abs(g["xi"] - o["xi"])) <= EST_TOL
     assert np.max(np.abs(g["eta"] - o["eta"])) <= EST_TOL
     assert np.array_equal(g["edge_hits"], o["edge_hits"])
+    # per-node executed path-steps (K1's per-node counter) equal the oracle's
+    assert np.array_equal(g["path_steps"], o["path_steps"])
 
 
 def test_config3_scale_properties_fp32(ctx):
