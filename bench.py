@@ -23,9 +23,11 @@ config 2's solve_interfaces: all 753 nodes at the config's 10^5 paths per node
 
 --impl reference runs the reference CPU implementation alone (rank 0), each
 step a bounded sample of the workload, and prints the same metric.
-Multi-GPU (torchrun): weak scaling, every rank walks its own 753-node batch
-(seed offset by rank); no collective in the timed region except the timing
-max-reduction after it.
+Multi-GPU (torchrun, one process per GPU): strong scaling of the same
+workload through the library's multi-GPU context (sddg_create_dist): the 753
+nodes are sharded across the ranks by expected cost (sddg_shard_plan) and
+every step ends with the one ncclAllGather of the 128-B estimate records
+inside the timed region, so every rank holds all 753 estimates.
 """
 from __future__ import annotations
 
@@ -507,14 +509,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    backend = os.environ.get("SDDG_BENCH_BACKEND", "nccl")  # gloo: multi-rank path check on 1 GPU
+    cdev = "cuda"  # device of the timing collectives
     if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    cdev = "cuda" if backend == "nccl" else "cpu"  # device of the collective tensors
-    ctx = sdd.Context(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # the library's own communicator over the same ranks (sddg_create_dist)
+        nid = [sdd.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        ctx = sdd.Context.dist(local, rank, world, nid[0])
+        print(f"sddg team: {json.dumps(ctx.team_info())} on cuda:{local}", file=sys.stderr, flush=True)
+    elif os.environ.get("SDDG_BENCH_TEAM"):  # the multi-GPU code path over a one-rank communicator
+        ctx = sdd.Context.dist(local, 0, 1, sdd.nccl_unique_id())
+        print(f"sddg team: {json.dumps(ctx.team_info())} on cuda:{local}", file=sys.stderr, flush=True)
+    else:
+        ctx = sdd.Context(local)
     stream = torch.cuda.current_stream()
 
     m = sdd.MonitorFunction.ring(analytic=args.drift == "analytic")
@@ -530,8 +537,8 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
     def cfg_for(step):
-        return sdd.WalkConfig(scheme="linear", dt=DT, walks=args.walks,
-                              seed=1 + step + 1000 * rank, precision=args.precision)
+        return sdd.WalkConfig(scheme="linear", dt=DT, walks=args.walks, seed=1 + step,
+                              precision=args.precision)
 
     def one_step(step):
         sdd.mc_estimate_batch_device(d_px, d_py, d_pid, d_out, m, dom, bd, cfg_for(step), ctx=ctx,
@@ -566,15 +573,16 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([elapsed_ms, float(total_steps), k1_ms], dtype=torch.float64, device=cdev)
+    # path-steps: every rank holds all records after the all-gather, so
+    # total_steps already counts the whole job; time: max over ranks
+    all_steps = float(total_steps)
+    shard_k1 = None
     if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        elapsed_ms, all_steps = float(tmax[0]), float(tsum[1])
-    else:
-        all_steps = float(total_steps)
+        t = torch.tensor([elapsed_ms, k1_ms], dtype=torch.float64, device=cdev)
+        tall = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tall, t)
+        elapsed_ms = max(float(v[0]) for v in tall)
+        shard_k1 = [float(v[1]) / args.steps for v in tall]
     value = all_steps / (elapsed_ms / 1e3)
 
     # ---- e2e through the public host-buffer API (pinned inputs, D2H result)
@@ -594,13 +602,10 @@ def main():
                                   cfg_for(args.warmup + k), ctx=ctx)
             e_sec += time.perf_counter() - t0
             e_steps += ctx.last_stats()["path_steps"]
-        et = torch.tensor([e_sec, float(e_steps)], dtype=torch.float64, device=cdev)
         if world > 1:
-            emax = et.clone()
-            dist.all_reduce(emax, op=dist.ReduceOp.MAX)
-            esum = et.clone()
-            dist.all_reduce(esum, op=dist.ReduceOp.SUM)
-            e_sec, e_steps = float(emax[0]), float(esum[1])
+            et = torch.tensor([e_sec], dtype=torch.float64, device=cdev)
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e_sec = float(et[0])
         tables_bytes = 8 * 4 * (GRID + GRID)
         e2e = {"value": e_steps / e_sec, "unit": "path-steps/s",
                "h2d_bytes_per_step": int(n * 24 + tables_bytes),
@@ -608,9 +613,10 @@ def main():
                "api": "sdd.mc_estimate_batch -> sddg_mc_estimate_batch (host buffers)"}
 
     # ---- end-to-end mesh generation (T_stoc + T_sub, proj/src/cli.cpp:322):
-    # full BASELINE configs 1 and 2 through sdd.solve_sdd, once each
+    # full BASELINE configs 1 and 2 through sdd.solve_sdd, once each (every
+    # rank calls it: with several GPUs the nodes and subdomains are sharded)
     mesh = None
-    if rank == 0 and world == 1 and not args.no_mesh:
+    if not args.no_mesh:
         mesh = {}
         for name, grid, subs_, place, k, walks, dt in (("config1", 65, 2, "equispaced", 31, 10_000, 1e-4),
                                                        ("config2", 129, 4, "all", 0, 100_000, 2e-5)):
@@ -622,26 +628,30 @@ def main():
             mesh[name] = {"t_stoc_s": r.t_stoc, "t_sub_s": r.t_sub, "t_total_s": r.t_stoc + r.t_sub,
                           "mc_points": r.mc_points, "paths_per_node": walks,
                           "path_steps": r.path_steps, "subdomain_solves": r.subdomain_solves,
-                          "solver": "rbsor tol 1e-10"}
+                          "solver": "rbsor tol 1e-10", "gpus": world}
 
-    # ---- like-for-like with the reference arm: the same walk phase with the
-    # reference's own drift (user_supplied central difference of rho = 1/w,
-    # monitor.cpp:206-219; the bit-faithful parity mode), on a 1e4-path sample
+    # ---- like-for-like with the reference arm: the full config-2 walk phase
+    # (753 nodes x 1e5 paths) with the reference's own drift (user_supplied
+    # central difference of rho = 1/w, monitor.cpp:206-219; the bit-faithful
+    # parity mode, what a drop-in caller gets by default), end to end through
+    # the public host-buffer API, one launch after a short warm-up launch
     parity_mode = None
     if rank == 0 and world == 1 and not args.no_mesh and args.drift == "analytic":
         m_ref = sdd.MonitorFunction.ring(analytic=False)
-        # through the host API on the same nodes, best of two launches (the
-        # first also loads the parity-mode kernel's module)
-        cfg_ref = sdd.WalkConfig(scheme="linear", dt=DT, walks=10_000, seed=7, precision="fp64")
-        st = None
-        for _ in range(2):
-            sdd.mc_estimate_batch(np.stack([px, py], axis=1), pid, m_ref, dom, bd, cfg_ref, ctx=ctx)
-            s_ = ctx.last_stats()
-            if st is None or s_["kernel_ms"] < st["kernel_ms"]:
-                st = s_
-        parity_mode = {"value": st["path_steps"] / (st["kernel_ms"] / 1e3), "unit": "path-steps/s",
-                       "paths_per_node": 10_000, "drift": "reference (user_supplied FD of 1/w, h = 1e-6)",
-                       "note": "same config-2 walk phase as `value`, bit-faithful parity mode, K1 time"}
+        pts2 = np.stack([px, py], axis=1)
+        sdd.mc_estimate_batch(pts2, pid, m_ref, dom, bd,
+                              sdd.WalkConfig(scheme="linear", dt=DT, walks=100, seed=6), ctx=ctx)
+        cfg_ref = sdd.WalkConfig(scheme="linear", dt=DT, walks=CONFIG_WALKS, seed=7, precision="fp64")
+        t0 = time.perf_counter()
+        sdd.mc_estimate_batch(pts2, pid, m_ref, dom, bd, cfg_ref, ctx=ctx)
+        wall = time.perf_counter() - t0
+        st = ctx.last_stats()
+        parity_mode = {"e2e": st["path_steps"] / wall, "value": st["path_steps"] / (st["kernel_ms"] / 1e3),
+                       "unit": "path-steps/s", "paths_per_node": CONFIG_WALKS, "nodes": n,
+                       "path_steps": st["path_steps"], "wall_s": wall,
+                       "drift": "reference (user_supplied FD of 1/w, h = 1e-6)",
+                       "note": "the full config-2 walk phase in the bit-faithful parity mode: e2e = "
+                               "host-buffer API wall clock, value = walk-kernel event time"}
 
     # ---- subdomain solver (K3/K3c), measured live: BASELINE config 3's batch
     # (128 x 129^2, shock weights, RB-SOR to 1e-10; one thread-block cluster per
@@ -677,16 +687,20 @@ def main():
         line = {
             "metric": "SDE walk path-steps/s", "value": value, "unit": "path-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic",
             "config": {"workload": "BASELINE config 2 walk phase (one step = the full config): 129^2 "
                                    "grid, 4x4 subdomains, all 753 interface nodes x 1e5 paths, ring "
                                    "density (analytic grad w / w), linear EM dt=2e-5 + bridge exit test",
                        "paths_per_node_per_step": args.walks, "config_paths_per_node": CONFIG_WALKS,
-                       "nodes_per_rank": n, "drift": args.drift, "precision": args.precision,
+                       "nodes": n, "drift": args.drift, "precision": args.precision,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": f"weak x{world} (independent node batches per rank)"},
+                       "parallelism": (f"dp{world}: the 753 nodes sharded over {world} GPUs by expected "
+                                       "cost (sddg_shard_plan), one ncclAllGather of the 128-B records "
+                                       "per step inside the timed region (sddg_create_dist)")
+                       if world > 1 else "single GPU"},
             "roofline": {"bound": "fp64" if args.precision == "fp64" else "fp32",
                          "achieved": achieved, "peak": prec_peak, "unit": "TFLOP/s",
                          "frac": achieved / prec_peak if prec_peak else None,
@@ -713,7 +727,8 @@ def main():
             "mesh_gen_seconds": mesh,
             "solver": solver,
             "parity_mode_walks": parity_mode,
-            "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value * world,
+            "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value,
+            "shard_k1_ms": shard_k1,
         }
         print(json.dumps(line))
     if world > 1:

@@ -177,6 +177,43 @@ sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* den
                                           const double* d_py, const uint64_t* d_point_id,
                                           int64_t n, sddg_estimate* d_out, void* stream);
 
+/* ------------------------------------------------------ several GPUs
+ * The reference parallelises solve_interfaces over interface nodes and
+ * solve_sdd over subdomains with std::thread (proj/src/decomposition.cpp:
+ * 171-174, 298-355).  A context may span several GPUs: every walk entry
+ * point (sddg_mc_estimate_batch[_device], sddg_solve_interfaces,
+ * sddg_solve_sdd, sddg_stochastic_full) then shards the nodes across the
+ * ranks by expected cost (sddg_shard_plan), walks each shard on its GPU and
+ * joins the 128-B records with ONE ncclAllGather; sddg_solve_sdd also splits
+ * the subdomains into contiguous per-rank ranges and all-gathers the fields.
+ * Every rank returns the complete result, bit-identical to a one-GPU
+ * context (each node is reduced on one rank in the reference's chunk
+ * order).  With one process per GPU every rank makes the same calls with the
+ * same arguments (SPMD). */
+typedef struct {
+    unsigned char bytes[128]; /* ncclUniqueId */
+} sddg_nccl_id;
+/* Rank 0 creates the id and passes it to the other processes. */
+sddg_status sddg_nccl_unique_id(sddg_nccl_id* id);
+/* One process per GPU: this process is `rank` of `nranks` (ncclCommInitRank,
+ * collective over all ranks).  nranks = 1 still runs the NCCL exchange. */
+sddg_status sddg_create_dist(int32_t device, int32_t rank, int32_t nranks, const sddg_nccl_id* id,
+                             sddg_ctx** out);
+/* One process for n GPUs (ncclCommInitAll, one host thread per device).  A
+ * device listed twice runs as separate ranks exchanging by device copies. */
+sddg_status sddg_create_multi(int32_t n, const int32_t* devices, sddg_ctx** out);
+/* This context's first global rank, the rank count, the GPUs this process
+ * drives, and whether the exchange is NCCL (1) or a device copy (0). */
+sddg_status sddg_team_info(const sddg_ctx* ctx, int32_t* rank, int32_t* nranks,
+                           int32_t* local_devices, int32_t* nccl);
+/* Host: the node shard plan the sharded calls use.  cost[k] = expected
+ * path-steps of node k's cfg->walks walks from the exit-time model (the
+ * expected first-exit time T of the walk, div(w grad T) = -w, T = 0 on the
+ * edges, over dt); rank_of[k] from longest-processing-time assignment. */
+sddg_status sddg_shard_plan(const sddg_density* dens, const sddg_domain* dom,
+                            const sddg_walk_config* cfg, const double* px, const double* py,
+                            int64_t n, int32_t nranks, int32_t* rank_of, double* cost);
+
 /* ------------------------------------------------ fused multi-GPU gather
  * The one collective of the sharded path (an all-gather of the per-node
  * records) fused into the finalize kernel K2: each rank opens every other

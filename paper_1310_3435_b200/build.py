@@ -38,6 +38,7 @@ UNITS = {
     "smooth.cu": ["-fmad=false"],
     "probe.cu": [],
     "runtime.cu": [],
+    "team.cu": [],
 }
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))
 
@@ -73,7 +74,7 @@ def build(verbose=False, force=False):
         results = list(ex.map(lambda kv: _compile(kv[0], kv[1], verbose), UNITS.items()))
     objs = [o for o, _ in results]
     if any(changed for _, changed in results) or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{r.stderr}")

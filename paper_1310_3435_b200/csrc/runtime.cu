@@ -26,53 +26,13 @@
 
 #include "fastmath.cuh"
 #include "host_density.h"
+#include "runtime_internal.h"
 #include "sddg_internal.h"
 
 using namespace sddg;
+using namespace sddg::rt;
 
 namespace {
-
-struct Fail {
-    sddg_status st;
-    std::string msg;
-};
-
-[[noreturn]] void fail(sddg_status st, const std::string& m) { throw Fail{st, m}; }
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) fail(SDDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-double now_s() {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
-        .count();
-}
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t cap = 0;
-    void* ensure(size_t bytes) {
-        if (bytes <= cap) return p;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        const size_t want = std::max<size_t>(bytes, 256);
-        ck(cudaMalloc(&p, want), "cudaMalloc");
-        cap = want;
-        return p;
-    }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-    }
-};
-
-struct Counters {
-    unsigned long long next, steps, err_info;
-    int err_flag;
-    int pad;
-};
 
 __global__ void set_next_kernel(Counters* c, unsigned long long v) { c->next = v; }
 
@@ -80,25 +40,8 @@ thread_local std::string g_free_err;
 
 }  // namespace
 
-struct sddg_ctx {
-    int device = 0;
-    int sms = 0;
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    std::string err;
-    std::mutex mu;
-    DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm, nsteps;
-    DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large, s_omega, s_perm;
-    DevBuf m_in, m_out, m_q, m_misc;
-    int64_t last_steps = 0, last_launches = 0;
-    double last_ms = 0.0;
-    std::map<int, std::pair<int, int>> occ;  // (dv*2+prec) -> (CTAs per SM, threads per CTA)
-    std::vector<cudaEvent_t> bev;  // per-batch walk-kernel events
-    DevBuf fm_tables;              // fastmath.cuh FmTables (performance mode)
-    DevBuf gidx;                   // fused-gather global indices
-};
-
-namespace {
+namespace sddg {
+namespace rt {
 
 // ------------------------------------------------------------ validation
 
@@ -263,20 +206,93 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     a.max_steps32 = static_cast<uint32_t>(cfg.max_steps);  // <= 2^29 (validate_walk)
 }
 
-// Longest-expected-walk-first node order (LPT): a first-exit walk from p
-// takes time ~ the product of its distances to opposite edges, so sort by
-// that descending; the batch tail is then made of short walks.
-std::vector<uint32_t> lpt_order(const sddg_domain& dom, const double* px, const double* py,
-                                int64_t n) {
-    std::vector<uint32_t> perm(n);
-    std::vector<double> key(n);
-    for (int64_t k = 0; k < n; ++k) {
-        perm[k] = static_cast<uint32_t>(k);
-        const double kx = (px[k] - dom.xmin) * (dom.xmax - px[k]);
-        const double ky = (py[k] - dom.ymin) * (dom.ymax - py[k]);
-        key[k] = kx * ky / (kx + ky);
+// ------------------------------------------------------------ cost model
+
+double ExitTimeModel::at(double x, double y) const {
+    double sx = (x - x0) / hx, sy = (y - y0) / hy;
+    sx = std::min(std::max(sx, 0.0), static_cast<double>(g - 1));
+    sy = std::min(std::max(sy, 0.0), static_cast<double>(g - 1));
+    const int i = std::min(static_cast<int>(sx), g - 2), j = std::min(static_cast<int>(sy), g - 2);
+    const double u = sx - i, v = sy - j;
+    const double* r0 = t.data() + static_cast<size_t>(j) * g + i;
+    const double* r1 = r0 + g;
+    return (1 - v) * ((1 - u) * r0[0] + u * r0[1]) + v * ((1 - u) * r1[0] + u * r1[1]);
+}
+
+// div(w grad T) = -w on a 65 x 65 grid over the domain, T = 0 on the edges:
+// the conservative five-point operator of solve_dirichlet (detsolver.cpp:88-111)
+// with a source, red-black SOR at the grid's optimal factor until the update
+// is below 1e-7 of max T (a few ms of host time, once per density/domain).
+const ExitTimeModel& exit_time_model(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom) {
+    char key[256];
+    std::snprintf(key, sizeof(key), "%d %a %a %a %a %a %a", d.kind, d.R, d.alpha, dom.xmin, dom.xmax,
+                  dom.ymin, dom.ymax);
+    auto it = c->cost_models.find(key);
+    if (it != c->cost_models.end()) return it->second;
+    ExitTimeModel m;
+    const int g = 65;
+    m.g = g;
+    m.x0 = dom.xmin;
+    m.y0 = dom.ymin;
+    m.hx = (dom.xmax - dom.xmin) / (g - 1);
+    m.hy = (dom.ymax - dom.ymin) / (g - 1);
+    const HostDensity h = host_density(d);
+    std::vector<double> w(static_cast<size_t>(g) * g);
+    for (int j = 0; j < g; ++j)
+        for (int i = 0; i < g; ++i) {
+            double r = 1.0;
+            try {
+                r = h.rho(m.x0 + i * m.hx, m.y0 + j * m.hy);
+            } catch (const std::exception&) {
+            }
+            w[static_cast<size_t>(j) * g + i] = (std::isfinite(r) && r > 0.0) ? 1.0 / r : 1.0;
+        }
+    const double ihx2 = 1.0 / (m.hx * m.hx), ihy2 = 1.0 / (m.hy * m.hy);
+    m.t.assign(static_cast<size_t>(g) * g, 0.0);
+    const double omega = 2.0 / (1.0 + std::sin(3.14159265358979323846 / (g - 1)));
+    for (int sweep = 0; sweep < 4000; ++sweep) {
+        double upd = 0.0, tmax = 0.0;
+        for (int colour = 0; colour < 2; ++colour)
+            for (int j = 1; j < g - 1; ++j)
+                for (int i = 1 + ((j + colour) & 1); i < g - 1; i += 2) {
+                    const size_t k = static_cast<size_t>(j) * g + i;
+                    const double ce = 0.5 * (w[k] + w[k + 1]) * ihx2, cw = 0.5 * (w[k] + w[k - 1]) * ihx2;
+                    const double cn = 0.5 * (w[k] + w[k + g]) * ihy2, cs = 0.5 * (w[k] + w[k - g]) * ihy2;
+                    const double gs = (ce * m.t[k + 1] + cw * m.t[k - 1] + cn * m.t[k + g] + cs * m.t[k - g] +
+                                       w[k]) / (ce + cw + cn + cs);
+                    const double nv = m.t[k] + omega * (gs - m.t[k]);
+                    upd = std::max(upd, std::fabs(nv - m.t[k]));
+                    tmax = std::max(tmax, nv);
+                    m.t[k] = nv;
+                }
+        if (upd <= 1e-7 * tmax) break;
     }
-    std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return key[a] > key[b]; });
+    return c->cost_models.emplace(key, std::move(m)).first->second;
+}
+
+std::vector<double> node_costs(const ExitTimeModel& m, const sddg_walk_config& cfg, const double* px,
+                               const double* py, int64_t n) {
+    // mean step: dt (linear) or 1/lambda (exponential, dt ~ Exp(lambda))
+    const double per = cfg.scheme == SDDG_SCHEME_LINEAR ? 1.0 / cfg.dt : cfg.lambda;
+    const double walks = static_cast<double>(cfg.walks);
+    std::vector<double> out(n);
+    for (int64_t k = 0; k < n; ++k) out[k] = walks * (1.0 + std::max(0.0, m.at(px[k], py[k])) * per);
+    return out;
+}
+
+// Longest-expected-walk-first launch order (LPT): the batch tail is then made
+// of short walks.
+std::vector<uint32_t> cost_order(const std::vector<double>& cost, const std::vector<uint32_t>* subset) {
+    std::vector<uint32_t> perm;
+    if (subset) {
+        perm = *subset;
+    } else {
+        perm.resize(cost.size());
+        for (size_t k = 0; k < cost.size(); ++k) perm[k] = static_cast<uint32_t>(k);
+    }
+    std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+        return cost[a] > cost[b] || (cost[a] == cost[b] && a < b);
+    });
     return perm;
 }
 
@@ -313,23 +329,27 @@ void raise_kernel_error(const Counters& hc) {
 // Walks + finalize for n device-resident nodes; estimates to d_out.
 void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
                    const sddg_boundary& bd, const sddg_walk_config& cfg, const double* d_px,
-                   const double* d_py, const uint64_t* d_pid, int64_t n, sddg_estimate* d_out,
-                   cudaStream_t st, const double* hpx, const double* hpy,
-                   const GatherTargets* gt = nullptr) {
+                   const double* d_py, const uint64_t* d_pid, int64_t n_all,
+                   const std::vector<uint32_t>& perm, sddg_estimate* d_out, cudaStream_t st,
+                   const GatherTargets* gt) {
     GatherTargets none;
     none.n_peers = 0;
     none.global_index = nullptr;
     const int dv = drift_variant(d, cfg.precision);
+    const int64_t n = static_cast<int64_t>(perm.size());
+    c->last_ms = 0.0;
+    c->last_steps = 0;
+    c->last_launches = 0;
+    if (n == 0) return;
     const double* dtab = upload_tables(c, bd);
-    const std::vector<uint32_t> perm = lpt_order(dom, hpx, hpy, n);
     uint32_t* dperm = static_cast<uint32_t*>(c->perm.ensure(sizeof(uint32_t) * n));
     ck(cudaMemcpyAsync(dperm, perm.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st),
        "h2d perm");
     Counters* cnt = static_cast<Counters*>(c->counters.ensure(sizeof(Counters)));
     ck(cudaMemsetAsync(cnt, 0, sizeof(Counters), st), "memset counters");
     unsigned long long* nst =
-        static_cast<unsigned long long*>(c->nsteps.ensure(sizeof(unsigned long long) * n));
-    ck(cudaMemsetAsync(nst, 0, sizeof(unsigned long long) * n, st), "memset node steps");
+        static_cast<unsigned long long*>(c->nsteps.ensure(sizeof(unsigned long long) * n_all));
+    ck(cudaMemsetAsync(nst, 0, sizeof(unsigned long long) * n_all, st), "memset node steps");
     const int64_t W = cfg.walks;
     const int64_t npb = std::max<int64_t>(1, batch_budget_walks() / W);
     const int64_t cap = std::min(npb, n) * W;
@@ -413,7 +433,13 @@ void estimates_host(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     ck(cudaMemcpyAsync(dpy, py, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
     ck(cudaMemcpyAsync(dpid, pid, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, c->stream), "h2d");
     sddg_estimate* dout = static_cast<sddg_estimate*>(c->est.ensure(sizeof(sddg_estimate) * n));
-    run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream, px, py, gt);
+    if (team_active(c) && !gt) {
+        team_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, dout, c->stream, px, py);
+    } else {
+        const std::vector<uint32_t> order =
+            cost_order(node_costs(exit_time_model(c, d, dom), cfg, px, py, n), nullptr);
+        run_estimates(c, d, dom, bd, cfg, dpx, dpy, dpid, n, order, dout, c->stream, gt);
+    }
     ck(cudaMemcpyAsync(out, dout, sizeof(sddg_estimate) * n, cudaMemcpyDeviceToHost, c->stream),
        "d2h");
     ck(cudaStreamSynchronize(c->stream), "d2h sync");
@@ -997,8 +1023,12 @@ void solve_subdomains(sddg_ctx* c, const sddg_density& d, const Layout& L,
     const int64_t nj = static_cast<int64_t>(subs.size());
     u.assign(static_cast<size_t>(nj) * (L.bx + 1) * (L.by + 1), 0.0);
     info.assign(nj, sddg_solve_info{});
-    solve_batch_host(c, w.data(), nx, ny, L.hx(), L.hy(), nj, subs.data(), bc.data(), sc, u.data(),
-                     info.data());
+    if (team_active(c))
+        team_solve_batch(c, w.data(), nx, ny, L.hx(), L.hy(), nj, 2, subs.data(), bc.data(), sc, u.data(),
+                         info.data());
+    else
+        solve_batch_host(c, w.data(), nx, ny, L.hx(), L.hy(), nj, subs.data(), bc.data(), sc, u.data(),
+                         info.data());
 }
 
 // smooth_interface on the GPU (K7, smoothing.cpp:140-183)
@@ -1077,7 +1107,10 @@ sddg_status finish(sddg_ctx* c, const Fail& f) {
     (ctx)->err.clear();                                  \
     return SDDG_OK;
 
-}  // namespace
+void set_free_error(const std::string& m) { g_free_err = m; }
+
+}  // namespace rt
+}  // namespace sddg
 
 namespace sddg {
 
@@ -1212,9 +1245,10 @@ sddg_status sddg_create(int32_t device, sddg_ctx** out) {
 
 void sddg_destroy(sddg_ctx* c) {
     if (!c) return;
+    team_destroy(c);
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->t_recv, &c->t_nodes, &c->t_pts, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->s_perm, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
@@ -1276,8 +1310,14 @@ sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* den
         ck(cudaMemcpyAsync(hy.data(), d_py, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "d2h");
         ck(cudaStreamSynchronize(st), "sync");
         check_points(*dom, hx.data(), hy.data(), n);
-        run_estimates(ctx, *dens, *dom, *bd, *cfg, d_px, d_py, d_pid, n, d_out, st, hx.data(),
-                      hy.data());
+        if (team_active(ctx)) {
+            team_estimates(ctx, *dens, *dom, *bd, *cfg, d_px, d_py, d_pid, n, d_out, st, hx.data(),
+                           hy.data());
+        } else {
+            const std::vector<uint32_t> order = cost_order(
+                node_costs(exit_time_model(ctx, *dens, *dom), *cfg, hx.data(), hy.data(), n), nullptr);
+            run_estimates(ctx, *dens, *dom, *bd, *cfg, d_px, d_py, d_pid, n, order, d_out, st);
+        }
     }
     API_END(ctx)
 }

@@ -26,17 +26,18 @@ import torch.distributed as dist
 from . import sdd
 
 
-def expected_cost(px, py, domain: sdd.RectDomain):
-    """Relative first-exit time of a walk from (px, py): the product of the
-    distances to opposite edges, combined harmonically (the LPT key of
-    runtime.cu).  Only the ordering matters."""
-    kx = (px - domain.xmin) * (domain.xmax - px)
-    ky = (py - domain.ymin) * (domain.ymax - py)
-    return kx * ky / np.maximum(kx + ky, 1e-300)
+def node_shards(px, py, m: sdd.MonitorFunction, domain: sdd.RectDomain, cfg: sdd.WalkConfig, world: int):
+    """The node shards of the C-ABI's multi-GPU contexts (sddg_shard_plan:
+    expected path-steps from the walk's exit-time model, LPT over ranks), so
+    this torch.distributed driver and sddg_create_dist shard identically.
+    Returns a list of sorted index arrays, one per rank."""
+    rank_of, _ = sdd.shard_plan(np.stack([px, py], 1), m, domain, cfg, world)
+    return [np.nonzero(rank_of == r)[0] for r in range(world)]
 
 
 def shard(costs, world: int):
-    """Greedy LPT assignment of items to `world` ranks; deterministic.
+    """Greedy LPT assignment of items to `world` ranks (the rule of
+    sddg_shard_plan); deterministic.
     Returns a list of sorted index arrays, one per rank."""
     costs = np.asarray(costs, dtype=np.float64)
     order = np.argsort(-costs, kind="stable")
@@ -113,7 +114,7 @@ def solve_interfaces_distributed(plan, m, bd, cfg, layout, estimator=None, ctx=N
     NCCL all-gather (needs the default estimator)."""
     rank, world = dist.get_rank(), dist.get_world_size()
     px, py, pid = sdd.interface_nodes(m, layout, plan)
-    mine = shard(expected_cost(px, py, layout.global_.domain), world)[rank]
+    mine = node_shards(px, py, m, layout.global_.domain, cfg, world)[rank]
     if transport == "peer":
         if estimator is not None:
             raise sdd.ValidationError("transport='peer' runs the walks itself; no estimator")

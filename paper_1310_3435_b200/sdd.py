@@ -153,13 +153,51 @@ def _f64(a):
 
 
 # --------------------------------------------------------------- context
-class Context:
-    """One device, its stream and buffers (sddg_create / sddg_destroy)."""
+class NcclId(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 128)]
 
-    def __init__(self, device=0):
+
+def nccl_unique_id() -> bytes:
+    """sddg_nccl_unique_id: rank 0 creates it and hands it to the other ranks."""
+    i = NcclId()
+    _check(lib().sddg_nccl_unique_id(C.byref(i)))
+    return bytes(i.bytes)
+
+
+class Context:
+    """One device, its stream and buffers (sddg_create / sddg_destroy); or
+    several GPUs (Context.dist: one process per GPU over NCCL;
+    Context.multi: one process driving several devices)."""
+
+    def __init__(self, device=0, _handle=None):
         self._h = C.c_void_p()
-        _check(lib().sddg_create(int(device), C.byref(self._h)))
+        if _handle is None:
+            _check(lib().sddg_create(int(device), C.byref(self._h)))
+        else:
+            self._h = _handle
         self.device = device
+
+    @staticmethod
+    def dist(device: int, rank: int, nranks: int, nccl_id: bytes) -> "Context":
+        """sddg_create_dist: this process is `rank` of `nranks` (collective)."""
+        h = C.c_void_p()
+        i = NcclId()
+        C.memmove(i.bytes, nccl_id, 128)
+        _check(lib().sddg_create_dist(int(device), int(rank), int(nranks), C.byref(i), C.byref(h)))
+        return Context(device, _handle=h)
+
+    @staticmethod
+    def multi(devices) -> "Context":
+        """sddg_create_multi: one process drives every device in `devices`."""
+        devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        h = C.c_void_p()
+        _check(lib().sddg_create_multi(len(devices), devs, C.byref(h)))
+        return Context(int(devices[0]), _handle=h)
+
+    def team_info(self):
+        r, n, loc, nc = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().sddg_team_info(self._h, C.byref(r), C.byref(n), C.byref(loc), C.byref(nc)), self._h)
+        return {"rank": r.value, "nranks": n.value, "local_devices": loc.value, "nccl": bool(nc.value)}
 
     @property
     def handle(self):
@@ -742,6 +780,20 @@ def interface_nodes(m: MonitorFunction, layout: SubdomainLayout, plan: Interface
                                       pid.ctypes.data_as(C.c_void_p), C.byref(n)))
     k = n.value
     return px[:k].copy(), py[:k].copy(), pid[:k].copy()
+
+
+def shard_plan(points, m: MonitorFunction, domain: RectDomain, cfg: WalkConfig, nranks: int):
+    """sddg_shard_plan (host): (rank of each node, expected path-steps of each
+    node's cfg.walks walks) -- the node shards of a multi-GPU context."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
+    px, py = _f64(pts[:, 0]), _f64(pts[:, 1])
+    rank = np.zeros(len(px), np.int32)
+    cost = np.zeros(len(px))
+    d, dom, c = m.c(), domain.c(), cfg.c()
+    _check(lib().sddg_shard_plan(C.byref(d), C.byref(dom), C.byref(c), _dp(px), _dp(py),
+                                 C.c_int64(len(px)), int(nranks), rank.ctypes.data_as(C.c_void_p),
+                                 _dp(cost)))
+    return rank, cost
 
 
 def fill_interfaces(m: MonitorFunction, layout: SubdomainLayout, plan: InterfacePlan,

@@ -18,6 +18,8 @@ from cases import plan_from_flat
 from oracle import bindings as B
 from paper_1310_3435_b200 import sdd
 
+UNIT = sdd.RectDomain(0, 1, 0, 1)
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -162,3 +164,40 @@ def test_plain_c_caller_builds_links_and_fails_loudly_without_a_gpu():
         pass
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 1 and "status 6" in r.stderr
+
+
+def test_shard_plan_exit_time_model_known_answer():
+    # the cost model behind the multi-GPU node shards: expected first-exit
+    # time T of dX = grad(w)/w dt + sqrt(2) dW, div(w grad T) = -w, T = 0 on
+    # the edges.  Constant w on the unit square: T solves Laplace(T) = -1,
+    # whose centre value is the square's torsion constant 0.0736713...
+    m = sdd.MonitorFunction.constant()
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=10)
+    rank, cost = sdd.shard_plan([(0.5, 0.5), (0.25, 0.5), (0.05, 0.05)], m, UNIT, cfg, 2)
+    t_centre = (cost[0] / 10 - 1) * 1e-4
+    assert abs(t_centre - 0.0736713) < 2e-4
+    assert cost[0] > cost[1] > cost[2]
+    assert rank.tolist() == [0, 1, 1]          # LPT: the largest alone, the rest on the other rank
+    # exponential scheme: mean step 1/lambda
+    _, ce = sdd.shard_plan([(0.5, 0.5)], m, UNIT, sdd.WalkConfig(scheme="exponential", lambda_=1000.0,
+                                                                  walks=1), 1)
+    assert abs((ce[0] - 1) / 1000 - t_centre) < 1e-9
+
+
+def test_shard_plan_tracks_the_density():
+    # a strong monitor (shock layer, w up to 21) slows walks down where w is
+    # large only through the drift; the plan must be deterministic, cover
+    # every node once and be balanced
+    m = sdd.MonitorFunction.shock()
+    rng = np.random.default_rng(2)
+    pts = rng.uniform(0.02, 0.98, (3000, 2))
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-5, walks=1000)
+    r1, c1 = sdd.shard_plan(pts, m, UNIT, cfg, 8)
+    r2, c2 = sdd.shard_plan(pts, m, UNIT, cfg, 8)
+    assert np.array_equal(r1, r2) and np.array_equal(c1, c2)
+    loads = np.array([c1[r1 == r].sum() for r in range(8)])
+    assert loads.max() / loads.min() < 1.001
+    with pytest.raises(sdd.OutOfDomainError):
+        sdd.shard_plan([(0.0, 0.5)], m, UNIT, cfg, 2)
+    with pytest.raises(sdd.ValidationError):
+        sdd.shard_plan(pts, m, UNIT, cfg, 0)

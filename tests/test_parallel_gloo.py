@@ -119,7 +119,13 @@ def test_config3_node_count_and_cost_order():
     plan = sdd.plan_interface_points("all", 0, m, lay)
     px, py, pid = sdd.interface_nodes(m, lay, plan)
     assert len(px) == 14273 and len(np.unique(pid)) == 14273
-    c = parallel.expected_cost(px, py, UNIT)
-    parts = parallel.shard(c, 8)
-    loads = [c[p].sum() for p in parts]
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-5, walks=1_000_000, seed=1, precision="fp32")
+    rank, cost = sdd.shard_plan(np.stack([px, py], 1), m, UNIT, cfg, 8)
+    loads = [cost[rank == r].sum() for r in range(8)]
     assert max(loads) / min(loads) < 1.001
+    # the torch.distributed driver shards exactly like the C-ABI plan
+    parts = parallel.node_shards(px, py, m, UNIT, cfg, 8)
+    assert all(np.array_equal(parts[r], np.nonzero(rank == r)[0]) for r in range(8))
+    # and the rule is parallel.shard's LPT
+    ref = parallel.shard(cost, 8)
+    assert all(np.array_equal(parts[r], ref[r]) for r in range(8))
