@@ -74,7 +74,7 @@ def build(verbose=False, force=False):
         results = list(ex.map(lambda kv: _compile(kv[0], kv[1], verbose), UNITS.items()))
     objs = [o for o, _ in results]
     if any(changed for _, changed in results) or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lnccl"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc link failed:\n{r.stderr}")

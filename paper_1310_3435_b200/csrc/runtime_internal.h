@@ -3,7 +3,7 @@
 // (several devices: node and subdomain sharding, NCCL all-gathers).
 #pragma once
 #include <cuda_runtime.h>
-#include <nccl.h>
+#include <nccl.h>  // types only: the library is loaded at run time (team.cu)
 
 #include <algorithm>
 #include <chrono>
@@ -29,10 +29,6 @@ struct Fail {
 
 inline void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(SDDG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-inline void nck(ncclResult_t r, const char* what) {
-    if (r != ncclSuccess) fail(SDDG_ERR_CUDA, std::string(what) + ": " + ncclGetErrorString(r));
 }
 
 inline double now_s() {

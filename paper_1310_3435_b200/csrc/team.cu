@@ -20,9 +20,12 @@
 // independent ranks whose exchange is a device copy (no NCCL): the sharded
 // path on a single GPU, for tests.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstddef>
+#include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <exception>
 #include <numeric>
@@ -35,6 +38,59 @@ using namespace sddg;
 using namespace sddg::rt;
 
 namespace {
+
+// NCCL is loaded at run time, the first time a multi-GPU context is made,
+// and never linked: a process that already holds a libnccl.so.2 (PyTorch
+// loads its bundled one) must keep using that copy, because a second copy
+// of the same soname loaded first would shadow the one PyTorch needs.
+// Order: an already-loaded libnccl.so.2; SDDG_NCCL_PATH (the Python mirror
+// points it at PyTorch's bundled library); the system libnccl.so.2.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string error;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        const char* env = std::getenv("SDDG_NCCL_PATH");
+        if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return;
+        }
+        auto sym = [&](const char* n) {
+            void* p = dlsym(h, n);
+            if (!p && api.error.empty()) api.error = std::string("libnccl.so.2 lacks ") + n;
+            return p;
+        };
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+        api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+        api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    });
+    if (!api.error.empty()) fail(SDDG_ERR_CUDA, api.error);
+    return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        fail(SDDG_ERR_CUDA, std::string(what) + ": " + nccl().GetErrorString(r));
+}
 
 __global__ void pack_kernel(const sddg_estimate* __restrict__ in, const int* __restrict__ nodes, int count,
                             sddg_estimate* __restrict__ out) {
@@ -164,13 +220,13 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     });
     // 2. the one collective: every rank's records to every rank
     if (!T.comms.empty()) {
-        nck(ncclGroupStart(), "ncclGroupStart");
+        nck(nccl().GroupStart(), "ncclGroupStart");
         for (int m = 0; m < nm; ++m) {
             const int r = T.rank0 + m;
-            nck(ncclAllGather(recv[m] + r * maxc, recv[m], rec * maxc, ncclUint8, T.comms[m], streams[m]),
+            nck(nccl().AllGather(recv[m] + r * maxc, recv[m], rec * maxc, ncclUint8, T.comms[m], streams[m]),
                 "ncclAllGather");
         }
-        nck(ncclGroupEnd(), "ncclGroupEnd");
+        nck(nccl().GroupEnd(), "ncclGroupEnd");
     } else {  // all ranks local (duplicate devices): copy into the owner's buffer
         for (int m = 0; m < nm; ++m) ck(cudaStreamSynchronize(streams[m]), "member sync");
         for (int m = 1; m < nm; ++m) {
@@ -233,7 +289,7 @@ void team_solve_batch(sddg_ctx* c, const double* w, int gnx, int gny, double hx,
     ck(cudaMemcpyAsync(dbuf + r * slot + sizeof(double) * max_u, info + lo[r],
                        sizeof(sddg_solve_info) * (lo[r + 1] - lo[r]), cudaMemcpyHostToDevice, c->stream),
        "h2d info");
-    nck(ncclAllGather(dbuf + r * slot, dbuf, slot, ncclUint8, T.comms[0], c->stream), "ncclAllGather fields");
+    nck(nccl().AllGather(dbuf + r * slot, dbuf, slot, ncclUint8, T.comms[0], c->stream), "ncclAllGather fields");
     std::vector<char> h(slot * R);
     ck(cudaMemcpyAsync(h.data(), dbuf, slot * R, cudaMemcpyDeviceToHost, c->stream), "d2h fields");
     ck(cudaStreamSynchronize(c->stream), "fields gather");
@@ -252,7 +308,7 @@ void team_destroy(sddg_ctx* c) {
     c->team = nullptr;
     for (size_t m = 0; m < T->comms.size(); ++m) {
         cudaSetDevice(T->members[m]->device);
-        ncclCommDestroy(T->comms[m]);
+        nccl().CommDestroy(T->comms[m]);
     }
     for (size_t m = 1; m < T->members.size(); ++m) sddg_destroy(T->members[m]);
     delete T;
@@ -274,7 +330,7 @@ sddg_status sddg_nccl_unique_id(sddg_nccl_id* id) {
     try {
         static_assert(sizeof(ncclUniqueId) == sizeof(sddg_nccl_id), "nccl id size");
         ncclUniqueId u;
-        nck(ncclGetUniqueId(&u), "ncclGetUniqueId");
+        nck(nccl().GetUniqueId(&u), "ncclGetUniqueId");
         std::memcpy(id->bytes, &u, sizeof(u));
     } catch (const Fail& f) {
         return team_fail(f);
@@ -297,7 +353,7 @@ sddg_status sddg_create_dist(int32_t device, int32_t rank, int32_t nranks, const
         std::memcpy(&u, id->bytes, sizeof(u));
         ncclComm_t comm;
         ck(cudaSetDevice(device), "cudaSetDevice");
-        nck(ncclCommInitRank(&comm, nranks, u, rank), "ncclCommInitRank");
+        nck(nccl().CommInitRank(&comm, nranks, u, rank), "ncclCommInitRank");
         c->team = new Team{nranks, rank, {c}, {comm}};
     } catch (const Fail& f) {
         sddg_destroy(c);
@@ -328,7 +384,7 @@ sddg_status sddg_create_multi(int32_t n, const int32_t* devices, sddg_ctx** out)
         std::vector<ncclComm_t> comms;
         if (n > 1 && static_cast<int32_t>(distinct.size()) == n) {
             comms.resize(n);
-            nck(ncclCommInitAll(comms.data(), n, devices), "ncclCommInitAll");
+            nck(nccl().CommInitAll(comms.data(), n, devices), "ncclCommInitAll");
         }
         if (n > 1) {
             // peer access for the point copies and the copy exchange

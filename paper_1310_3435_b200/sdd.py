@@ -128,6 +128,20 @@ def lib():
             if not os.path.exists(_LIB_PATH):
                 raise ImportError(f"{_LIB_PATH} not built: run __graft_entry__.build() or "
                                   "python paper_1310_3435_b200/build.py")
+            # multi-GPU contexts load NCCL at run time: point the library at
+            # PyTorch's bundled libnccl.so.2 (the copy torch links), so the
+            # two never load different copies of the same soname
+            if "SDDG_NCCL_PATH" not in os.environ:
+                try:
+                    import importlib.util
+                    spec = importlib.util.find_spec("nvidia.nccl")
+                    for d in (spec.submodule_search_locations or []) if spec else []:
+                        cand = os.path.join(d, "lib", "libnccl.so.2")
+                        if os.path.exists(cand):
+                            os.environ["SDDG_NCCL_PATH"] = cand
+                            break
+                except (ImportError, ValueError):
+                    pass
             L = C.CDLL(_LIB_PATH)
             L.sddg_version.restype = C.c_char_p
             L.sddg_last_error.restype = C.c_char_p

@@ -201,3 +201,19 @@ def test_shard_plan_tracks_the_density():
         sdd.shard_plan([(0.0, 0.5)], m, UNIT, cfg, 2)
     with pytest.raises(sdd.ValidationError):
         sdd.shard_plan(pts, m, UNIT, cfg, 0)
+
+
+def test_nccl_loaded_at_run_time_and_torch_still_imports():
+    # libsddg links no NCCL; the first multi-GPU call loads one at run time,
+    # and it must be the copy PyTorch links (a second libnccl.so.2 loaded
+    # first would shadow torch's), so torch imports fine afterwards
+    import sys
+    code = ("from paper_1310_3435_b200 import sdd; i = sdd.nccl_unique_id(); assert len(i) == 128; "
+            "import torch, torch.distributed; "
+            "maps = open('/proc/self/maps').read(); "
+            "libs = {l.split()[-1] for l in maps.splitlines() if 'libnccl' in l}; "
+            "assert len(libs) == 1, libs; print(libs.pop())")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = subprocess.run(["readelf", "-d", sdd.library_path()], capture_output=True, text=True).stdout
+    assert "nccl" not in out
