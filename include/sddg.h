@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define SDDG_ABI_VERSION 1
+#define SDDG_ABI_VERSION 2
 
 typedef enum {
     SDDG_OK = 0,
@@ -45,7 +45,14 @@ typedef enum {
  * (proj/include/sdd/monitor.hpp:11-18, formulas proj/src/monitor.cpp:121-223).
  * Kinds 16-18 are the BASELINE.json densities given as the diffusion weight
  * w, which the reference receives as MonitorFunction::user_supplied(rho=1/w)
- * (proj/src/monitor.cpp:73-80). */
+ * (proj/src/monitor.cpp:73-80).  Kind 32 carries ANY user_supplied density
+ * as data: rho sampled on a tnx x tny grid over tdom, read through a fixed
+ * interpolant -- Catmull-Rom bicubic (cubic convolution, a = -1/2) on the
+ * grid padded by one linearly extrapolated node per side, so linear rho is
+ * reproduced exactly and the drift is continuous.  In reference mode the
+ * gradient is the reference's user_supplied central difference of that
+ * interpolant (monitor.cpp:206-219); in performance mode its analytic
+ * gradient. */
 typedef enum {
     SDDG_DENS_CONSTANT = 0,
     SDDG_DENS_RUNNING = 1,
@@ -54,7 +61,8 @@ typedef enum {
     SDDG_DENS_FIVE_RING = 4,
     SDDG_DENS_RING_W = 16,   /* w = 1+10 exp(-200 ((x-.5)^2+(y-.5)^2-1/16)^2)     */
     SDDG_DENS_SHOCK_W = 17,  /* w = 1+20 sech^2(50 (y-.5-.15 sin 2 pi x))         */
-    SDDG_DENS_TWOBUMP_W = 18 /* w = 1+15 e^{-100|x-(.3,.3)|^2}+15 e^{-100|x-(.7,.6)|^2} */
+    SDDG_DENS_TWOBUMP_W = 18, /* w = 1+15 e^{-100|x-(.3,.3)|^2}+15 e^{-100|x-(.7,.6)|^2} */
+    SDDG_DENS_TABLE = 32      /* rho tabulated on a grid (table, tnx, tny, tdom)    */
 } sddg_density_kind;
 
 typedef enum {
@@ -63,21 +71,28 @@ typedef enum {
      * for kinds 16-18 (proj/src/monitor.cpp:206-219). */
     SDDG_GRAD_REFERENCE = 0,
     /* Performance mode: analytic drift grad(w)/w for kinds 16-18 (BASELINE.json
-     * configs), and the five-ring (kind 4) with table-driven tanh; fastmath
-     * elementary functions, fp64 or fp32, checked statistically. */
+     * configs), the five-ring (kind 4) with table-driven tanh, and the
+     * interpolant's own gradient for kind 32; fastmath elementary functions,
+     * fp64 or fp32, checked statistically. */
     SDDG_GRAD_ANALYTIC = 1
 } sddg_grad_mode;
+
+typedef struct {
+    double xmin, xmax, ymin, ymax; /* sdd::RectDomain (geometry.hpp:27-46) */
+} sddg_domain;
 
 typedef struct {
     int32_t kind;      /* sddg_density_kind */
     int32_t grad_mode; /* sddg_grad_mode */
     double R, alpha;   /* builtin parameters (monitor.hpp:26-38) */
     double fd_h;       /* user_supplied FD step, reference default 1e-6 */
+    /* SDDG_DENS_TABLE only: rho at the nodes of a tnx x tny grid over tdom
+     * (index j*tnx + i, tnx, tny >= 2, finite and > 0); read during the
+     * call, not retained */
+    const double* table;
+    int32_t tnx, tny;
+    sddg_domain tdom;
 } sddg_density;
-
-typedef struct {
-    double xmin, xmax, ymin, ymax; /* sdd::RectDomain (geometry.hpp:27-46) */
-} sddg_domain;
 
 /* sdd::BoundaryData (proj/include/sdd/boundary.hpp:12-18): Dirichlet tables
  * tabulated at the nodes of an nx x ny grid over dom; index 0..3 = bottom,

@@ -25,19 +25,21 @@ ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
 # density kinds (sdd_oracle.h; same numbering as include/sddg.h)
 CONSTANT, RUNNING, HUANG_SLOAN, MACKENZIE, FIVE_RING = 0, 1, 2, 3, 4
 RING_W, SHOCK_W, TWOBUMP_W = 16, 17, 18
+TABLE = 32
 
 ERRORS = {1: "ValidationError", 2: "OutOfDomainError", 3: "EvaluationError",
           4: "NumericalError", 5: "LayoutError", 7: "Error"}
 
 
-class Density(C.Structure):
-    _fields_ = [("kind", C.c_int), ("R", C.c_double), ("alpha", C.c_double),
-                ("fd_h", C.c_double)]
-
-
 class Domain(C.Structure):
     _fields_ = [("xmin", C.c_double), ("xmax", C.c_double), ("ymin", C.c_double),
                 ("ymax", C.c_double)]
+
+
+class Density(C.Structure):
+    _fields_ = [("kind", C.c_int), ("R", C.c_double), ("alpha", C.c_double),
+                ("fd_h", C.c_double), ("table", C.POINTER(C.c_double)), ("tnx", C.c_int),
+                ("tny", C.c_int), ("tdom", Domain)]
 
 
 class WalkCfg(C.Structure):
@@ -73,6 +75,16 @@ def density(kind, R=None, alpha=None, fd_h=1e-6):
                 MACKENZIE: (50.0, 10.0), FIVE_RING: (30.0, 0.2)}
     r0, a0 = defaults.get(kind, (0.0, 0.0))
     return Density(kind, r0 if R is None else R, a0 if alpha is None else alpha, fd_h)
+
+
+def table_density(rho, dom, fd_h=1e-6):
+    """A tabulated user density (rho[j, i] at the grid nodes over dom): the
+    reference receives it as user_supplied(the harness's interpolant)."""
+    t = np.ascontiguousarray(rho, dtype=np.float64)
+    d = Density(TABLE, 0.0, 0.0, fd_h, t.ctypes.data_as(C.POINTER(C.c_double)), t.shape[1], t.shape[0],
+                Domain(dom.xmin, dom.xmax, dom.ymin, dom.ymax))
+    d._keep = t
+    return d
 
 
 def walk_cfg(scheme="linear", dt=1e-4, lam=1000.0, walks=10000, seed=1,

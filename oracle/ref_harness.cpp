@@ -13,8 +13,11 @@
 // Used by tests/golden/make_golden.py (fixtures), tests/ (pins) and the
 // bench.py CPU arms (timing of the reference's own mc_estimate path).
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <exception>
 #include <optional>
 #include <string>
@@ -38,13 +41,70 @@ namespace {
 
 thread_local std::string g_err;
 
+struct Domain {
+    double xmin, xmax, ymin, ymax;
+};
+
 struct Density {
     int kind;
     double R, alpha, fd_h;
+    // kind 32 (a tabulated user density, include/sddg.h SDDG_DENS_TABLE)
+    const double* table;
+    int tnx, tny;
+    Domain tdom;
 };
 
-struct Domain {
-    double xmin, xmax, ymin, ymax;
+// A tabulated rho as the reference receives any user density: a callable
+// handed to MonitorFunction::user_supplied.  The callable restates the
+// library's documented interpolant (include/sddg.h, SDDG_DENS_TABLE):
+// Catmull-Rom bicubic on the samples padded by one linearly extrapolated
+// node per side, cell clamp(floor(s), 0, n-2), local t = s - cell, with the
+// normative operation order, so the reference's central difference of it is
+// what the GPU's reference mode must reproduce.
+struct TabRho {
+    std::vector<double> pad;  // (nx+2) x (ny+2)
+    int nx, ny;
+    double x0, y0, ihx, ihy;
+
+    TabRho(const double* f, int nx_, int ny_, const Domain& dom) : nx(nx_), ny(ny_) {
+        const int w = nx + 2;
+        pad.assign(static_cast<std::size_t>(w) * (ny + 2), 0.0);
+        for (int j = 1; j <= ny; ++j) {
+            for (int i = 1; i <= nx; ++i) pad[j * w + i] = f[(j - 1) * nx + (i - 1)];
+            pad[j * w] = 2.0 * pad[j * w + 1] - pad[j * w + 2];
+            pad[j * w + nx + 1] = 2.0 * pad[j * w + nx] - pad[j * w + nx - 1];
+        }
+        for (int i = 0; i < w; ++i) {
+            pad[i] = 2.0 * pad[w + i] - pad[2 * w + i];
+            pad[(ny + 1) * w + i] = 2.0 * pad[ny * w + i] - pad[(ny - 1) * w + i];
+        }
+        x0 = dom.xmin;
+        y0 = dom.ymin;
+        ihx = 1.0 / ((dom.xmax - dom.xmin) / (nx - 1));
+        ihy = 1.0 / ((dom.ymax - dom.ymin) / (ny - 1));
+    }
+    static void weights(double t, double w[4]) {
+        w[0] = 0.5 * (((2.0 - t) * t - 1.0) * t);
+        w[1] = 0.5 * ((3.0 * t - 5.0) * t * t + 2.0);
+        w[2] = 0.5 * (((4.0 - 3.0 * t) * t + 1.0) * t);
+        w[3] = 0.5 * ((t - 1.0) * t * t);
+    }
+    double operator()(Point q) const {
+        const double sx = (q.x - x0) * ihx, sy = (q.y - y0) * ihy;
+        int i = static_cast<int>(std::floor(sx)), j = static_cast<int>(std::floor(sy));
+        i = std::min(std::max(i, 0), nx - 2);
+        j = std::min(std::max(j, 0), ny - 2);
+        double wx[4], wy[4];
+        weights(sx - i, wx);
+        weights(sy - j, wy);
+        const int w = nx + 2;
+        double v = 0.0;
+        for (int b = 0; b < 4; ++b) {
+            const double* r = pad.data() + static_cast<std::size_t>(j + b) * w + i;
+            v = v + wy[b] * (((wx[0] * r[0] + wx[1] * r[1]) + wx[2] * r[2]) + wx[3] * r[3]);
+        }
+        return v;
+    }
 };
 
 struct WalkCfgC {
@@ -78,6 +138,13 @@ MonitorFunction make_monitor(const Density& d, const Domain& dom) {
         case 2: return MonitorFunction::huang_sloan(d.alpha, d.R);
         case 3: return MonitorFunction::mackenzie(d.alpha, d.R);
         case 4: return MonitorFunction::five_ring(d.alpha, d.R);
+        case 32: {
+            auto t = std::make_shared<TabRho>(d.table, d.tnx, d.tny, d.tdom);
+            return MonitorFunction::user_supplied([t](Point p) { return (*t)(p); },
+                                                  RectDomain(d.tdom.xmin, d.tdom.xmax, d.tdom.ymin,
+                                                             d.tdom.ymax),
+                                                  d.fd_h);
+        }
         default: {
             const int k = d.kind;
             return MonitorFunction::user_supplied(

@@ -7,16 +7,37 @@
 // weights are bit-identical to the reference's.
 #pragma once
 #include <cmath>
+#include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/sddg.h"
+#include "table_density.h"
 
 namespace sddg {
 
 struct HostDensity {
     int kind;
     double R, alpha, fd_h;
+    // SDDG_DENS_TABLE: the padded samples (owned) and their interpolant view
+    std::shared_ptr<const std::vector<double>> padded;
+    TableDensity td;
+
+    static HostDensity of(const sddg_density& d) {
+        HostDensity h{d.kind, d.R, d.alpha, d.fd_h, nullptr, TableDensity{}};
+        if (d.kind == SDDG_DENS_TABLE && d.table && d.tnx >= 2 && d.tny >= 2) {
+            h.padded = std::make_shared<const std::vector<double>>(pad_table(d.table, d.tnx, d.tny));
+            h.td.t = h.padded->data();
+            h.td.nx = d.tnx;
+            h.td.ny = d.tny;
+            h.td.x0 = d.tdom.xmin;
+            h.td.y0 = d.tdom.ymin;
+            h.td.ihx = 1.0 / ((d.tdom.xmax - d.tdom.xmin) / (d.tnx - 1));
+            h.td.ihy = 1.0 / ((d.tdom.ymax - d.tdom.ymin) / (d.tny - 1));
+        }
+        return h;
+    }
 
     static double w_of(int kind, double x, double y) {
         constexpr double kPi = 3.14159265358979323846264338327950288;
@@ -91,6 +112,7 @@ struct HostDensity {
                 r = std::sqrt(1.0 + alpha * (ux * ux + uy * uy));
                 break;
             }
+            case SDDG_DENS_TABLE: r = table_rho(td, x, y); break;
             default: r = 1.0 / w_of(kind, x, y); break;
         }
         if (!std::isfinite(r)) throw std::domain_error("monitor density not finite");
@@ -140,6 +162,12 @@ struct HostDensity {
                 const double r = std::sqrt(1.0 + alpha * (ux * ux + uy * uy));
                 gx = alpha * (ux * uxx + uy * uxy) / r;
                 gy = alpha * (ux * uxy + uy * uyy) / r;
+                return;
+            }
+            case SDDG_DENS_TABLE: {  // user_supplied central difference of the interpolant
+                const double h = fd_h;
+                gx = (table_rho(td, x + h, y) - table_rho(td, x - h, y)) / (2.0 * h);
+                gy = (table_rho(td, x, y + h) - table_rho(td, x, y - h)) / (2.0 * h);
                 return;
             }
             default: {

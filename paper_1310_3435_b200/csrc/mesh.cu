@@ -223,7 +223,7 @@ __global__ void quality_fold(const double* __restrict__ q, long long cells, doub
     out[1] = sum / static_cast<double>(cells);
 }
 
-__device__ double rho_any(int kind, double R, double al, double x, double y) {
+__device__ double rho_any(int kind, double R, double al, const TableDensity& tab, double x, double y) {
     switch (kind) {
         case SDDG_DENS_CONSTANT: return R;
         case SDDG_DENS_RUNNING: {
@@ -248,6 +248,7 @@ __device__ double rho_any(int kind, double R, double al, double x, double y) {
         }
         case SDDG_DENS_RING_W: return 1.0 / w_ring(x, y);
         case SDDG_DENS_SHOCK_W: return 1.0 / w_shock(x, y);
+        case SDDG_DENS_TABLE: return table_rho(tab, x, y);
         default: return 1.0 / w_twobump(x, y);
     }
 }
@@ -256,13 +257,13 @@ __device__ double rho_any(int kind, double R, double al, double x, double y) {
 // order-free; per-block max then atomic max on the (non-negative) bits.
 __global__ void linf_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                             const double* __restrict__ RX, const double* __restrict__ RY,
-                            long long n, int kind, double R, double al,
+                            long long n, int kind, double R, double al, const TableDensity tab,
                             unsigned long long* out_bits) {
     const long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     double v = 0.0;
     if (k < n) {
-        const double rr = rho_any(kind, R, al, RX[k], RY[k]);
-        const double rm = rho_any(kind, R, al, X[k], Y[k]);
+        const double rr = rho_any(kind, R, al, tab, RX[k], RY[k]);
+        const double rm = rho_any(kind, R, al, tab, X[k], Y[k]);
         v = fabs(rr - rm);
     }
 #pragma unroll
@@ -293,9 +294,9 @@ cudaError_t launch_quality(const double* X, const double* Y, int m_xi, int m_eta
 }
 
 cudaError_t launch_linf(const double* X, const double* Y, const double* RX, const double* RY,
-                        long long n, int kind, double R, double al, unsigned long long* out_bits,
-                        cudaStream_t s) {
-    linf_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(X, Y, RX, RY, n, kind, R, al,
+                        long long n, int kind, double R, double al, const TableDensity& tab,
+                        unsigned long long* out_bits, cudaStream_t s) {
+    linf_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(X, Y, RX, RY, n, kind, R, al, tab,
                                                                        out_bits);
     return cudaGetLastError();
 }

@@ -67,7 +67,29 @@ void validate_walk(const sddg_walk_config& c) {
         fail(SDDG_ERR_VALIDATION, "WalkConfig: unknown precision");
 }
 
+// A tabulated density: a table, >= 2 x 2 finite positive samples over a
+// non-empty domain (the reference's user_supplied checks its rho the same
+// way, monitor.cpp:105-119, on the interpolant: check_positivity).
+void check_table(const sddg_density& d) {
+    if (!d.table) fail(SDDG_ERR_VALIDATION, "tabulated density: table is NULL");
+    if (d.tnx < 2 || d.tny < 2) fail(SDDG_ERR_VALIDATION, "tabulated density: needs at least 2 x 2 samples");
+    if (!(d.tdom.xmin < d.tdom.xmax) || !(d.tdom.ymin < d.tdom.ymax))
+        fail(SDDG_ERR_VALIDATION, "tabulated density: empty domain");
+    if (!(d.fd_h > 0.0)) fail(SDDG_ERR_VALIDATION, "fd_h must be > 0");
+    for (int64_t k = 0; k < static_cast<int64_t>(d.tnx) * d.tny; ++k)
+        if (!std::isfinite(d.table[k]) || d.table[k] <= 0.0)
+            fail(SDDG_ERR_EVALUATION, "tabulated density: samples must be finite and > 0");
+}
+
 int drift_variant(const sddg_density& d, int precision) {
+    if (d.kind == SDDG_DENS_TABLE) {
+        check_table(d);
+        if (d.grad_mode == SDDG_GRAD_ANALYTIC) return 36;  // DV_TABLE_AN
+        if (d.grad_mode != SDDG_GRAD_REFERENCE) fail(SDDG_ERR_VALIDATION, "unknown grad_mode");
+        if (precision == SDDG_FP32)
+            fail(SDDG_ERR_VALIDATION, "fp32 walks need the analytic drift (grad_mode SDDG_GRAD_ANALYTIC)");
+        return 20;  // DV_TABLE_FD
+    }
     const bool wkind = d.kind >= SDDG_DENS_RING_W && d.kind <= SDDG_DENS_TWOBUMP_W;
     const bool builtin = d.kind >= SDDG_DENS_CONSTANT && d.kind <= SDDG_DENS_FIVE_RING;
     if (!wkind && !builtin) fail(SDDG_ERR_VALIDATION, "unknown density kind");
@@ -87,7 +109,12 @@ int drift_variant(const sddg_density& d, int precision) {
     return d.kind;
 }
 
-HostDensity host_density(const sddg_density& d) { return HostDensity{d.kind, d.R, d.alpha, d.fd_h}; }
+void check_table(const sddg_density& d);
+
+HostDensity host_density(const sddg_density& d) {
+    if (d.kind == SDDG_DENS_TABLE) check_table(d);
+    return HostDensity::of(d);
+}
 
 // MonitorFunction::check_positivity (proj/src/monitor.cpp:105-119) over the
 // density's domain: the builtins' own, the caller's for user_supplied kinds.
@@ -95,6 +122,7 @@ void check_positivity(const sddg_density& d, const sddg_domain& dom) {
     sddg_domain pd = dom;
     if (d.kind <= SDDG_DENS_MACKENZIE) pd = {0, 1, 0, 1};
     if (d.kind == SDDG_DENS_FIVE_RING) pd = {-1, 1, -1, 1};
+    if (d.kind == SDDG_DENS_TABLE) pd = d.tdom;
     const HostDensity h = host_density(d);
     for (int j = 0; j < 33; ++j)
         for (int i = 0; i < 33; ++i) {
@@ -296,6 +324,20 @@ std::vector<uint32_t> cost_order(const std::vector<double>& cost, const std::vec
     return perm;
 }
 
+// A tabulated density's padded samples in device memory (empty view for the
+// formula kinds).
+TableDensity upload_density(sddg_ctx* c, const sddg_density& d) {
+    TableDensity t;
+    if (d.kind != SDDG_DENS_TABLE) return t;
+    const HostDensity h = host_density(d);
+    const size_t bytes = sizeof(double) * h.padded->size();
+    double* p = static_cast<double*>(c->dens_tab.ensure(bytes));
+    ck(cudaMemcpy(p, h.padded->data(), bytes, cudaMemcpyHostToDevice), "h2d density table");
+    t = h.td;
+    t.t = p;
+    return t;
+}
+
 double* upload_tables(sddg_ctx* c, const sddg_boundary& bd) {
     const size_t nx = bd.nx, ny = bd.ny;
     std::vector<double> h(4 * (nx + ny));
@@ -358,6 +400,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     uint32_t* rm = static_cast<uint32_t*>(c->rec_meta.ensure(sizeof(uint32_t) * cap));
     WalkArgs a;
     fill_args(a, d, dom, bd, cfg, dtab);
+    a.tab = upload_density(c, d);
     a.fm_tables = c->fm_tables.p;
     a.walks = W;
     a.walk_lo = 0;
@@ -1182,8 +1225,8 @@ void make_fm_tables(void* out) {
 }
 
 bool walk_variant_supported(int dv, int precision) {
-    if (dv >= 32 && dv <= 35) return true;  // walk_fast.cu: DV_RING_AN .. DV_FIVE_RING_AN
-    return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18));
+    if (dv >= 32 && dv <= 36) return true;  // walk_fast.cu: DV_RING_AN .. DV_TABLE_AN
+    return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18) || dv == 20);
 }
 
 cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s) {
@@ -1248,7 +1291,7 @@ void sddg_destroy(sddg_ctx* c) {
     team_destroy(c);
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->t_recv, &c->t_nodes, &c->t_pts, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->t_recv, &c->t_nodes, &c->t_pts, &c->dens_tab, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->s_perm, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
@@ -1350,6 +1393,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         sddg_path* dd = static_cast<sddg_path*>(ctx->dump.ensure(sizeof(sddg_path) * n));
         WalkArgs a;
         fill_args(a, *dens, *dom, *bd, *cfg, dtab);
+        a.tab = upload_density(ctx, *dens);
         a.fm_tables = ctx->fm_tables.p;
         a.px = dn;
         a.py = dn + 1;
@@ -1668,7 +1712,7 @@ sddg_status sddg_quality_report(sddg_ctx* ctx, const double* x, const double* y,
         if (dens) {
             drift_variant(*dens, SDDG_FP64);  // validates the kind
             ck(launch_linf(dm, dm + M, dm + 2 * M, dm + 3 * M, static_cast<long long>(M), dens->kind,
-                           dens->R, dens->alpha, dl, st),
+                           dens->R, dens->alpha, upload_density(ctx, *dens), dl, st),
                "linf launch");
             launches += 1;
         }

@@ -102,6 +102,7 @@ struct sddg_ctx {
     // several GPUs (team.cu): null for a single-device context
     Team* team = nullptr;
     sddg::rt::DevBuf t_recv, t_nodes, t_pts;  // team exchange buffers on this device
+    sddg::rt::DevBuf dens_tab;                // padded samples of a tabulated density
 };
 
 namespace sddg {

@@ -10,6 +10,7 @@
 
 #include "../../include/sddg.h"
 #include "philox.cuh"
+#include "table_density.h"
 
 namespace sddg {
 
@@ -30,6 +31,7 @@ struct WalkArgs {
     const double* tg[4];
     // density
     double R, alpha, fd_h;
+    TableDensity tab;  // SDDG_DENS_TABLE: padded samples in device memory
     // walk config
     int scheme, bridge;
     double dt, sqrt2dt, lambda, nu2, bridge_thr;
@@ -148,8 +150,8 @@ cudaError_t launch_invert(const double* xi, const double* eta, int nx, int ny, d
 cudaError_t launch_quality(const double* X, const double* Y, int m_xi, int m_eta, double* qbuf,
                            double* out2, int* err, cudaStream_t s);
 cudaError_t launch_linf(const double* X, const double* Y, const double* RX, const double* RY,
-                        long long n, int kind, double R, double al, unsigned long long* out_bits,
-                        cudaStream_t s);
+                        long long n, int kind, double R, double al, const TableDensity& tab,
+                        unsigned long long* out_bits, cudaStream_t s);
 
 cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
 cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long* host_maxulp5);

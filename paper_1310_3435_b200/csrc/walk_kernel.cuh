@@ -383,7 +383,7 @@ constexpr bool kBigTables = sizeof(fm::FmTables) > 24 * 1024;
 // drifts that need more than 64 registers in the fp64 table kernel
 template <int DV>
 __host__ __device__ constexpr bool walk_heavy_drift() {
-    return DV == DV_SHOCK_AN || DV == DV_FIVE_RING_AN;
+    return DV == DV_SHOCK_AN || DV == DV_FIVE_RING_AN || DV == DV_TABLE_AN;
 }
 template <int DV, typename Real>
 __host__ __device__ constexpr int walk_block() {
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
         if constexpr (walk_uses_tables<DV, Real>()) return dom.in_box_hi(px, py);
         else return dom.in_box(px, py);
     };
-    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h)};
+    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab};
     const Real dt = Real(a.dt);
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);

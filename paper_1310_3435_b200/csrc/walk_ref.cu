@@ -1,6 +1,7 @@
 // walk_ref.cu -- K1 instantiations that reproduce the reference arithmetic:
 // fp64 with the reference's builtin analytic drifts (DV 0-4) and the
-// user_supplied central-difference drift of the BASELINE densities (DV 16-18).
+// user_supplied central-difference drift of the BASELINE densities (DV 16-18)
+// and of a tabulated density's interpolant (DV 20).
 // Compiled with -fmad=false: every multiply and add rounds separately, as in
 // the FMA-free x86-64 reference objects.  The only remaining difference from
 // the reference is libm (CUDA's exp/log/sincos vs glibc's, ~1 ulp).
@@ -9,7 +10,7 @@
 namespace sddg {
 
 #define SDDG_REF_VARIANTS(X) X(DV_CONSTANT) X(DV_RUNNING) X(DV_HUANG_SLOAN) X(DV_MACKENZIE) \
-    X(DV_FIVE_RING) X(DV_RING_FD) X(DV_SHOCK_FD) X(DV_TWOBUMP_FD)
+    X(DV_FIVE_RING) X(DV_RING_FD) X(DV_SHOCK_FD) X(DV_TWOBUMP_FD) X(DV_TABLE_FD)
 
 cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s) {
     switch (dv) {

@@ -55,6 +55,7 @@ _ERR = {1: ValidationError, 2: OutOfDomainError, 3: EvaluationError, 4: Numerica
 # --------------------------------------------------------------- C structs
 CONSTANT, RUNNING, HUANG_SLOAN, MACKENZIE, FIVE_RING = 0, 1, 2, 3, 4
 RING_W, SHOCK_W, TWOBUMP_W = 16, 17, 18
+TABLE = 32
 GRAD_REFERENCE, GRAD_ANALYTIC = 0, 1
 LINEAR, EXPONENTIAL = 0, 1
 FP64, FP32 = 0, 1
@@ -64,14 +65,15 @@ INTERP = {"linear": 0, "spline": 1}
 BC_REFERENCE, BC_IDENTITY = 0, 1
 
 
-class _Density(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("grad_mode", C.c_int32), ("R", C.c_double),
-                ("alpha", C.c_double), ("fd_h", C.c_double)]
-
-
 class _Domain(C.Structure):
     _fields_ = [("xmin", C.c_double), ("xmax", C.c_double), ("ymin", C.c_double),
                 ("ymax", C.c_double)]
+
+
+class _Density(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("grad_mode", C.c_int32), ("R", C.c_double),
+                ("alpha", C.c_double), ("fd_h", C.c_double), ("table", C.POINTER(C.c_double)),
+                ("tnx", C.c_int32), ("tny", C.c_int32), ("tdom", _Domain)]
 
 
 class _Boundary(C.Structure):
@@ -306,6 +308,8 @@ class MonitorFunction:
     grad_mode: int = GRAD_REFERENCE
     fd_h: float = 1e-6
     domain: RectDomain = RectDomain(0.0, 1.0, 0.0, 1.0)
+    # SDDG_DENS_TABLE: rho samples (ny, nx) at the grid nodes over `domain`
+    table: np.ndarray | None = field(default=None, compare=False, hash=False, repr=False)
 
     @staticmethod
     def constant(value=1.0):
@@ -355,15 +359,35 @@ class MonitorFunction:
         return MonitorFunction(kind, grad_mode=GRAD_ANALYTIC if analytic else GRAD_REFERENCE,
                                fd_h=fd_step, domain=domain)
 
+    @staticmethod
+    def tabulated(rho, domain: RectDomain, analytic=False, fd_step=1e-6):
+        """Any user_supplied density as data (SDDG_DENS_TABLE): rho sampled at
+        the nodes of a grid over `domain`, rho[j, i] at (x_i, y_j), read through
+        the library's Catmull-Rom bicubic interpolant.  analytic=False: the
+        reference's central difference of the interpolant (bit-faithful to
+        MonitorFunction::user_supplied of that interpolant); analytic=True:
+        its exact gradient (performance mode, fp64 or fp32)."""
+        t = np.ascontiguousarray(rho, dtype=np.float64)
+        if t.ndim != 2 or t.shape[0] < 2 or t.shape[1] < 2:
+            raise ValidationError("tabulated density: rho must be a 2-D array of at least 2 x 2")
+        return MonitorFunction(TABLE, grad_mode=GRAD_ANALYTIC if analytic else GRAD_REFERENCE,
+                               fd_h=fd_step, domain=domain, table=t)
+
     ring = staticmethod(lambda analytic=False: MonitorFunction.weight(RING_W, analytic))
     shock = staticmethod(lambda analytic=False: MonitorFunction.weight(SHOCK_W, analytic))
     two_bump = staticmethod(lambda analytic=False: MonitorFunction.weight(TWOBUMP_W, analytic))
 
     def with_grad(self, grad_mode):
-        return MonitorFunction(self.kind, self.R, self.alpha, grad_mode, self.fd_h, self.domain)
+        return MonitorFunction(self.kind, self.R, self.alpha, grad_mode, self.fd_h, self.domain, self.table)
 
     def c(self):
-        return _Density(self.kind, self.grad_mode, self.R, self.alpha, self.fd_h)
+        d = _Density(self.kind, self.grad_mode, self.R, self.alpha, self.fd_h)
+        if self.table is not None:
+            d.table = self.table.ctypes.data_as(C.POINTER(C.c_double))
+            d.tny, d.tnx = self.table.shape
+            d.tdom = self.domain.c()
+            d._keep = self.table
+        return d
 
 
 # --------------------------------------------------------------- configs

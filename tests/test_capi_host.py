@@ -49,7 +49,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version():
-    assert sdd.lib().sddg_abi_version() == 1
+    assert sdd.lib().sddg_abi_version() == 2
     assert b"sm_100a" in sdd.lib().sddg_version()
 
 
