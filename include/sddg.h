@@ -460,6 +460,15 @@ sddg_status sddg_perona_malik(sddg_ctx* ctx, double* xi, double* eta, int32_t nx
                               const sddg_domain* dom, const sddg_smooth_config* cfg, int32_t sx,
                               int32_t sy, int32_t* stability_warning);
 
+/* BASELINE.json config 4's "Laplacian smoothing, N sweeps" as the reference
+ * can express it: Perona-Malik FTCS (perona_malik above,
+ * smoothing.cpp:33-123) with the edge-stopping factor c = 1 (k = infinity)
+ * and dt = hx*hy/4, the largest stable step, i.e. every sweep replaces each
+ * interior value by the 4-neighbour average (hx = hy; the hx, hy-weighted
+ * average otherwise).  Boundary values are kept; global scope. */
+sddg_status sddg_laplacian_smooth(sddg_ctx* ctx, double* xi, double* eta, int32_t nx, int32_t ny,
+                                  const sddg_domain* dom, int32_t sweeps);
+
 /* Replaces sdd::smooth_interface (smoothing.hpp:41): tricube-weighted local
  * quadratic regression over an odd `span` window; endpoints kept. */
 sddg_status sddg_smooth_interface(sddg_ctx* ctx, const double* values, int32_t n, int32_t span,

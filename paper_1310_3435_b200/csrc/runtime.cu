@@ -1806,6 +1806,21 @@ sddg_status sddg_perona_malik(sddg_ctx* ctx, double* xi, double* eta, int32_t nx
     API_END(ctx)
 }
 
+sddg_status sddg_laplacian_smooth(sddg_ctx* ctx, double* xi, double* eta, int32_t nx, int32_t ny,
+                                  const sddg_domain* dom, int32_t sweeps) {
+    if (!dom) {
+        set_free_error("laplacian_smooth: domain is NULL");
+        return SDDG_ERR_VALIDATION;
+    }
+    if (sweeps < 0) {
+        if (ctx) ctx->err = "laplacian_smooth: sweeps must be >= 0";
+        return SDDG_ERR_VALIDATION;
+    }
+    const double hx = (dom->xmax - dom->xmin) / (nx - 1), hy = (dom->ymax - dom->ymin) / (ny - 1);
+    const sddg_smooth_config cfg{INFINITY, hx * hy / 4.0, sweeps, SDDG_SMOOTH_GLOBAL};
+    return sddg_perona_malik(ctx, xi, eta, nx, ny, dom, &cfg, 1, 1, nullptr);
+}
+
 sddg_status sddg_stochastic_full(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                                  int32_t nx, int32_t ny, const sddg_walk_config* cfg, double* xi,
                                  double* eta, sddg_sdd_stats* stats) {

@@ -1008,10 +1008,14 @@ def write_mesh(mesh: PhysicalMesh, xi, eta, spec: GridSpec, path: str):
 
 
 def laplacian_smooth(xi, eta, spec: GridSpec, sweeps: int, ctx=None):
-    """BASELINE config 4's "Laplacian smoothing, N sweeps" as the reference
-    maps it: Perona-Malik FTCS with c = 1 (k huge) and
-    dt = hx*hy/4, i.e. the 4-neighbour average for hx = hy."""
-    dt = spec.hx() * spec.hy() / 4.0
-    xi2, eta2, _ = perona_malik(xi, eta, spec, SmoothConfig(k=1e150, dt=dt, steps=sweeps, scope="global"),
-                                ctx=ctx)
+    """BASELINE config 4's "Laplacian smoothing, N sweeps" (sddg_laplacian_smooth):
+    as the reference can express it, Perona-Malik FTCS with c = 1
+    and dt = hx*hy/4, i.e. the 4-neighbour average for hx = hy; boundary kept."""
+    ctx = ctx or default_context()
+    xi2, eta2 = _f64(xi).copy(), _f64(eta).copy()
+    if xi2.size != spec.nx * spec.ny or eta2.size != spec.nx * spec.ny:
+        raise ValidationError("laplacian_smooth: field size does not match the grid")
+    dom = spec.domain.c()
+    _check(lib().sddg_laplacian_smooth(ctx.handle, _dp(xi2), _dp(eta2), spec.nx, spec.ny, C.byref(dom),
+                                       int(sweeps)), ctx.handle)
     return xi2, eta2

@@ -91,3 +91,29 @@ def test_unknown_interp_rejected():
     px, py, pid = sdd.interface_nodes(m, lay, plan)
     with pytest.raises(sdd.ValidationError):
         sdd.fill_interfaces(m, lay, plan, bd, _fake(px, py, pid, lambda a, b: a), interp="cubic")
+
+
+@pytest.mark.gpu
+def test_laplacian_smooth_is_the_four_neighbour_average(refimpl):
+    # sddg_laplacian_smooth (config 4's "5 Laplacian sweeps"):
+    # Perona-Malik FTCS with c = 1 and dt = h^2/4 is the 4-neighbour average
+    # (to the rounding of u + dt * lap u), boundary kept; and it equals the
+    # reference's perona_malik with the same mapping bit for bit
+    from oracle import bindings as B
+    n = 65
+    spec = sdd.GridSpec(UNIT, n, n)
+    rng = np.random.default_rng(1)
+    x = np.linspace(0, 1, n)
+    X, Y = np.meshgrid(x, x)
+    xi = (X + 0.01 * rng.standard_normal((n, n)) * (X > 0) * (X < 1) * (Y > 0) * (Y < 1)).ravel()
+    eta = (Y + 0.01 * rng.standard_normal((n, n)) * (X > 0) * (X < 1) * (Y > 0) * (Y < 1)).ravel()
+    a, b = sdd.laplacian_smooth(xi, eta, spec, 5)
+    u = xi.reshape(n, n).copy()
+    for _ in range(5):
+        v = u.copy()
+        v[1:-1, 1:-1] = 0.25 * (u[1:-1, 2:] + u[1:-1, :-2] + u[2:, 1:-1] + u[:-2, 1:-1])
+        u = v
+    assert np.max(np.abs(a.reshape(n, n) - u)) < 1e-15
+    assert np.array_equal(a.reshape(n, n)[0], xi.reshape(n, n)[0])
+    rx, ry = refimpl.perona_malik(xi, eta, n, n, B.Domain(0, 1, 0, 1), 1e150, (1 / 64) ** 2 / 4, 5)
+    assert np.array_equal(a, rx) and np.array_equal(b, ry)
