@@ -143,15 +143,19 @@ def pipe_fractions(steps_per_s, sm_mhz, precision, sms):
 
 
 def ncu_summary():
-    """Pipe / issue utilisation of K1 from the committed ncu capture
-    (profiles/ncu_walk_summary.json; measured with ncu, not in this run)."""
+    """Pipe / issue utilisation of K1 from the committed ncu capture at the
+    bench config (profiles/ncu_walk_summary.json; measured with ncu, not in
+    this run)."""
     path = os.path.join(ROOT, "profiles", "ncu_walk_summary.json")
     try:
-        d = json.load(open(path))["fp64_config2"]
+        d = json.load(open(path))["fp64_config2_1e5"]
         m = d["metrics"]
-        return {"source": "profiles/ncu_walk_summary.json (" + d["command"] + ")",
-                "issue_slots_busy_pct": float(m["sm__inst_issued.avg.pct_of_peak_sustained_active"]["value"]),
-                "fp64_pipe_pct": float(m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]["value"]),
+        g = lambda k: float(m[k]["value"])  # noqa: E731
+        return {"source": "profiles/ncu_walk_summary.json fp64_config2_1e5 (" + d["command"] + ")",
+                "issue_slots_busy_pct": g("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+                "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "alu_pipe_pct": g("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                "active_lanes_per_warp_instruction": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
                 "instructions_per_path_step": d["instructions_per_path_step"],
                 "dram_bytes_per_walk": d.get("dram_bytes_per_walk")}
     except (OSError, KeyError, ValueError):

@@ -33,3 +33,4 @@ def test_ncu_summary_fields():
     assert 0 < s["issue_slots_busy_pct"] <= 100 and 0 < s["fp64_pipe_pct"] <= 100
     assert 100 < s["instructions_per_path_step"] < 400
     assert 15 < s["dram_bytes_per_walk"] < 40  # algorithmic 20 B per walk record
+    assert 28 <= s["active_lanes_per_warp_instruction"] <= 32
