@@ -34,7 +34,13 @@ using namespace sddg::rt;
 
 namespace {
 
-__global__ void set_next_kernel(Counters* c, unsigned long long v) { c->next = v; }
+// batch start: the walk counter past the grid's first walks, the walks in
+// flight, and no handoff yet
+__global__ void set_next_kernel(Counters* c, unsigned long long v, unsigned long long live) {
+    c->next = v;
+    c->live = live;
+    c->n_cont = 0;
+}
 
 thread_local std::string g_free_err;
 
@@ -368,6 +374,19 @@ void raise_kernel_error(const Counters& hc) {
                                 std::to_string(hc.err_info) + ", not the compiled SDDG_SMEM_ABS");
 }
 
+// The tail kernel (walk_tail.cuh) for fp64 walks: a handoff buffer of one
+// walk per warp of one 16-warp CTA per SM.  SDDG_NO_TAIL=1: K1 alone.
+void enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt) {
+    a.cont = nullptr;
+    a.cont_cap = 0;
+    if (precision != SDDG_FP64 || std::getenv("SDDG_NO_TAIL")) return;
+    const uint32_t cap = static_cast<uint32_t>(c->sms) * 16u;
+    a.cont = static_cast<WalkCont*>(c->tail_cont.ensure(sizeof(WalkCont) * cap));
+    a.cont_cap = cap;
+    a.n_cont = &cnt->n_cont;
+    a.live = &cnt->live;
+}
+
 // Walks + finalize for n device-resident nodes; estimates to d_out.
 void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
                    const sddg_boundary& bd, const sddg_walk_config& cfg, const double* d_px,
@@ -401,6 +420,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     WalkArgs a;
     fill_args(a, d, dom, bd, cfg, dtab);
     a.tab = upload_density(c, d);
+    enable_tail(c, a, cfg.precision, cnt);
     a.fm_tables = c->fm_tables.p;
     a.walks = W;
     a.walk_lo = 0;
@@ -428,13 +448,14 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         a.perm = dperm + b;
         a.total = static_cast<uint64_t>(nb) * W;
         const auto [grid, blk] = walk_grid(c, dv, cfg.precision, a.total);
-        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * blk);
+        const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
+        set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaGetLastError(), "set_next");
         ck(cudaEventRecord(c->bev[2 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
         ck(cudaEventRecord(c->bev[2 * bi + 1], st), "event");
         ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, nst, d_out, st, gt ? *gt : none), "reduce launch");
-        launches += 3;
+        launches += a.cont ? 4 : 3;
     }
     Counters hc;
     ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "read counters");
@@ -1291,7 +1312,7 @@ void sddg_destroy(sddg_ctx* c) {
     team_destroy(c);
     cudaSetDevice(c->device);
     for (DevBuf* b : {&c->rec_f, &c->rec_g, &c->rec_meta, &c->nodes, &c->est, &c->tables,
-                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->t_recv, &c->t_nodes, &c->t_pts, &c->dens_tab, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
+                      &c->counters, &c->dump, &c->perm, &c->nsteps, &c->t_recv, &c->t_nodes, &c->t_pts, &c->dens_tab, &c->tail_cont, &c->fm_tables, &c->gidx, &c->s_w, &c->s_jobs, &c->s_bc, &c->s_u, &c->s_info,
                       &c->s_coef, &c->s_err, &c->s_large, &c->s_omega, &c->s_perm, &c->m_in, &c->m_out, &c->m_q, &c->m_misc})
         b->release();
     for (cudaEvent_t e : c->bev) cudaEventDestroy(e);
@@ -1406,8 +1427,10 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         a.err_flag = &cnt->err_flag;
         a.err_info = &cnt->err_info;
         a.dump = dd;
+        enable_tail(ctx, a, cfg->precision, cnt);
         const auto [grid, blk] = walk_grid(ctx, dv, cfg->precision, a.total);
-        set_next_kernel<<<1, 1, 0, st>>>(cnt, static_cast<unsigned long long>(grid) * blk);
+        const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
+        set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaEventRecord(ctx->ev0, st), "event");
         ck(launch_walk(dv, cfg->precision, a, grid, st), "walk kernel launch");
         ck(cudaEventRecord(ctx->ev1, st), "event");
@@ -1419,7 +1442,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         ctx->last_ms = ms;
         ctx->last_steps = static_cast<int64_t>(hc.steps);
-        ctx->last_launches = 2;
+        ctx->last_launches = a.cont ? 3 : 2;
         raise_kernel_error(hc);
     }
     API_END(ctx)

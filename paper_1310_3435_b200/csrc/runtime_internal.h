@@ -60,7 +60,8 @@ struct DevBuf {
 struct Counters {
     unsigned long long next, steps, err_info;
     int err_flag;
-    int pad;
+    unsigned int n_cont;     // walks handed to the tail kernel
+    unsigned long long live;  // walks in flight once the batch counter has run out
 };
 
 // Expected first-exit time T(x) of the walk dX = grad(w)/w dt + sqrt(2) dW
@@ -103,6 +104,7 @@ struct sddg_ctx {
     Team* team = nullptr;
     sddg::rt::DevBuf t_recv, t_nodes, t_pts;  // team exchange buffers on this device
     sddg::rt::DevBuf dens_tab;                // padded samples of a tabulated density
+    sddg::rt::DevBuf tail_cont;               // walks handed from K1 to the tail kernel
 };
 
 namespace sddg {

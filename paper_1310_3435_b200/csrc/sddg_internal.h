@@ -59,6 +59,12 @@ struct WalkArgs {
     uint32_t* rec_meta;  // edge | epochs_used << 2
     sddg_path* dump;
     const void* fm_tables;  // fastmath.cuh FmTables in global memory (performance mode)
+    // tail handoff (walk_tail.cuh): when the batch counter has run out and at
+    // most cont_cap walks remain in flight (live), walks move to cont[] (null: off)
+    struct WalkCont* cont;
+    uint32_t cont_cap;
+    unsigned int* n_cont;
+    unsigned long long* live;
     double inv_dt;          // 1/dt: performance-mode bridge exponent d0 d1 / dt as a multiply
     double half_inv_lambda; // 1/(2 lambda): performance-mode Exp(lambda) step from -2 ln u
 };
@@ -79,6 +85,14 @@ cudaError_t occupancy_walk_fast(int dv, int precision, int* b, int* block);
 // reduce.cu: K2 fixed chunk-order finalize, one CTA per node; with peers,
 // also the fused all-gather (each record stored into every rank's buffer)
 constexpr int kMaxPeers = 16;
+// A walk handed from K1 to the tail kernel: position, slot, stream position.
+struct WalkCont {
+    double x, y;
+    uint64_t g;  // record slot
+    uint32_t node, walk, epoch, step;
+    uint32_t n;  // u64s drawn in this epoch
+    uint32_t pad;
+};
 // walk_kernel.cuh: per-lane bookkeeping of the running walk (shared memory)
 struct LaneState {
     uint64_t g;       // record slot of the running walk

@@ -28,6 +28,13 @@
 #include "philox.cuh"
 #include "sddg_internal.h"
 
+// steps between the walk kernel's handoff checks (tail kernel enabled)
+constexpr uint32_t kHandoffCheck = 256;
+// fp64 walks hand their batch tail to the tail kernel; fp32 walks (config 3's
+// huge batches, whose tail is a small share) keep the 72-register loop
+template <typename Real>
+constexpr bool kTailHandoff = sizeof(Real) == 8;
+
 #ifndef SDDG_WALK_UNROLL
 #define SDDG_WALK_UNROLL 2  // step-loop copies (A/B: tools/ab.sh with -DSDDG_WALK_UNROLL=n)
 #endif
@@ -202,10 +209,10 @@ __device__ __forceinline__ void segment_exit(const Dom<Real>& d, Real x0, Real y
 // edge_crossing_test (proj/src/sde.cpp:72-109): edges sorted by
 // (min(d0,d1), id); exponent > 40 skips without a draw; else fire if
 // u01 < exp(-ex).  SCHEME 0: ex = d0 d1 / dt (bridge_exit_test); 1: nu2 min(d0,d1).
-template <typename Real, bool FAST, int SCHEME>
+template <typename Real, bool FAST, int SCHEME, typename Stream>
 __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real y0, Real x1,
                                               Real y1, Real par, const RoundKeys& rk,
-                                              const fm::FmTables& T, LaneStream& rng, Real& hx,
+                                              const fm::FmTables& T, Stream& rng, Real& hx,
                                               Real& hy, int& edge) {
     const Real k0 = d.dist(x0, y0, 0), k1 = d.dist(x0, y0, 1), k2 = d.dist(x0, y0, 2),
                k3 = d.dist(x0, y0, 3);
@@ -329,10 +336,10 @@ __device__ __noinline__ BridgeRes bridge_rare(Real x0, Real y0, Real x1, Real y1
 // so this runs on nearly every step: the qualifying set is a bitmask, the
 // edge sort runs only when two or more edges qualify, and the draws share one
 // rolled loop.  Skipped edges draw nothing, as in edge_crossing.
-template <typename Real>
+template <typename Real, typename Stream>
 __device__ __forceinline__ bool bridge_exp_fast(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
                                                 Real nu2, const RoundKeys& rk, const fm::FmTables& T,
-                                                LaneStream& rng, Real& hx, Real& hy, int& edge) {
+                                                Stream& rng, Real& hx, Real& hy, int& edge) {
     int mask = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -371,6 +378,205 @@ __device__ __forceinline__ double table_at(const double* __restrict__ t, int n, 
     return (1.0 - u) * __ldg(t + k) + u * __ldg(t + k + 1);
 }
 
+// ---------------------------------------------------------------- one step
+// The arithmetic of one step, shared by the walk kernel K1 and the tail
+// kernel (walk_tail.cuh), so that both compute every step bit for bit alike.
+
+// u64 draws of a step's own randoms (the exit test may draw more)
+template <int SCHEME>
+constexpr uint32_t kStepDraws = SCHEME == 0 ? 2u : 3u;
+
+// Random-derived values of one step: a pure function of the stream words it
+// consumes (SCHEME 0: the normal pair's two u64s; SCHEME 1: the Exp(lambda)
+// step's u64, then the pair's two).  FAST: (R, sn, cs) of the polar form;
+// reference: (z0, z1) and, for SCHEME 1, s = sqrt(2 edt).
+template <typename Real>
+struct StepRand {
+    Real edt, r0, r1, r2;
+};
+
+template <int DV, typename Real, int SCHEME>
+__device__ __forceinline__ StepRand<Real> step_rand(const fm::FmTables& T, const WalkArgs& a, Real sq2dt,
+                                                    uint64_t w0, uint64_t w1, uint64_t w2) {
+    constexpr bool FAST = DV >= DV_RING_AN;
+    using Ops = RealOps<Real, FAST>;
+    StepRand<Real> r;
+    r.edt = Real(0);
+    r.r2 = Real(0);
+    if constexpr (SCHEME == 0 && FAST) {
+        // sqrt(2 dt) z = R (cs, sn)
+        Ops::bm_polar(T, w0, w1, sq2dt, r.r0, r.r1, r.r2);
+    } else if constexpr (SCHEME == 0) {
+        Ops::box_muller(T, w0, w1, r.r0, r.r1);
+    } else if constexpr (FAST && sizeof(Real) == 8) {
+        // step_exponential (sde.cpp:123-140), fp64 performance mode: edt =
+        // -ln u / lambda from the raw bits, one root for the radius
+        // sqrt(-2 ln u1) * sqrt(2 edt) = sqrt(-2 ln u1 * 2 edt)
+        r.edt = Ops::m2ln_open(T, w0) * Real(a.half_inv_lambda);
+        Ops::bm_polar_sq(T, w1, w2, Real(2) * r.edt, r.r0, r.r1, r.r2);
+    } else {
+        // step_exponential (sde.cpp:123-140): dt ~ Exp(lambda) first
+        r.edt = -Ops::lg(T, Ops::u_open(w0)) / Real(a.lambda);
+        const Real sv = Ops::sq(Real(2) * r.edt);
+        if constexpr (FAST) {  // fp32 (A/B: the fp64 form above is 10-18% slower here)
+            Ops::bm_polar(T, w1, w2, sv, r.r0, r.r1, r.r2);
+        } else {
+            Ops::box_muller(T, w1, w2, r.r0, r.r1);
+            r.r2 = sv;
+        }
+    }
+    return r;
+}
+
+// The drift of one step at (x, y): linear performance mode the scaled form
+// dt grad(w)/w = c (vx, vy) (drift_cv), otherwise (bx, by) = grad(w)/w;
+// ok false where the reference throws EvaluationError (non-finite drift).
+template <typename Real>
+struct StepDrift {
+    Real c, vx, vy;  // bx, by in vx, vy for the unscaled forms
+    bool ok;
+};
+
+template <int DV, typename Real, int SCHEME>
+__device__ __forceinline__ StepDrift<Real> step_drift(const fm::FmTables& T, const DensityParams& P, Real dt,
+                                                      Real x, Real y) {
+    StepDrift<Real> d;
+    if constexpr (SCHEME == 0 && DV >= DV_RING_AN) {
+        drift_cv<DV>(T, P, x, y, dt, d.c, d.vx, d.vy);
+        d.ok = true;  // closed forms: finite everywhere
+    } else {
+        d.c = Real(0);
+        d.ok = drift<DV, Real>(P, T, x, y, d.vx, d.vy);
+    }
+    return d;
+}
+
+// Euler-Maruyama update (step_linear, sde.cpp:21-29; step_exponential,
+// :123-140) from the step's drift and randoms.
+template <int DV, typename Real, int SCHEME>
+__device__ __forceinline__ void step_update(const StepDrift<Real>& d, const StepRand<Real>& r, Real dt,
+                                            Real sq2dt, Real x, Real y, Real& nxp, Real& nyp) {
+    constexpr bool FAST = DV >= DV_RING_AN;
+    if constexpr (SCHEME == 0 && FAST) {
+        // x + b dt + sqrt(2 dt) z with b dt = c v and sqrt(2 dt) z = R (cs, sn)
+        nxp = fma(r.r0, r.r2, fma(d.c, d.vx, x));
+        nyp = fma(r.r0, r.r1, fma(d.c, d.vy, y));
+    } else if constexpr (SCHEME == 0) {
+        nxp = x + d.vx * dt + sq2dt * r.r0;
+        nyp = y + d.vy * dt + sq2dt * r.r1;
+    } else if constexpr (FAST && sizeof(Real) == 8) {
+        nxp = fma(r.r0, r.r2, fma(d.vx, r.edt, x));
+        nyp = fma(r.r0, r.r1, fma(d.vy, r.edt, y));
+    } else if constexpr (FAST) {
+        nxp = x + d.vx * r.edt + r.r0 * r.r2;
+        nyp = y + d.vy * r.edt + r.r0 * r.r1;
+    } else {
+        nxp = x + d.vx * r.edt + r.r2 * r.r0;
+        nyp = y + d.vy * r.edt + r.r2 * r.r1;
+    }
+}
+
+// The inner-box test of the step loop: the integer high-word form in the
+// fp64 table kernels (performance mode), the exact one otherwise.
+template <int DV, typename Real>
+__device__ __forceinline__ bool box_test(const Dom<Real>& d, Real px, Real py) {
+    if constexpr (DV >= DV_RING_AN && sizeof(Real) == 8) return d.in_box_hi(px, py);
+    else return d.in_box(px, py);
+}
+
+// Exit test of the step (x, y) -> (nxp, nyp): explicit exit (segment_exit,
+// sde.cpp:31-65) or the scheme's edge-crossing draws (sde.cpp:72-121), from
+// the stream `rng` (the lane's own Philox stream in K1, the warp's window in
+// the tail kernel).  nb: whether (nxp, nyp) lies in the inner box.
+template <int DV, typename Real, int SCHEME, bool BRIDGE, typename Stream>
+__device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& a, const fm::FmTables& T,
+                                          Real thr, Real dt, Real x, Real y, Real nxp, Real nyp,
+                                          bool in_box, Stream& rng, Real& hx, Real& hy, int& edge,
+                                          bool& nb) {
+    constexpr bool FAST = DV >= DV_RING_AN;
+    bool exited = false;
+    nb = true;
+    if constexpr (SCHEME == 0 && BRIDGE) {
+        // inner box first: box inside the domain, so both ends in the
+        // box means no exit and no bridge draw (the common step)
+        nb = box_test<DV, Real>(dom, nxp, nyp);
+        if (!(nb && in_box)) {
+            if (!dom.inside(nxp, nyp)) {
+                segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+                exited = true;
+            } else {
+                // exact pre-filter: an edge draws only if d0*d1 <= 40 dt
+                const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
+                const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
+                const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
+                const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
+                if constexpr (FAST && sizeof(Real) == 4 &&
+                              (SDDG_FP32_BRIDGE_OOL_SHOCK || DV != DV_SHOCK_AN)) {
+                    // fp32: out of line (A/B +2.4%); fp64 keeps the inline test below
+                    // (out of line it costs the step loop a local-memory round trip: -0.5%)
+                    static_assert(sizeof(Stream) == sizeof(LaneStream), "fp32 runs in K1 only");
+                    const Real idt = Real(a.inv_dt);
+                    const int mask = int(!(pB * idt > Real(40))) | (int(!(pT * idt > Real(40))) << 1) |
+                                     (int(!(pL * idt > Real(40))) << 2) | (int(!(pR * idt > Real(40))) << 3);
+                    if (mask) {
+                        const BridgeRes r = bridge_rare<Real>(x, y, nxp, nyp, mask, rng, &a, &T);
+                        rng.n = r.n;
+                        rng.cw2 = r.cw2;
+                        rng.cw3 = r.cw3;
+                        if (r.edge >= 0) {
+                            hx = Real(r.hx);
+                            hy = Real(r.hy);
+                            edge = r.edge;
+                            exited = true;
+                        }
+                    }
+                } else if (pB <= thr || pT <= thr || pL <= thr || pR <= thr) {
+                    exited = edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T, rng, hx, hy, edge);
+                }
+            }
+        }
+    } else if (!dom.inside(nxp, nyp)) {
+        segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+        exited = true;
+    } else if constexpr (SCHEME == 1 && FAST && sizeof(Real) == 8) {
+        exited = bridge_exp_fast<Real, Stream>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx, hy, edge);
+    } else if constexpr (SCHEME == 1) {
+        exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx, hy, edge);
+    }
+    return exited;
+}
+
+// A walk's exit (run_walk, sde.cpp:170-177): boundary values at the exit
+// point (table_at, boundary.cpp:10-42), the walk record (or per-path dump)
+// at slot g, and its path-steps over all epochs into the node's counter.
+template <typename Real>
+__device__ __forceinline__ void record_exit(const WalkArgs& a, uint64_t g, uint32_t node, uint32_t epoch,
+                                            uint32_t step, int edge, Real hx, Real hy) {
+    const double dhx = static_cast<double>(hx), dhy = static_cast<double>(hy);
+    const bool horiz = edge < 2;
+    const double par = horiz ? (dhx - a.txmin) / a.thx : (dhy - a.tymin) / a.thy;
+    const int tn = horiz ? a.tnx : a.tny;
+    const double fv = table_at(a.tf[edge], tn, par);
+    const double gv = table_at(a.tg[edge], tn, par);
+    // restarts happen at exactly max_steps: one atomic per finished walk
+    if (a.node_steps)
+        atomicAdd(a.node_steps + node, static_cast<unsigned long long>(epoch) * a.max_steps32 + step);
+    if (a.dump) {
+        sddg_path& r = a.dump[g];
+        r.f = fv;
+        r.g = gv;
+        r.ex = dhx;
+        r.ey = dhy;
+        r.steps = step;
+        r.epoch = static_cast<int32_t>(epoch);
+        r.edge = edge;
+    } else {
+        a.rec_f[g] = fv;
+        a.rec_g[g] = gv;
+        a.rec_meta[g] = static_cast<uint32_t>(edge) | (epoch << 2);
+    }
+}
+
 // Launch shape per variant.  Performance-mode fp64 reads the fastmath tables
 // from shared memory; with the large tables (64 KB) one CTA fills an SM:
 // 1024 threads at 64 registers, or 640 at 96 for the register-hungrier
@@ -401,9 +607,10 @@ __host__ __device__ constexpr int walk_min_blocks() {
         return SDDG_WALK_TABLE_BLOCKS_PER_SM;
 #endif
     if constexpr (walk_uses_tables<DV, Real>() && kBigTables) return 1;
-#ifdef SDDG_SHOCK32_MIN_BLOCKS
-    if constexpr (DV == DV_SHOCK_AN && sizeof(Real) == 4) return SDDG_SHOCK32_MIN_BLOCKS;
+#ifndef SDDG_SHOCK32_MIN_BLOCKS
+#define SDDG_SHOCK32_MIN_BLOCKS 7  // 7 x 128 threads per SM: ptxas keeps the shock fp32 loop <= 72 registers
 #endif
+    if constexpr (DV == DV_SHOCK_AN && sizeof(Real) == 4) return SDDG_SHOCK32_MIN_BLOCKS;
     return (walk_heavy_drift<DV>() || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
 }
 
@@ -421,11 +628,6 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
     const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax),
                         Real(a.box[0]), Real(a.box[1]), Real(a.box[2]), Real(a.box[3]),
                         a.box_hi[0], a.box_hi[1], a.box_hi[2], a.box_hi[3]};
-    // the inner-box test used by the step loop
-    auto box_test = [&](Real px, Real py) {
-        if constexpr (walk_uses_tables<DV, Real>()) return dom.in_box_hi(px, py);
-        else return dom.in_box(px, py);
-    };
     const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab};
     const Real dt = Real(a.dt);
     const Real sq2dt = Real(a.sqrt2dt);
@@ -479,59 +681,30 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             rng.init(a.pid[node], L.walk, 0);
         };
         start_walk(L.g);
-        bool in_box = box_test(x, y);
+        bool in_box = box_test<DV, Real>(dom, x, y);
         uint32_t step = 0;
+        // steps between handoff check points (max_steps when the tail
+        // kernel is off: the restart compare the loop always had)
+        const uint32_t walk_lim =
+            kTailHandoff<Real> && a.cont && kHandoffCheck < max_steps ? kHandoffCheck : max_steps;
+        uint32_t lim = walk_lim;
         SDDG_UNROLL(SDDG_WALK_UNROLL)  // 2: step copies alternate x, y registers (no loop-carried moves)
         for (;;) {
-            // ---- one step
-            Real bx, by, nxp, nyp, z0, z1;
-            bool ok;
-            if constexpr (SCHEME == 0 && FAST) {
-                // x + b dt + sqrt(2 dt) z with b dt = c v and sqrt(2 dt) z = R (cs, sn)
-                Real c, vx, vy, R, sn, cs;
-                drift_cv<DV>(T, P, x, y, dt, c, vx, vy);
-                ok = true;  // closed forms: finite everywhere
-                uint64_t ua, ub;
-                rng.next_pair(a.rk, ua, ub);
-                Ops::bm_polar(T, ua, ub, sq2dt, R, sn, cs);
-                nxp = fma(R, cs, fma(c, vx, x));
-                nyp = fma(R, sn, fma(c, vy, y));
-            } else if constexpr (SCHEME == 0) {
-                ok = drift<DV, Real>(P, T, x, y, bx, by);
-                uint64_t ua, ub;
-                rng.next_pair(a.rk, ua, ub);
-                Ops::box_muller(T, ua, ub, z0, z1);
-                nxp = x + bx * dt + sq2dt * z0;
-                nyp = y + by * dt + sq2dt * z1;
-            } else if constexpr (FAST && sizeof(Real) == 8) {
-                // step_exponential (sde.cpp:123-140), fp64 performance mode: edt =
-                // -ln u / lambda from the raw bits, one root for the radius
-                // sqrt(-2 ln u1) * sqrt(2 edt) = sqrt(-2 ln u1 * 2 edt)
-                const Real edt = Ops::m2ln_open(T, rng.next_one(a.rk)) * Real(a.half_inv_lambda);
-                ok = drift<DV, Real>(P, T, x, y, bx, by);
-                uint64_t ua, ub;
-                rng.next_pair(a.rk, ua, ub);
-                Real R, sn, cs;
-                Ops::bm_polar_sq(T, ua, ub, Real(2) * edt, R, sn, cs);
-                nxp = fma(R, cs, fma(bx, edt, x));
-                nyp = fma(R, sn, fma(by, edt, y));
-            } else {
-                // step_exponential (sde.cpp:123-140): dt ~ Exp(lambda) first
-                const Real edt = -Ops::lg(T, Ops::u_open(rng.next_one(a.rk))) / Real(a.lambda);
-                ok = drift<DV, Real>(P, T, x, y, bx, by);
-                uint64_t ua, ub;
-                rng.next_pair(a.rk, ua, ub);
-                const Real s = Ops::sq(Real(2) * edt);
-                if constexpr (FAST) {  // fp32 (A/B: the fp64 form above is 10-18% slower here)
-                    Real R, sn, cs;
-                    Ops::bm_polar(T, ua, ub, s, R, sn, cs);
-                    nxp = x + bx * edt + R * cs;
-                    nyp = y + by * edt + R * sn;
+            // ---- one step (step_drift, step_rand, step_update: shared with the
+            // tail kernel so both compute every step bit for bit alike)
+            const StepDrift<Real> sd = step_drift<DV, Real, SCHEME>(T, P, dt, x, y);
+            const bool ok = sd.ok;
+            Real nxp, nyp;
+            {
+                uint64_t w0, w1, w2 = 0;
+                if constexpr (SCHEME == 0) {
+                    rng.next_pair(a.rk, w0, w1);
                 } else {
-                    Ops::box_muller(T, ua, ub, z0, z1);
-                    nxp = x + bx * edt + s * z0;
-                    nyp = y + by * edt + s * z1;
+                    w0 = rng.next_one(a.rk);
+                    rng.next_pair(a.rk, w1, w2);
                 }
+                const StepRand<Real> r = step_rand<DV, Real, SCHEME>(T, a, sq2dt, w0, w1, w2);
+                step_update<DV, Real, SCHEME>(sd, r, dt, sq2dt, x, y, nxp, nyp);
             }
             ++step;
             if (!ok) {
@@ -539,66 +712,40 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 atomicExch(a.err_info, static_cast<unsigned long long>(a.pid[L.node]));
                 break;
             }
-            bool exited = false;
             Real hx = Real(0), hy = Real(0);
             int edge = 0;
-            bool nb = true;
-            if constexpr (SCHEME == 0 && BRIDGE) {
-                // inner box first: box inside the domain, so both ends in the
-                // box means no exit and no bridge draw (the common step)
-                nb = box_test(nxp, nyp);
-                if (!(nb && in_box)) {
-                    if (!dom.inside(nxp, nyp)) {
-                        segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
-                        exited = true;
-                    } else {
-                        // exact pre-filter: an edge draws only if d0*d1 <= 40 dt
-                        const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
-                        const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
-                        const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
-                        const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
-                        if constexpr (FAST && sizeof(Real) == 4 &&
-                                      (SDDG_FP32_BRIDGE_OOL_SHOCK || DV != DV_SHOCK_AN)) {
-                            // fp32: out of line (A/B +2.4%); fp64 keeps the inline test below
-                            // (out of line it costs the step loop a local-memory round trip: -0.5%)
-                            const Real idt = Real(a.inv_dt);
-                            const int mask = int(!(pB * idt > Real(40))) |
-                                             (int(!(pT * idt > Real(40))) << 1) |
-                                             (int(!(pL * idt > Real(40))) << 2) |
-                                             (int(!(pR * idt > Real(40))) << 3);
-                            if (mask) {
-                                const BridgeRes r = bridge_rare<Real>(x, y, nxp, nyp, mask, rng, &a, &T);
-                                rng.n = r.n;
-                                rng.cw2 = r.cw2;
-                                rng.cw3 = r.cw3;
-                                if (r.edge >= 0) {
-                                    hx = Real(r.hx);
-                                    hy = Real(r.hy);
-                                    edge = r.edge;
-                                    exited = true;
-                                }
-                            }
-                        } else if (pB <= thr || pT <= thr || pL <= thr || pR <= thr) {
-                            exited = edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T,
-                                                                  rng, hx, hy, edge);
-                        }
-                    }
-                }
-            } else if (!dom.inside(nxp, nyp)) {
-                segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
-                exited = true;
-            } else if constexpr (SCHEME == 1 && FAST && sizeof(Real) == 8) {
-                exited = bridge_exp_fast<Real>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx,
-                                               hy, edge);
-            } else if constexpr (SCHEME == 1) {
-                exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T,
-                                                      rng, hx, hy, edge);
-            }
+            bool nb;
+            const bool exited = exit_test<DV, Real, SCHEME, BRIDGE>(dom, a, T, thr, dt, x, y, nxp, nyp, in_box,
+                                                                    rng, hx, hy, edge, nb);
             if (!exited) {
                 x = nxp;
                 y = nyp;
                 in_box = nb;
-                if (step < max_steps) continue;
+                if (step < (kTailHandoff<Real> ? lim : max_steps)) continue;
+                if (kTailHandoff<Real> && step < max_steps) {
+                    // handoff check point (tail kernel enabled): once the batch
+                    // counter has run out and few walks remain, the walk moves to
+                    // the tail kernel, which runs it on a whole warp at a fraction
+                    // of a lane's step latency (walk_tail.cuh)
+                    lim = max_steps - step > kHandoffCheck ? step + kHandoffCheck : max_steps;
+                    if (*reinterpret_cast<volatile unsigned long long*>(a.next) >= a.total &&
+                        *reinterpret_cast<volatile unsigned long long*>(a.live) <= a.cont_cap) {
+                        const uint32_t k = atomicAdd(a.n_cont, 1u);
+                        if (k < a.cont_cap) {
+                            WalkCont& c = a.cont[k];
+                            c.x = static_cast<double>(x);
+                            c.y = static_cast<double>(y);
+                            c.g = L.g;
+                            c.node = L.node;
+                            c.walk = L.walk;
+                            c.epoch = L.epoch;
+                            c.step = step;
+                            c.n = rng.n;
+                            break;
+                        }
+                    }
+                    continue;
+                }
                 // max_steps reached: restart on the next epoch's stream
                 L.steps += step;
                 const uint32_t epoch = ++L.epoch;
@@ -611,44 +758,24 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 rng.init(a.pid[node], L.walk, epoch);
                 x = Real(a.px[node]);
                 y = Real(a.py[node]);
-                in_box = box_test(x, y);
+                in_box = box_test<DV, Real>(dom, x, y);
                 step = 0;
+                lim = walk_lim;
                 continue;
             }
             // ---- exit: boundary values, record, next walk
-            const double dhx = static_cast<double>(hx), dhy = static_cast<double>(hy);
-            const bool horiz = edge < 2;
-            const double par = horiz ? (dhx - a.txmin) / a.thx : (dhy - a.tymin) / a.thy;
-            const int tn = horiz ? a.tnx : a.tny;
-            const double fv = table_at(a.tf[edge], tn, par);
-            const double gv = table_at(a.tg[edge], tn, par);
             L.steps += step;
-            // per-node path-steps of this walk, all epochs (restarts happen at
-            // exactly max_steps): one atomic per finished walk
-            if (a.node_steps)
-                atomicAdd(a.node_steps + L.node,
-                          static_cast<unsigned long long>(L.epoch) * max_steps + step);
-            const uint64_t g = L.g;
-            if (a.dump) {
-                sddg_path& r = a.dump[g];
-                r.f = fv;
-                r.g = gv;
-                r.ex = dhx;
-                r.ey = dhy;
-                r.steps = step;
-                r.epoch = static_cast<int32_t>(L.epoch);
-                r.edge = edge;
-            } else {
-                a.rec_f[g] = fv;
-                a.rec_g[g] = gv;
-                a.rec_meta[g] = static_cast<uint32_t>(edge) | (L.epoch << 2);
-            }
+            record_exit<Real>(a, L.g, L.node, L.epoch, step, edge, hx, hy);
             const uint64_t gn = atomicAdd(a.next, 1ull);
-            if (gn >= a.total) break;
+            if (gn >= a.total) {
+                if (kTailHandoff<Real> && a.cont) atomicAdd(a.live, ~0ull);  // one walk fewer in flight (-1)
+                break;
+            }
             L.g = gn;
             start_walk(gn);
-            in_box = box_test(x, y);
+            in_box = box_test<DV, Real>(dom, x, y);
             step = 0;
+            lim = walk_lim;
         }
     }
     uint64_t my_steps = L.steps;
@@ -687,11 +814,26 @@ cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+}  // namespace sddg
+
+#include "walk_tail.cuh"
+
+namespace sddg {
+
+// K1, then (fp64 with a handoff buffer) the tail kernel on the same stream
 template <int DV, typename Real>
 cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
-    if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false>(a, grid, s);
-    if (a.bridge) return launch_one<DV, Real, 0, true>(a, grid, s);
-    return launch_one<DV, Real, 0, false>(a, grid, s);
+    cudaError_t e;
+    if (a.scheme == SDDG_SCHEME_EXPONENTIAL) e = launch_one<DV, Real, 1, false>(a, grid, s);
+    else if (a.bridge) e = launch_one<DV, Real, 0, true>(a, grid, s);
+    else e = launch_one<DV, Real, 0, false>(a, grid, s);
+    if constexpr (kTailHandoff<Real>) {
+        if (e != cudaSuccess || !a.cont) return e;
+        if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_tail_one<DV, Real, 1, false>(a, s);
+        if (a.bridge) return launch_tail_one<DV, Real, 0, true>(a, s);
+        return launch_tail_one<DV, Real, 0, false>(a, s);
+    }
+    return e;
 }
 
 // CTAs per SM and threads per CTA of the variant's bridge-test kernel
