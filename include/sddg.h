@@ -160,6 +160,11 @@ const char* sddg_last_error(const sddg_ctx* ctx);
 sddg_status sddg_last_stats(const sddg_ctx* ctx, int64_t* path_steps, int64_t* launches,
                             double* kernel_ms);
 
+/* The walk batch's tail: walks handed from the walk kernel K1 to the tail
+ * kernel (one warp per walk, fp64 only) and the tail kernel's device time of
+ * the last walk call (included in sddg_last_stats' kernel time). */
+sddg_status sddg_last_tail_stats(const sddg_ctx* ctx, int64_t* handoffs, double* tail_ms);
+
 /* Measured non-tensor FMA peak of this device in TFLOP/s (independent
  * DFMA / FFMA chains on every SM), the denominator of the walk kernel's
  * pipe roofline. */

@@ -434,7 +434,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     a.rec_meta = rm;
     int64_t launches = 0;
     const size_t nbatch = static_cast<size_t>((n + npb - 1) / npb);
-    while (c->bev.size() < 2 * nbatch) {
+    while (c->bev.size() < 3 * nbatch) {
         cudaEvent_t e;
         ck(cudaEventCreate(&e), "event");
         c->bev.push_back(e);
@@ -451,22 +451,28 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
         set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaGetLastError(), "set_next");
-        ck(cudaEventRecord(c->bev[2 * bi], st), "event");
+        ck(cudaEventRecord(c->bev[3 * bi], st), "event");
         ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
-        ck(cudaEventRecord(c->bev[2 * bi + 1], st), "event");
+        ck(cudaEventRecord(c->bev[3 * bi + 1], st), "event");
+        ck(launch_walk_tail(dv, a, st), "tail kernel launch");
+        ck(cudaEventRecord(c->bev[3 * bi + 2], st), "event");
         ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, nst, d_out, st, gt ? *gt : none), "reduce launch");
         launches += a.cont ? 4 : 3;
     }
     Counters hc;
     ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "read counters");
     ck(cudaStreamSynchronize(st), "walk kernels");
-    double tot_ms = 0.0;
+    double tot_ms = 0.0, tail_ms = 0.0;
     for (size_t k = 0; k < nbatch; ++k) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->bev[2 * k], c->bev[2 * k + 1]);
+        float ms = 0.f, ms_t = 0.f;
+        cudaEventElapsedTime(&ms, c->bev[3 * k], c->bev[3 * k + 2]);
+        cudaEventElapsedTime(&ms_t, c->bev[3 * k + 1], c->bev[3 * k + 2]);
         tot_ms += ms;
+        tail_ms += ms_t;
     }
     c->last_ms = tot_ms;
+    c->last_tail_ms = a.cont ? tail_ms : 0.0;
+    c->last_handoffs = a.cont ? std::min<int64_t>(hc.n_cont, a.cont_cap) : 0;
     c->last_steps = static_cast<int64_t>(hc.steps);
     c->last_launches = launches;
     raise_kernel_error(hc);
@@ -1256,6 +1262,12 @@ cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cuda
     return launch_walk_ref(dv, a, grid, s);
 }
 
+cudaError_t launch_walk_tail(int dv, const WalkArgs& a, cudaStream_t s) {
+    if (!a.cont) return cudaSuccess;
+    if (dv >= 32) return launch_walk_tail_fast(dv, a, s);
+    return launch_walk_tail_ref(dv, a, s);
+}
+
 cudaError_t walk_occupancy(int dv, int precision, int* b, int* block) {
     if (!walk_variant_supported(dv, precision)) return cudaErrorInvalidValue;
     if (dv >= 32) return occupancy_walk_fast(dv, precision, b, block);
@@ -1329,6 +1341,13 @@ sddg_status sddg_last_stats(const sddg_ctx* c, int64_t* steps, int64_t* launches
     if (steps) *steps = c->last_steps;
     if (launches) *launches = c->last_launches;
     if (ms) *ms = c->last_ms;
+    return SDDG_OK;
+}
+
+sddg_status sddg_last_tail_stats(const sddg_ctx* c, int64_t* handoffs, double* tail_ms) {
+    if (!c) return SDDG_ERR_VALIDATION;
+    if (handoffs) *handoffs = c->last_handoffs;
+    if (tail_ms) *tail_ms = c->last_tail_ms;
     return SDDG_OK;
 }
 
@@ -1433,6 +1452,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaEventRecord(ctx->ev0, st), "event");
         ck(launch_walk(dv, cfg->precision, a, grid, st), "walk kernel launch");
+        ck(launch_walk_tail(dv, a, st), "tail kernel launch");
         ck(cudaEventRecord(ctx->ev1, st), "event");
         Counters hc;
         ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "d2h");
@@ -1443,6 +1463,8 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         ctx->last_ms = ms;
         ctx->last_steps = static_cast<int64_t>(hc.steps);
         ctx->last_launches = a.cont ? 3 : 2;
+        ctx->last_handoffs = a.cont ? std::min<int64_t>(hc.n_cont, a.cont_cap) : 0;
+        ctx->last_tail_ms = 0.0;
         raise_kernel_error(hc);
     }
     API_END(ctx)

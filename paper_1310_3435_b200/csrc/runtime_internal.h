@@ -92,8 +92,8 @@ struct sddg_ctx {
     sddg::rt::DevBuf rec_f, rec_g, rec_meta, nodes, est, tables, counters, dump, perm, nsteps;
     sddg::rt::DevBuf s_w, s_jobs, s_bc, s_u, s_info, s_coef, s_err, s_large, s_omega, s_perm;
     sddg::rt::DevBuf m_in, m_out, m_q, m_misc;
-    int64_t last_steps = 0, last_launches = 0;
-    double last_ms = 0.0;
+    int64_t last_steps = 0, last_launches = 0, last_handoffs = 0;
+    double last_ms = 0.0, last_tail_ms = 0.0;
     std::map<int, std::pair<int, int>> occ;  // (dv*2+prec) -> (CTAs per SM, threads per CTA)
     std::vector<cudaEvent_t> bev;  // per-batch walk-kernel events
     sddg::rt::DevBuf fm_tables;    // fastmath.cuh FmTables (performance mode)

@@ -75,6 +75,10 @@ void make_fm_tables(void* host_tables7680);
 // walk_ref.cu (fp64, -fmad=false) and walk_fast.cu (analytic drifts, fp64 + fp32)
 bool walk_variant_supported(int dv, int precision);
 cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
+// the tail kernel of an fp64 walk batch (walk_tail.cuh), after launch_walk
+cudaError_t launch_walk_tail(int dv, const WalkArgs& a, cudaStream_t s);
+cudaError_t launch_walk_tail_ref(int dv, const WalkArgs& a, cudaStream_t s);
+cudaError_t launch_walk_tail_fast(int dv, const WalkArgs& a, cudaStream_t s);
 cudaError_t walk_occupancy(int dv, int precision, int* blocks_per_sm, int* block);
 // the two TUs' own dispatchers
 cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s);

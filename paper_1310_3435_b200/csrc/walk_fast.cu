@@ -19,6 +19,15 @@ cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid,
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_walk_tail_fast(int dv, const WalkArgs& a, cudaStream_t s) {
+    switch (dv) {
+#define X(V) case V: return launch_tail_variant<V, double>(a, s);
+        SDDG_FAST_VARIANTS(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t occupancy_walk_fast(int dv, int precision, int* b, int* block) {
     switch (dv) {
 #define X(V) case V: return precision == SDDG_FP64 ? occupancy_variant<V, double>(b, block) \

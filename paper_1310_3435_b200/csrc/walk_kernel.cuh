@@ -820,20 +820,22 @@ cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
 
 namespace sddg {
 
-// K1, then (fp64 with a handoff buffer) the tail kernel on the same stream
 template <int DV, typename Real>
 cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
-    cudaError_t e;
-    if (a.scheme == SDDG_SCHEME_EXPONENTIAL) e = launch_one<DV, Real, 1, false>(a, grid, s);
-    else if (a.bridge) e = launch_one<DV, Real, 0, true>(a, grid, s);
-    else e = launch_one<DV, Real, 0, false>(a, grid, s);
+    if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false>(a, grid, s);
+    if (a.bridge) return launch_one<DV, Real, 0, true>(a, grid, s);
+    return launch_one<DV, Real, 0, false>(a, grid, s);
+}
+
+// The tail kernel after K1 on the same stream (fp64, a.cont set)
+template <int DV, typename Real>
+cudaError_t launch_tail_variant(const WalkArgs& a, cudaStream_t s) {
     if constexpr (kTailHandoff<Real>) {
-        if (e != cudaSuccess || !a.cont) return e;
         if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_tail_one<DV, Real, 1, false>(a, s);
         if (a.bridge) return launch_tail_one<DV, Real, 0, true>(a, s);
         return launch_tail_one<DV, Real, 0, false>(a, s);
     }
-    return e;
+    return cudaErrorInvalidValue;
 }
 
 // CTAs per SM and threads per CTA of the variant's bridge-test kernel

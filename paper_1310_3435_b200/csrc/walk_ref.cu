@@ -21,6 +21,15 @@ cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s)
     return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_walk_tail_ref(int dv, const WalkArgs& a, cudaStream_t s) {
+    switch (dv) {
+#define X(V) case V: return launch_tail_variant<V, double>(a, s);
+        SDDG_REF_VARIANTS(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t occupancy_walk_ref(int dv, int* b, int* block) {
     switch (dv) {
 #define X(V) case V: return occupancy_variant<V, double>(b, block);

@@ -240,7 +240,10 @@ class Context:
     def last_stats(self):
         s, n, ms = C.c_int64(), C.c_int64(), C.c_double()
         _check(lib().sddg_last_stats(self._h, C.byref(s), C.byref(n), C.byref(ms)), self._h)
-        return {"path_steps": s.value, "launches": n.value, "kernel_ms": ms.value}
+        h, tms = C.c_int64(), C.c_double()
+        _check(lib().sddg_last_tail_stats(self._h, C.byref(h), C.byref(tms)), self._h)
+        return {"path_steps": s.value, "launches": n.value, "kernel_ms": ms.value,
+                "tail_handoffs": h.value, "tail_ms": tms.value}
 
 
 _default_ctx = {}
