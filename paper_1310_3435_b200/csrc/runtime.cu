@@ -235,6 +235,11 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
         a.box_hi[k] = static_cast<int32_t>(bits >> 32);
     }
     if (!pos) a.box_hi[0] = a.box_hi[2] = INT32_MAX;
+    const double dv[8] = {a.xmin, a.xmax, a.ymin, a.ymax, a.box[0], a.box[1], a.box[2], a.box[3]};
+    for (int k = 0; k < 8; ++k) a.f_dom[k] = static_cast<float>(dv[k]);
+    a.f_dt = static_cast<float>(a.dt);
+    a.f_sqrt2dt = static_cast<float>(a.sqrt2dt);
+    a.f_thr = static_cast<float>(a.bridge_thr);
     a.seed = cfg.seed;
     a.rk = make_round_keys(cfg.seed);
     a.max_steps32 = static_cast<uint32_t>(cfg.max_steps);  // <= 2^29 (validate_walk)
@@ -375,11 +380,24 @@ void raise_kernel_error(const Counters& hc) {
 }
 
 // The tail kernel (walk_tail.cuh) for fp64 walks: a handoff buffer of one
-// walk per warp of one 16-warp CTA per SM.  SDDG_NO_TAIL=1: K1 alone.
-void enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt) {
+// walk per warp of one 16-warp CTA per SM, for batches of at most
+// kTailWalksPerLane walks per K1 lane (larger batches, whose tail is a small
+// share, keep the plain K1 loop: 1.5 instructions per step fewer).
+// SDDG_NO_TAIL=1: K1 alone.
+constexpr uint64_t kTailWalksPerLane = 32;
+
+void enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt, uint64_t lanes) {
     a.cont = nullptr;
     a.cont_cap = 0;
+    a.chunk32 = a.max_steps32;
     if (precision != SDDG_FP64 || std::getenv("SDDG_NO_TAIL")) return;
+    if (a.total > kTailWalksPerLane * lanes) return;
+    // K1's check points every chunk32 steps: the largest of 256, 128, 64
+    // dividing max_steps (the restart must still fall on a chunk end)
+    uint32_t chunk = 256;
+    while (chunk >= 64 && a.max_steps32 % chunk != 0) chunk /= 2;
+    if (chunk < 64 || chunk >= a.max_steps32) return;
+    a.chunk32 = chunk;
     const uint32_t cap = static_cast<uint32_t>(c->sms) * 16u;
     a.cont = static_cast<WalkCont*>(c->tail_cont.ensure(sizeof(WalkCont) * cap));
     a.cont_cap = cap;
@@ -420,7 +438,6 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     WalkArgs a;
     fill_args(a, d, dom, bd, cfg, dtab);
     a.tab = upload_density(c, d);
-    enable_tail(c, a, cfg.precision, cnt);
     a.fm_tables = c->fm_tables.p;
     a.walks = W;
     a.walk_lo = 0;
@@ -449,6 +466,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         a.total = static_cast<uint64_t>(nb) * W;
         const auto [grid, blk] = walk_grid(c, dv, cfg.precision, a.total);
         const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
+        enable_tail(c, a, cfg.precision, cnt, lanes);
         set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaGetLastError(), "set_next");
         ck(cudaEventRecord(c->bev[3 * bi], st), "event");
@@ -1446,9 +1464,9 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         a.err_flag = &cnt->err_flag;
         a.err_info = &cnt->err_info;
         a.dump = dd;
-        enable_tail(ctx, a, cfg->precision, cnt);
         const auto [grid, blk] = walk_grid(ctx, dv, cfg->precision, a.total);
         const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
+        enable_tail(ctx, a, cfg->precision, cnt, lanes);
         set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaEventRecord(ctx->ev0, st), "event");
         ck(launch_walk(dv, cfg->precision, a, grid, st), "walk kernel launch");

@@ -36,10 +36,16 @@ struct WalkArgs {
     int scheme, bridge;
     double dt, sqrt2dt, lambda, nu2, bridge_thr;
     double box[4];  // inner box x0, x1, y0, y1 (edge distances > sqrt(bridge_thr))
+    // fp32 copies (fp32 walks read them from the constant bank instead of
+    // converting the doubles in the step loop): xmin, xmax, ymin, ymax, box[4],
+    // dt, sqrt2dt, bridge_thr
+    float f_dom[8];
+    float f_dt, f_sqrt2dt, f_thr, f_pad;
     int32_t box_hi[4];  // high words of box[] for the integer test (INT32_MAX: disabled)
     uint64_t seed;
     RoundKeys rk;
     uint32_t max_steps32;  // max_steps (validated <= 2^29)
+    uint32_t chunk32;      // steps between K1 check points: max_steps, or (tail kernel) a divisor of it
     // batch: total = n_nodes * walks
     const double* px;
     const double* py;
@@ -101,7 +107,8 @@ struct WalkCont {
 struct LaneState {
     uint64_t g;       // record slot of the running walk
     uint64_t steps;   // path steps finished by this lane
-    uint32_t node, walk, epoch, pad;
+    uint32_t node, walk, epoch;
+    uint32_t base;    // steps of the completed chunks of this epoch
 };
 struct GatherTargets {
     int n_peers;                     // 0: no fused gather

@@ -153,7 +153,44 @@ __device__ __forceinline__ double sor_point(const double2 ew, const double2 ns, 
     return fma(omega, gs - uc, uc);
 }
 
-template <int METHOD, int PTS, int G = 1>
+// ---- bulk copies (K3s): cp.async.bulk global -> shared, completion on an
+// mbarrier (transaction bytes), one elected thread issuing
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "SDDG_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra SDDG_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// K3s ring: per stage the (aE, aW) and (aN, aS) pairs of kStreamChunk slots
+// of one colour, streamed from the job's packed weights in global memory
+// (L2-resident) while the previous stage is being swept.
+constexpr int kStreamChunk = 1024;  // slots per stage (a multiple of kSolveThreads)
+constexpr size_t kStreamRingBytes = 2 * 2 * kStreamChunk * sizeof(double2);
+
+template <int METHOD, int PTS, int G = 1, bool STREAM = false>
 __global__ void __launch_bounds__(kSolveThreads)
 solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
              const SolveJob* __restrict__ jobs, const double* __restrict__ bc, double tol,
@@ -233,6 +270,39 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     // initial guess (detsolver.cpp:121-148)
     for (int c = tid; c < N; c += nt)
         u[c] = initial_value(c % nx, c / nx, nx, ny, B, T, L, Rt, bmin, bmax, init_blend);
+    // K3s: the ring after u, its two mbarriers, and the first two chunks
+    __shared__ uint64_t bars[2];
+    double2* ring = reinterpret_cast<double2*>(smem + ((N + 1) & ~1));
+    const int nchunk = (nslots + kStreamChunk - 1) / kStreamChunk;
+    const double2* PQg = reinterpret_cast<const double2*>(cE);
+    int64_t kc = 0;  // chunks consumed so far (all sweeps): stage kc & 1, phase (kc >> 1) & 1
+    auto issue_chunk = [&](int64_t k, int stage) {
+        const int seq = static_cast<int>(k % (2 * nchunk));
+        const int colour = seq / nchunk, cix = seq - colour * nchunk;
+        const int q0 = cix * kStreamChunk;
+        const int cnt = min(kStreamChunk, nslots - q0);
+        const uint32_t bytes = static_cast<uint32_t>(cnt) * sizeof(double2);
+        const double2* src = PQg + colour * 2 * nslots + q0;
+        double2* dst = ring + stage * 2 * kStreamChunk;
+        mbar_expect_tx(&bars[stage], 2 * bytes);
+        bulk_g2s(dst, src, bytes, &bars[stage]);
+        bulk_g2s(dst + kStreamChunk, src + nslots, bytes, &bars[stage]);
+    };
+    if constexpr (STREAM) {
+        // the packed weights were written through the generic proxy: order
+        // them before the bulk copies (async proxy) read them
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (tid == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+            issue_chunk(0, 0);
+            issue_chunk(1, 1);
+        }
+    }
     __syncthreads();
 
     const int64_t max_iters =
@@ -273,6 +343,44 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
             for (int k = 0; k < PTS; ++k) {
                 const int p = tid + k * nt;
                 if (p < mi * mj) u[(p / mi + 1) * nx + (p % mi + 1)] = nu[k];
+            }
+        } else if constexpr (STREAM) {
+            // K3s: the packed weights stream through a two-stage shared-memory
+            // ring (cp.async.bulk, one elected thread; mbarrier completion),
+            // kStreamChunk slots of one colour per stage; thread t sweeps
+            // slots t, t + nt, ... of each chunk in order
+#pragma unroll 1
+            for (int colour = 0; colour < 2; ++colour) {
+                int j = j_first, sl = s_first;
+#pragma unroll 1
+                for (int cix = 0; cix < nchunk; ++cix, ++kc) {
+                    const int stage = static_cast<int>(kc & 1);
+                    mbar_wait(&bars[stage], static_cast<uint32_t>((kc >> 1) & 1));
+                    const double2* P = ring + stage * 2 * kStreamChunk;
+                    const double2* Q = P + kStreamChunk;
+                    const int lim = nslots - cix * kStreamChunk;
+#pragma unroll 2
+                    for (int q = tid; q < kStreamChunk && q < lim; q += nt) {
+                        const int i = 2 * sl + 1 + ((j + 1 + colour) & 1);
+                        if (i <= mi) {
+                            const int c = j * nx + i;
+                            const double uc = u[c];
+                            const double nv = sor_point(P[q], Q[q], u[c + 1], u[c - 1], u[c + nx], u[c - nx], uc,
+                                                        omega);
+                            const double du = fabs(nv - uc);
+                            lupd = lupd < du ? du : lupd;
+                            u[c] = nv;
+                        }
+                        sl += ds;
+                        j += dj;
+                        if (sl >= half) {
+                            sl -= half;
+                            ++j;
+                        }
+                    }
+                    __syncthreads();  // stage consumed; the colour's points published
+                    if (tid == 0) issue_chunk(kc + 2, stage);
+                }
             }
         } else {
 #pragma unroll 1
@@ -323,6 +431,11 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
             conv = true;
             break;
         }
+    }
+    if constexpr (STREAM) {
+        // the two chunks still in flight land before the CTA leaves
+        mbar_wait(&bars[kc & 1], static_cast<uint32_t>((kc >> 1) & 1));
+        mbar_wait(&bars[(kc + 1) & 1], static_cast<uint32_t>(((kc + 1) >> 1) & 1));
     }
     __syncthreads();
     // maximum principle (detsolver.cpp:191-198) and write-out

@@ -28,8 +28,6 @@
 #include "philox.cuh"
 #include "sddg_internal.h"
 
-// steps between the walk kernel's handoff checks (tail kernel enabled)
-constexpr uint32_t kHandoffCheck = 256;
 // fp64 walks hand their batch tail to the tail kernel; fp32 walks (config 3's
 // huge batches, whose tail is a small share) keep the 72-register loop
 template <typename Real>
@@ -174,6 +172,22 @@ struct Dom {
         hy = clampr(hy, ymin, ymax);
     }
 };
+
+// Walk parameters in the walk's precision: fp32 walks take the host-rounded
+// float copies (constant-bank operands, no conversion in the step loop)
+template <typename Real>
+__device__ __forceinline__ Real walk_prm(double d, float f) {
+    if constexpr (sizeof(Real) == 4) return f;
+    else return d;
+}
+template <typename Real>
+__device__ __forceinline__ Dom<Real> walk_dom(const WalkArgs& a) {
+    return Dom<Real>{walk_prm<Real>(a.xmin, a.f_dom[0]), walk_prm<Real>(a.xmax, a.f_dom[1]),
+                     walk_prm<Real>(a.ymin, a.f_dom[2]), walk_prm<Real>(a.ymax, a.f_dom[3]),
+                     walk_prm<Real>(a.box[0], a.f_dom[4]), walk_prm<Real>(a.box[1], a.f_dom[5]),
+                     walk_prm<Real>(a.box[2], a.f_dom[6]), walk_prm<Real>(a.box[3], a.f_dom[7]),
+                     a.box_hi[0], a.box_hi[1], a.box_hi[2], a.box_hi[3]};
+}
 
 // segment_exit (proj/src/sde.cpp:31-65)
 template <typename Real>
@@ -551,7 +565,7 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
 // at slot g, and its path-steps over all epochs into the node's counter.
 template <typename Real>
 __device__ __forceinline__ void record_exit(const WalkArgs& a, uint64_t g, uint32_t node, uint32_t epoch,
-                                            uint32_t step, int edge, Real hx, Real hy) {
+                                            uint32_t step, int edge, Real hx, Real hy, uint32_t max_steps) {
     const double dhx = static_cast<double>(hx), dhy = static_cast<double>(hy);
     const bool horiz = edge < 2;
     const double par = horiz ? (dhx - a.txmin) / a.thx : (dhy - a.tymin) / a.thy;
@@ -560,7 +574,7 @@ __device__ __forceinline__ void record_exit(const WalkArgs& a, uint64_t g, uint3
     const double gv = table_at(a.tg[edge], tn, par);
     // restarts happen at exactly max_steps: one atomic per finished walk
     if (a.node_steps)
-        atomicAdd(a.node_steps + node, static_cast<unsigned long long>(epoch) * a.max_steps32 + step);
+        atomicAdd(a.node_steps + node, static_cast<unsigned long long>(epoch) * max_steps + step);
     if (a.dump) {
         sddg_path& r = a.dump[g];
         r.f = fv;
@@ -620,18 +634,21 @@ __host__ __device__ constexpr size_t walk_table_bytes() {
 }
 static_assert(sizeof(fm::FmTables) % 16 == 0, "LaneState alignment after the tables");
 
-template <int DV, typename Real, int SCHEME, bool BRIDGE>
+// TAIL: the batch hands its last walks to the tail kernel (walk_tail.cuh):
+// the step loop counts chunks of a.chunk32 steps with check points between
+// them.  Without TAIL the loop is the plain one (1.5 instructions per step
+// fewer: the large batches, where the tail is a negligible share).
+template <int DV, typename Real, int SCHEME, bool BRIDGE, bool TAIL = false>
 __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Real>())
     walk_kernel(const __grid_constant__ WalkArgs a) {
+    static_assert(!TAIL || kTailHandoff<Real>, "tail handoff is fp64 only");
     constexpr bool FAST = DV >= DV_RING_AN;
     using Ops = RealOps<Real, FAST>;
-    const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax),
-                        Real(a.box[0]), Real(a.box[1]), Real(a.box[2]), Real(a.box[3]),
-                        a.box_hi[0], a.box_hi[1], a.box_hi[2], a.box_hi[3]};
+    const Dom<Real> dom = walk_dom<Real>(a);
     const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab};
-    const Real dt = Real(a.dt);
-    const Real sq2dt = Real(a.sqrt2dt);
-    const Real thr = Real(a.bridge_thr);
+    const Real dt = walk_prm<Real>(a.dt, a.f_dt);
+    const Real sq2dt = walk_prm<Real>(a.sqrt2dt, a.f_sqrt2dt);
+    const Real thr = walk_prm<Real>(a.bridge_thr, a.f_thr);
     const uint32_t max_steps = a.max_steps32;
     // Dynamic shared memory: the fastmath tables (performance-mode fp64) then
     // the per-lane bookkeeping.  No static shared memory, so the tables sit at
@@ -676,6 +693,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             L.node = node;
             L.walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
             L.epoch = 0;
+            if constexpr (TAIL) L.base = 0;
             x = Real(a.px[node]);
             y = Real(a.py[node]);
             rng.init(a.pid[node], L.walk, 0);
@@ -683,18 +701,18 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
         start_walk(L.g);
         bool in_box = box_test<DV, Real>(dom, x, y);
         uint32_t step = 0;
-        // steps between handoff check points (max_steps when the tail
-        // kernel is off: the restart compare the loop always had)
-        const uint32_t walk_lim =
-            kTailHandoff<Real> && a.cont && kHandoffCheck < max_steps ? kHandoffCheck : max_steps;
-        uint32_t lim = walk_lim;
+        // `step` counts the steps of the current chunk of a.chunk32 steps;
+        // L.base the chunks completed in this epoch.  The loop's only compare
+        // is the one it always had (a.chunk32 = max_steps without the tail
+        // kernel); with it, a.chunk32 divides max_steps and each chunk end is
+        // a handoff check point.
+        const uint32_t chunk = a.chunk32;
         SDDG_UNROLL(SDDG_WALK_UNROLL)  // 2: step copies alternate x, y registers (no loop-carried moves)
         for (;;) {
             // ---- one step (step_drift, step_rand, step_update: shared with the
             // tail kernel so both compute every step bit for bit alike)
-            const StepDrift<Real> sd = step_drift<DV, Real, SCHEME>(T, P, dt, x, y);
-            const bool ok = sd.ok;
             Real nxp, nyp;
+            bool ok;
             {
                 uint64_t w0, w1, w2 = 0;
                 if constexpr (SCHEME == 0) {
@@ -704,6 +722,8 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                     rng.next_pair(a.rk, w1, w2);
                 }
                 const StepRand<Real> r = step_rand<DV, Real, SCHEME>(T, a, sq2dt, w0, w1, w2);
+                const StepDrift<Real> sd = step_drift<DV, Real, SCHEME>(T, P, dt, x, y);
+                ok = sd.ok;
                 step_update<DV, Real, SCHEME>(sd, r, dt, sq2dt, x, y, nxp, nyp);
             }
             ++step;
@@ -721,13 +741,15 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 x = nxp;
                 y = nyp;
                 in_box = nb;
-                if (step < (kTailHandoff<Real> ? lim : max_steps)) continue;
-                if (kTailHandoff<Real> && step < max_steps) {
-                    // handoff check point (tail kernel enabled): once the batch
-                    // counter has run out and few walks remain, the walk moves to
-                    // the tail kernel, which runs it on a whole warp at a fraction
-                    // of a lane's step latency (walk_tail.cuh)
-                    lim = max_steps - step > kHandoffCheck ? step + kHandoffCheck : max_steps;
+                if (step < (TAIL ? chunk : max_steps)) continue;
+                const uint32_t done = TAIL ? L.base + step : step;  // steps of this epoch
+                if (TAIL && done < max_steps) {
+                    // handoff check point: once the batch counter has run out
+                    // and few walks remain, the walk moves to the tail kernel,
+                    // which runs it on a whole warp at a fraction of a lane's
+                    // step latency (walk_tail.cuh)
+                    L.base = done;
+                    step = 0;
                     if (*reinterpret_cast<volatile unsigned long long*>(a.next) >= a.total &&
                         *reinterpret_cast<volatile unsigned long long*>(a.live) <= a.cont_cap) {
                         const uint32_t k = atomicAdd(a.n_cont, 1u);
@@ -739,7 +761,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                             c.node = L.node;
                             c.walk = L.walk;
                             c.epoch = L.epoch;
-                            c.step = step;
+                            c.step = done;
                             c.n = rng.n;
                             break;
                         }
@@ -747,7 +769,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                     continue;
                 }
                 // max_steps reached: restart on the next epoch's stream
-                L.steps += step;
+                L.steps += done;
                 const uint32_t epoch = ++L.epoch;
                 const uint32_t node = L.node;
                 if (epoch >= 1024u) {
@@ -759,23 +781,23 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 x = Real(a.px[node]);
                 y = Real(a.py[node]);
                 in_box = box_test<DV, Real>(dom, x, y);
+                if constexpr (TAIL) L.base = 0;
                 step = 0;
-                lim = walk_lim;
                 continue;
             }
             // ---- exit: boundary values, record, next walk
-            L.steps += step;
-            record_exit<Real>(a, L.g, L.node, L.epoch, step, edge, hx, hy);
+            const uint32_t walk_steps = TAIL ? L.base + step : step;
+            L.steps += walk_steps;
+            record_exit<Real>(a, L.g, L.node, L.epoch, walk_steps, edge, hx, hy, max_steps);
             const uint64_t gn = atomicAdd(a.next, 1ull);
             if (gn >= a.total) {
-                if (kTailHandoff<Real> && a.cont) atomicAdd(a.live, ~0ull);  // one walk fewer in flight (-1)
+                if constexpr (TAIL) atomicAdd(a.live, ~0ull);  // one walk fewer in flight (-1)
                 break;
             }
             L.g = gn;
             start_walk(gn);
             in_box = box_test<DV, Real>(dom, x, y);
             step = 0;
-            lim = walk_lim;
         }
     }
     uint64_t my_steps = L.steps;
@@ -793,7 +815,7 @@ constexpr size_t walk_smem() {
     return walk_table_bytes<DV, Real>() + sizeof(LaneState) * walk_block<DV, Real>();
 }
 
-template <int DV, typename Real, int SCHEME, bool BRIDGE>
+template <int DV, typename Real, int SCHEME, bool BRIDGE, bool TAIL = false>
 cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
     constexpr size_t sm = walk_smem<DV, Real>();
     if constexpr (sm > 48 * 1024) {
@@ -803,14 +825,14 @@ cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_relaxed)) {
-            const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE>,
+            const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE, TAIL>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(sm));
             if (e != cudaSuccess) return e;
             if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_relaxed);
         }
     }
-    walk_kernel<DV, Real, SCHEME, BRIDGE><<<grid, walk_block<DV, Real>(), sm, s>>>(a);
+    walk_kernel<DV, Real, SCHEME, BRIDGE, TAIL><<<grid, walk_block<DV, Real>(), sm, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -822,6 +844,13 @@ namespace sddg {
 
 template <int DV, typename Real>
 cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
+    if constexpr (kTailHandoff<Real>) {
+        if (a.cont) {
+            if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false, true>(a, grid, s);
+            if (a.bridge) return launch_one<DV, Real, 0, true, true>(a, grid, s);
+            return launch_one<DV, Real, 0, false, true>(a, grid, s);
+        }
+    }
     if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false>(a, grid, s);
     if (a.bridge) return launch_one<DV, Real, 0, true>(a, grid, s);
     return launch_one<DV, Real, 0, false>(a, grid, s);

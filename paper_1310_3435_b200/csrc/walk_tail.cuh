@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
                                                                         in_box, ws, hx, hy, edge, nb);
                 if (exited) {
                     if (lane == 0) {
-                        record_exit<Real>(a, c.g, node, epoch, step, edge, hx, hy);
+                        record_exit<Real>(a, c.g, node, epoch, step, edge, hx, hy, max_steps);
                         atomicAdd(a.steps, static_cast<unsigned long long>(extra + step));
                     }
                     done = true;
