@@ -458,13 +458,13 @@ solve_kernel(const double* __restrict__ wg, int gnx, double ihx2, double ihy2,
     }
 }
 
-template <int METHOD, int PTS, int G = 1>
+template <int METHOD, int PTS, int G = 1, bool STREAM = false>
 cudaError_t launch_one(int grid, int threads, size_t smem, cudaStream_t st, const double* wg,
                        int gnx, double ihx2, double ihy2, const SolveJob* jobs, const double* bc,
                        double tol, int64_t mi, int init_blend, const double* omega, const int* perm, double* u,
                        sddg_solve_info* info, double* scratch, int64_t cstride, int cin,
                        int* err) {
-    auto k = solve_kernel<METHOD, PTS, G>;
+    auto k = solve_kernel<METHOD, PTS, G, STREAM>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -957,6 +957,14 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
     const int64_t cstride = static_cast<int64_t>(ncoef) * max_n;
     const int grid = static_cast<int>(n_jobs);
     const int T = kSolveThreads;
+    // K3s: weights streamed through a shared-memory ring by bulk copies when
+    // they do not fit next to u but u and the ring do (129^2: 133 + 64 KB)
+    const size_t smem_stream = sizeof(double) * ((static_cast<size_t>(max_n) + 1) & ~size_t(1)) + kStreamRingBytes;
+    if (method == SDDG_SOLVER_RBSOR && !coef_in_smem && smem_stream <= 227 * 1024 &&
+        !std::getenv("SDDG_NO_STREAM"))
+        return launch_one<1, 1, 1, true>(grid, T, smem_stream, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
+                                         max_iters_cfg, init_blend, omega, perm, u, info, coef_scratch,
+                                         cstride, coef_in_smem, err);
     if (method == SDDG_SOLVER_RBSOR)
         return coef_in_smem
                    ? launch_one<1, 1, 1>(grid, T, smem, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,

@@ -296,3 +296,29 @@ def test_per_job_sor_factor_same_fixed_point_fewer_sweeps(oracle, ctx):
     for a, b in zip(e1, g1):
         assert abs(a.iterations - b.iterations) <= 2
         assert np.max(np.abs(a.values - b.values)) <= 1e-10
+
+
+@pytest.mark.parametrize("nx,ny", [(129, 129), (97, 130)])
+def test_streamed_solver_matches_l2_solver(oracle, ctx, monkeypatch, nx, ny):
+    # K3s (the packed weights streamed through a two-stage shared-memory ring
+    # by cp.async.bulk + mbarriers) runs K3's iteration on the same weights:
+    # identical iterates, bit for bit.  200 jobs > one per SM, so the batch
+    # is not a cluster batch.
+    g = 513
+    w = oracle.weight_values(B.density(B.SHOCK_W), UNIT, g, g)
+    rng = np.random.default_rng(nx + ny)
+    subs, bcs = [], []
+    for k in range(200):
+        v0, v1, v2, v3 = np.sort(rng.random(4))
+        ex = lambda lo, hi: np.linspace(lo, hi, nx)  # noqa: E731
+        ey = lambda lo, hi: np.linspace(lo, hi, ny)  # noqa: E731
+        bcs.append(sdd.EdgeData(ex(v0, v1), ex(v2, v3), ey(v0, v2), ey(v1, v3)))
+        subs.append(((k * 37) % (g - nx), (k * 53) % (g - ny), nx, ny))
+    cfg = sdd.SolverConfig(tol=1e-12, method="rbsor")
+    a = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), subs, bcs, cfg, ctx=ctx)
+    monkeypatch.setenv("SDDG_NO_STREAM", "1")
+    b = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), subs, bcs, cfg, ctx=ctx)
+    for ra, rb in zip(a, b):
+        assert ra.converged and rb.converged
+        assert np.array_equal(ra.values, rb.values)
+        assert ra.iterations == rb.iterations and ra.final_update == rb.final_update
