@@ -957,11 +957,15 @@ cudaError_t launch_solve_batch(const double* w_global, int gnx, double hx, doubl
     const int64_t cstride = static_cast<int64_t>(ncoef) * max_n;
     const int grid = static_cast<int>(n_jobs);
     const int T = kSolveThreads;
-    // K3s: weights streamed through a shared-memory ring by bulk copies when
-    // they do not fit next to u but u and the ring do (129^2: 133 + 64 KB)
+    // K3s (opt-in, SDDG_SOLVER_STREAM=1): the weights streamed through a
+    // shared-memory ring by bulk copies.  Bit-identical to K3 but slower on
+    // the 2048 x 129^2 batch (59 vs 40 ms): next to u's 133 KB the ring gets
+    // 64 KB, one 32-KB stage in flight while the other is swept, against the
+    // 64 KB that K3's 512 threads keep in flight with 4 slots of L2 loads each.
     const size_t smem_stream = sizeof(double) * ((static_cast<size_t>(max_n) + 1) & ~size_t(1)) + kStreamRingBytes;
-    if (method == SDDG_SOLVER_RBSOR && !coef_in_smem && smem_stream <= 227 * 1024 &&
-        !std::getenv("SDDG_NO_STREAM"))
+    const char* stream_env = std::getenv("SDDG_SOLVER_STREAM");
+    if (method == SDDG_SOLVER_RBSOR && !coef_in_smem && smem_stream <= 227 * 1024 && stream_env &&
+        stream_env[0] == '1')
         return launch_one<1, 1, 1, true>(grid, T, smem_stream, s, w_global, gnx, ihx2, ihy2, jobs, bc, tol,
                                          max_iters_cfg, init_blend, omega, perm, u, info, coef_scratch,
                                          cstride, coef_in_smem, err);

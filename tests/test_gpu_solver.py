@@ -315,8 +315,9 @@ def test_streamed_solver_matches_l2_solver(oracle, ctx, monkeypatch, nx, ny):
         bcs.append(sdd.EdgeData(ex(v0, v1), ex(v2, v3), ey(v0, v2), ey(v1, v3)))
         subs.append(((k * 37) % (g - nx), (k * 53) % (g - ny), nx, ny))
     cfg = sdd.SolverConfig(tol=1e-12, method="rbsor")
+    monkeypatch.setenv("SDDG_SOLVER_STREAM", "1")
     a = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), subs, bcs, cfg, ctx=ctx)
-    monkeypatch.setenv("SDDG_NO_STREAM", "1")
+    monkeypatch.delenv("SDDG_SOLVER_STREAM")
     b = sdd.solve_dirichlet_batch(w, g, g, 1 / (g - 1), 1 / (g - 1), subs, bcs, cfg, ctx=ctx)
     for ra, rb in zip(a, b):
         assert ra.converged and rb.converged
