@@ -254,7 +254,13 @@ def solver_rooflines(sdd, ctx):
     X, Y = np.meshgrid(x, x)
     w = (1.0 + 20.0 / np.cosh(50 * (Y - 0.5 - 0.15 * np.sin(2 * np.pi * X))) ** 2).ravel()
     peak, src = hbm_peak_gbs()
-    out = {"bytes_per_point_update": 40, "peak_GBps": peak, "peak_source": src}
+    onchip = ctx.probe_onchip_bandwidth()
+    out = {"bytes_per_point_update": 40, "peak_GBps": peak, "peak_source": src,
+           "onchip_peaks_GBps": onchip,
+           "onchip_note": "the batches stay on chip (SURVEY D9): K3 reads its 32 B of packed weights per "
+                          "update from L2 (u in shared memory) -> frac_of_l2; K3c keeps weights and u in "
+                          "shared memory: 80 B of shared-memory reads per update (5 u + 32 B weights + "
+                          "the write) -> frac_of_smem; peaks measured on this GPU (sddg_probe_onchip_bandwidth)"}
     for name, n_jobs in (("config3_batch", 128), ("batch_2048", 2048)):
         rng = np.random.default_rng(3)
         jobs, bcs = [], []
@@ -278,6 +284,13 @@ def solver_rooflines(sdd, ctx):
                      "sweeps_max": int(its.max()), "point_updates_per_s": upd / (best / 1e3),
                      "effective_GBps": gbs, "frac_of_hbm_peak": gbs / peak,
                      "converged": bool(all(r.converged for r in res))}
+        ups = upd / (best / 1e3)
+        if n_jobs <= 148:
+            out[name]["onchip_bound"] = "smem"
+            out[name]["frac_of_smem"] = ups * 80 / 1e9 / onchip["smem_GBps"]
+        else:
+            out[name]["onchip_bound"] = "l2"
+            out[name]["frac_of_l2"] = ups * 32 / 1e9 / onchip["l2_GBps"]
     return out
 
 

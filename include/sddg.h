@@ -170,6 +170,12 @@ sddg_status sddg_last_tail_stats(const sddg_ctx* ctx, int64_t* handoffs, double*
  * pipe roofline. */
 sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops);
 
+/* Measured on-chip read bandwidths of this device in GB/s: L2 (every SM
+ * streaming a 64 MB L2-resident buffer) and shared memory (conflict-free
+ * 16-B loads on every SM), the rooflines of the subdomain solver, whose
+ * batches stay on chip. */
+sddg_status sddg_probe_onchip_bandwidth(sddg_ctx* ctx, double* l2_gbps, double* smem_gbps);
+
 /* Diagnostics: max ulp error over n sample points of the performance-mode
  * elementary functions (exp, log on (0, 0.9], sincos(2 pi u), sqrt, rcp)
  * against the CUDA library; slot 5: max ulp error of log on (0.9, 1). */

@@ -58,6 +58,89 @@ cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tf
     return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
+// ---- on-chip bandwidth peaks (the subdomain solver's rooflines, SURVEY D9:
+// its batches live in shared memory and L2, not HBM)
+
+namespace {
+
+// L2: every CTA streams the whole L2-resident buffer (16-B loads, grid-
+// strided so all LTS slices serve), summing to keep the loads live
+__global__ void __launch_bounds__(512) l2_probe(const double2* __restrict__ buf, size_t n, int reps,
+                                                double* out) {
+    double s = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x + r * 32ull * blockDim.x;
+             k < n + r * 32ull * blockDim.x; k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+            const double2 v = __ldcg(buf + (k % n));
+            s += v.x + v.y;
+        }
+    }
+    if (s == -12345.0) out[0] = s;
+}
+
+// shared memory: 16-B loads from a 48 KB array, conflict-free (consecutive
+// lanes, consecutive 16-B words)
+__global__ void __launch_bounds__(1024) smem_probe(int iters, double* out) {
+    __shared__ double2 a[3072];
+    for (int k = threadIdx.x; k < 3072; k += blockDim.x) a[k] = make_double2(k, k + 1);
+    __syncthreads();
+    double s0 = 0.0, s1 = 0.0;
+    int idx = threadIdx.x;
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const double2 v = a[(idx + u * 32) % 3072];
+            s0 += v.x;
+            s1 += v.y;
+        }
+        idx = (idx + 256) % 3072;
+    }
+    if (s0 + s1 == -12345.0) out[0] = s0;
+}
+
+}  // namespace
+
+cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double* smem_gbps) {
+    const size_t bytes = 64ull << 20;  // 64 MB: L2-resident (126 MB)
+    void* buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, bytes + 64);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(buf, 0, bytes, st);
+    double* out = reinterpret_cast<double*>(static_cast<char*>(buf) + bytes);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    const size_t n = bytes / sizeof(double2);
+    const int reps = 8;
+    double best_l2 = 0.0, best_sm = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(a, st);
+        l2_probe<<<sms * 4, 512, 0, st>>>(static_cast<const double2*>(buf), n, reps, out);
+        cudaEventRecord(b, st);
+        e = cudaEventSynchronize(b);
+        if (e != cudaSuccess) break;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep > 0) best_l2 = std::max(best_l2, double(bytes) * reps / (ms * 1e-3) / 1e9);
+        const int iters = 4096;
+        cudaEventRecord(a, st);
+        smem_probe<<<sms * 2, 1024, 0, st>>>(iters, out);
+        cudaEventRecord(b, st);
+        e = cudaEventSynchronize(b);
+        if (e != cudaSuccess) break;
+        cudaEventElapsedTime(&ms, a, b);
+        const double sbytes = 16.0 * 8 * iters * sms * 2.0 * 1024;
+        if (rep > 0) best_sm = std::max(best_sm, sbytes / (ms * 1e-3) / 1e9);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    *l2_gbps = best_l2;
+    *smem_gbps = best_sm;
+    return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
 }  // namespace sddg
 
 // ---- accuracy self-test of fastmath.cuh against the CUDA library

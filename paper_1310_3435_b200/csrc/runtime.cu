@@ -1376,6 +1376,12 @@ sddg_status sddg_probe_fma_peak(sddg_ctx* ctx, int32_t precision, double* tflops
     API_END(ctx)
 }
 
+sddg_status sddg_probe_onchip_bandwidth(sddg_ctx* ctx, double* l2_gbps, double* smem_gbps) {
+    API_BEGIN(ctx)
+    ck(probe_onchip_gbps(ctx->sms, ctx->stream, l2_gbps, smem_gbps), "probe");
+    API_END(ctx)
+}
+
 sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[6]) {
     API_BEGIN(ctx)
     unsigned long long m[6];

@@ -179,6 +179,7 @@ cudaError_t launch_linf(const double* X, const double* Y, const double* RX, cons
                         unsigned long long* out_bits, cudaStream_t s);
 
 cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
+cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double* smem_gbps);
 cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long* host_maxulp5);
 
 }  // namespace sddg

@@ -237,6 +237,12 @@ class Context:
                self._h)
         return t.value
 
+    def probe_onchip_bandwidth(self):
+        """Measured L2 and shared-memory read bandwidth (GB/s) of this device."""
+        l2, sm = C.c_double(), C.c_double()
+        _check(lib().sddg_probe_onchip_bandwidth(self._h, C.byref(l2), C.byref(sm)), self._h)
+        return {"l2_GBps": l2.value, "smem_GBps": sm.value}
+
     def last_stats(self):
         s, n, ms = C.c_int64(), C.c_int64(), C.c_double()
         _check(lib().sddg_last_stats(self._h, C.byref(s), C.byref(n), C.byref(ms)), self._h)
