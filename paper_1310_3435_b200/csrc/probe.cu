@@ -63,16 +63,18 @@ cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tf
 
 namespace {
 
-// L2: every CTA streams the whole L2-resident buffer (16-B loads, grid-
-// strided so all LTS slices serve), summing to keep the loads live
+// L2: the grid streams an L2-resident buffer reps times (16-B loads, four
+// independent ones in flight per thread, grid-strided so all LTS slices serve)
 __global__ void __launch_bounds__(512) l2_probe(const double2* __restrict__ buf, size_t n, int reps,
                                                 double* out) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     double s = 0.0;
     for (int r = 0; r < reps; ++r) {
-        for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x + r * 32ull * blockDim.x;
-             k < n + r * 32ull * blockDim.x; k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-            const double2 v = __ldcg(buf + (k % n));
-            s += v.x + v.y;
+        for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k + 3 * stride < n;
+             k += 4 * stride) {
+            const double2 v0 = __ldcg(buf + k), v1 = __ldcg(buf + k + stride);
+            const double2 v2 = __ldcg(buf + k + 2 * stride), v3 = __ldcg(buf + k + 3 * stride);
+            s += (v0.x + v1.y) + (v2.x + v3.y);
         }
     }
     if (s == -12345.0) out[0] = s;
@@ -112,9 +114,9 @@ cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double*
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const size_t n = bytes / sizeof(double2);
-    const int reps = 8;
+    const int reps = 32;
     double best_l2 = 0.0, best_sm = 0.0;
-    for (int rep = 0; rep < 4; ++rep) {
+    for (int rep = 0; rep < 5; ++rep) {
         cudaEventRecord(a, st);
         l2_probe<<<sms * 4, 512, 0, st>>>(static_cast<const double2*>(buf), n, reps, out);
         cudaEventRecord(b, st);
@@ -122,7 +124,9 @@ cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double*
         if (e != cudaSuccess) break;
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
-        if (rep > 0) best_l2 = std::max(best_l2, double(bytes) * reps / (ms * 1e-3) / 1e9);
+        const size_t stride = static_cast<size_t>(sms) * 4 * 512;
+        const double read = double(n / (4 * stride)) * 4 * stride * sizeof(double2) * reps;
+        if (rep > 0) best_l2 = std::max(best_l2, read / (ms * 1e-3) / 1e9);
         const int iters = 4096;
         cudaEventRecord(a, st);
         smem_probe<<<sms * 2, 1024, 0, st>>>(iters, out);
