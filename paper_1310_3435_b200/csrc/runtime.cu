@@ -391,14 +391,17 @@ void enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt, uint64_
     a.cont_cap = 0;
     a.chunk32 = a.max_steps32;
     if (precision != SDDG_FP64 || std::getenv("SDDG_NO_TAIL")) return;
-    if (a.total > kTailWalksPerLane * lanes) return;
+    const char* wpl = std::getenv("SDDG_TAIL_WALKS_PER_LANE");  // A/B knob
+    const uint64_t max_wpl = wpl ? std::strtoull(wpl, nullptr, 10) : kTailWalksPerLane;
+    if (a.total > max_wpl * lanes) return;
     // K1's check points every chunk32 steps: the largest of 256, 128, 64
     // dividing max_steps (the restart must still fall on a chunk end)
     uint32_t chunk = 256;
     while (chunk >= 64 && a.max_steps32 % chunk != 0) chunk /= 2;
     if (chunk < 64 || chunk >= a.max_steps32) return;
     a.chunk32 = chunk;
-    const uint32_t cap = static_cast<uint32_t>(c->sms) * 16u;
+    const char* per_sm = std::getenv("SDDG_TAIL_PER_SM");  // A/B knob: walks handed over per SM
+    const uint32_t cap = static_cast<uint32_t>(c->sms) * (per_sm ? std::max(1, std::atoi(per_sm)) : 16);
     a.cont = static_cast<WalkCont*>(c->tail_cont.ensure(sizeof(WalkCont) * cap));
     a.cont_cap = cap;
     a.n_cont = &cnt->n_cont;

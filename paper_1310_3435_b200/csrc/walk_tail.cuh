@@ -230,7 +230,12 @@ cudaError_t launch_tail_one(const WalkArgs& a, cudaStream_t s) {
             if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_relaxed);
         }
     }
-    const unsigned grid = (a.cont_cap + kTailWarps - 1) / kTailWarps;
+    // one CTA per SM (cont_cap = 16 per SM by default); a larger cap queues
+    // the walks of a warp (grid-stride over the continuations)
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = std::min<unsigned>((a.cont_cap + kTailWarps - 1) / kTailWarps, static_cast<unsigned>(sms));
     walk_tail_kernel<DV, Real, SCHEME, BRIDGE><<<grid, kTailWarps * 32, sm, s>>>(a);
     return cudaGetLastError();
 }

@@ -47,7 +47,10 @@ def cases():
 
 
 out = {}
+only = set(sys.argv[1:])
 for name, m, pts, pid, bd, cfg, dom in cases():
+    if only and name not in only:
+        continue
     res = {}
     for mode in ("tail", "k1_only"):
         if mode == "k1_only":
