@@ -74,24 +74,62 @@ __device__ __forceinline__ PhiloxWords philox4x32_10(const RoundKeys& rk, uint32
 }
 
 // Per-lane stream (one walk, one epoch); the seed lives in RoundKeys.
+//
+// Within one stream only the block counter c0 changes, so part of the first
+// two rounds is the same for every block and is computed once per walk:
+// round 1's product of the third word, M1 * c2, gives the round-1 outputs
+// c0' = hi(M1 c2) ^ walk ^ k0 and c1' = lo(M1 c2); round 2's product of that
+// c0', M0 * c0', is then fixed as well.  Per block the first two rounds cost
+// one 32x32->64 multiply each instead of two (the same words as
+// philox4x32_10; tests/test_gpu_walk.py compares every stream with the
+// reference's).
 struct LaneStream {
-    uint32_t c1;       // walk
-    uint32_t c2, c3;   // point id lo, point id hi16 | epoch << 16
-    uint32_t n;        // u64s consumed this epoch
-    uint32_t cw2, cw3; // words 2,3 of the last generated block
+    uint32_t c3;         // point id hi16 | epoch << 16 (round-1 input)
+    uint32_t r1c1;       // round-1 output word 1: lo(M1 * c2)
+    uint32_t r2lo, r2hi; // round 2: lo/hi of M0 * c0'
+    uint32_t n;          // u64s consumed this epoch
+    uint32_t cw2, cw3;   // words 2,3 of the last generated block
 
-    __device__ __forceinline__ void init(uint64_t pid, uint32_t walk, uint32_t epoch) {
-        c1 = walk;
-        c2 = static_cast<uint32_t>(pid);
+    __device__ __forceinline__ void init(const RoundKeys& rk, uint64_t pid, uint32_t walk, uint32_t epoch) {
+        const uint32_t c2 = static_cast<uint32_t>(pid);
         c3 = static_cast<uint32_t>((pid >> 32) & 0xFFFFu) | (epoch << 16);
+        r1c1 = 0xCD9E8D57u * c2;
+        const uint32_t c0p = __umulhi(0xCD9E8D57u, c2) ^ walk ^ rk.k[0];
+        r2lo = 0xD2511F53u * c0p;
+        r2hi = __umulhi(0xD2511F53u, c0p);
         n = 0;
         cw2 = cw3 = 0;
+    }
+
+    // Philox4x32-10 of block c0 of this stream (philox4x32_10 with rounds 1
+    // and 2 partly precomputed)
+    __device__ __forceinline__ PhiloxWords block(const RoundKeys& rk, uint32_t c0) const {
+        // round 1: (c0, walk, c2, c3) -> (c0', r1c1, hi(M0 c0) ^ c3 ^ k1, lo(M0 c0))
+        const uint32_t a2 = __umulhi(0xD2511F53u, c0) ^ c3 ^ rk.k[1];
+        const uint32_t a3 = 0xD2511F53u * c0;
+        // round 2: M0 * c0' precomputed
+        uint32_t x0 = __umulhi(0xCD9E8D57u, a2) ^ r1c1 ^ rk.k[2];
+        uint32_t x1 = 0xCD9E8D57u * a2;
+        uint32_t x2 = r2hi ^ a3 ^ rk.k[3];
+        uint32_t x3 = r2lo;
+#pragma unroll
+        for (int r = 2; r < 10; ++r) {
+            const uint32_t lo0 = 0xD2511F53u * x0;
+            const uint32_t hi0 = __umulhi(0xD2511F53u, x0);
+            const uint32_t lo1 = 0xCD9E8D57u * x2;
+            const uint32_t hi1 = __umulhi(0xCD9E8D57u, x2);
+            x0 = hi1 ^ x1 ^ rk.k[2 * r];
+            x1 = lo1;
+            x2 = hi0 ^ x3 ^ rk.k[2 * r + 1];
+            x3 = lo0;
+        }
+        return {x0, x1, x2, x3};
     }
 
     // Two consecutive u64s (n, n+1): exactly one new block, index (n+1)>>1,
     // for either parity of n -- the per-step Philox call is warp-uniform.
     __device__ __forceinline__ void next_pair(const RoundKeys& rk, uint64_t& a, uint64_t& b) {
-        const PhiloxWords w = philox4x32_10(rk, (n + 1) >> 1, c1, c2, c3);
+        const PhiloxWords w = block(rk, (n + 1) >> 1);
         const bool odd = n & 1u;
         a = odd ? join64(cw2, cw3) : join64(w.w0, w.w1);
         b = odd ? join64(w.w0, w.w1) : join64(w.w2, w.w3);
@@ -106,7 +144,7 @@ struct LaneStream {
         if (n & 1u) {
             v = join64(cw2, cw3);
         } else {
-            const PhiloxWords w = philox4x32_10(rk, n >> 1, c1, c2, c3);
+            const PhiloxWords w = block(rk, n >> 1);
             v = join64(w.w0, w.w1);
             cw2 = w.w2;
             cw3 = w.w3;

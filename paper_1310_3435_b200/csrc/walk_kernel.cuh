@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             if constexpr (TAIL) L.base = 0;
             x = Real(a.px[node]);
             y = Real(a.py[node]);
-            rng.init(a.pid[node], L.walk, 0);
+            rng.init(a.rk, a.pid[node], L.walk, 0);
         };
         start_walk(L.g);
         bool in_box = box_test<DV, Real>(dom, x, y);
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                     atomicExch(a.err_info, static_cast<unsigned long long>(a.pid[node]));
                     break;
                 }
-                rng.init(a.pid[node], L.walk, epoch);
+                rng.init(a.rk, a.pid[node], L.walk, epoch);
                 x = Real(a.px[node]);
                 y = Real(a.py[node]);
                 in_box = box_test<DV, Real>(dom, x, y);
