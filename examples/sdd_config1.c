@@ -10,7 +10,11 @@
  * proj/include/sdd/decomposition.hpp:91-94), then inverts the mesh and
  * reports its quality (sddg_invert_mesh / sddg_quality_report).
  *
- * usage: sdd_config1 [reference|analytic] [seed]
+ * usage: sdd_config1 [reference|analytic] [seed] [devices]
+ * devices: a comma-separated CUDA device list, e.g. "0,1,2,3": one process
+ * drives all of them through sddg_create_multi (nodes and subdomains sharded,
+ * NCCL all-gathers; a device listed twice runs as two ranks exchanging by
+ * device copies).  Default: one device, sddg_create(0).
  * prints: one line "mc_points path_steps t_stoc t_sub checksum_xi checksum_eta
  * q_max q_mean" (checksums = plain sums in index order; tests/test_gpu_sdd.py
  * compares them with the Python mirror's solve_sdd on the same inputs).
@@ -36,7 +40,17 @@ int main(int argc, char** argv) {
         return 2;
     }
     sddg_ctx* ctx = NULL;
-    if (check(sddg_create(0, &ctx), NULL, "sddg_create")) return 1;
+    if (argc > 3) {
+        int devices[16], nd = 0;
+        const char* p = argv[3];
+        while (*p && nd < 16) {
+            devices[nd++] = (int)strtol(p, (char**)&p, 10);
+            if (*p == ',') ++p;
+        }
+        if (check(sddg_create_multi(nd, devices, &ctx), NULL, "sddg_create_multi")) return 1;
+    } else if (check(sddg_create(0, &ctx), NULL, "sddg_create")) {
+        return 1;
+    }
 
     sddg_density dens;
     memset(&dens, 0, sizeof dens);

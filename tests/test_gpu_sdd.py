@@ -193,3 +193,16 @@ def test_plain_c_caller_matches_python_mirror(ctx, mode):
     assert float(sx) == float(np.cumsum(r.xi)[-1]) and float(se) == float(np.cumsum(r.eta)[-1])
     q = sdd.quality_report(sdd.invert_mesh(r.xi, r.eta, spec, 65, 65, ctx=ctx), ctx=ctx)
     assert float(qmax) == q.q_max and float(qmean) == q.q_mean
+
+
+def test_plain_c_caller_on_a_multi_gpu_context():
+    # the same C program through sddg_create_multi: device 0 listed three
+    # times (three ranks: sharded nodes and subdomains, device-copy exchange)
+    # prints the single-device mesh checksums bit for bit
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "_bin", "sdd_config1")
+    one = subprocess.run([exe, "analytic", "3"], capture_output=True, text=True, timeout=300)
+    three = subprocess.run([exe, "analytic", "3", "0,0,0"], capture_output=True, text=True, timeout=300)
+    assert one.returncode == 0 and three.returncode == 0, (one.stderr, three.stderr)
+    a, b = one.stdout.split(), three.stdout.split()
+    assert a[:2] == b[:2] and a[4:] == b[4:]  # all but the two timings
