@@ -108,7 +108,20 @@ typedef struct {
 typedef enum { SDDG_SCHEME_LINEAR = 0, SDDG_SCHEME_EXPONENTIAL = 1 } sddg_scheme;
 typedef enum { SDDG_FP64 = 0, SDDG_FP32 = 1 } sddg_precision;
 
-/* sdd::WalkConfig (proj/include/sdd/sde.hpp:16-26) + precision. */
+typedef enum {
+    /* the reference's SDE (sde.cpp:21-29): drift grad(w)/w = -grad(rho)/rho,
+     * noise sqrt(2 dt) z; generator (1/w) div(w grad).  Parity mode. */
+    SDDG_FORM_REFERENCE = 0,
+    /* BASELINE.json's literal SDE dX = grad(w) dt + sqrt(2 w) dW: generator
+     * div(w grad), the reference's times w -- a time change, so the same
+     * harmonic functions and exit law (estimates agree statistically, walks
+     * take fewer steps where w > 1).  The bridge exponent becomes
+     * d0 d1 / (w dt) with w at the step's start.  Opt-in: BASELINE weights
+     * (kinds 16-18), analytic grad(w), linear scheme, fp64 or fp32. */
+    SDDG_FORM_LITERAL = 1
+} sddg_sde_form;
+
+/* sdd::WalkConfig (proj/include/sdd/sde.hpp:16-26) + precision + SDE form. */
 typedef struct {
     int32_t scheme;    /* sddg_scheme */
     int32_t precision; /* sddg_precision: FP32 walks keep fp64 sums (config 3) */
@@ -118,7 +131,7 @@ typedef struct {
     uint64_t seed;
     int64_t max_steps; /* steps per epoch before a restart, 1..2^29 */
     int32_t bridge_test;
-    int32_t reserved;
+    int32_t form;      /* sddg_sde_form (0: the reference's) */
 } sddg_walk_config;
 
 /* sdd::McEstimate (proj/include/sdd/sde.hpp:61-68) + the raw fixed-order

@@ -117,6 +117,19 @@ int drift_variant(const sddg_density& d, int precision) {
 
 void check_table(const sddg_density& d);
 
+// The walk kernel variant of (density, walk config): the drift variant, or
+// for BASELINE's literal SDE (cfg.form) its own variant (the BASELINE
+// weights, performance mode, linear scheme).
+int walk_variant(const sddg_density& d, const sddg_walk_config& cfg) {
+    if (cfg.form == SDDG_FORM_REFERENCE) return drift_variant(d, cfg.precision);
+    if (cfg.form != SDDG_FORM_LITERAL) fail(SDDG_ERR_VALIDATION, "WalkConfig: unknown SDE form");
+    if (d.kind < SDDG_DENS_RING_W || d.kind > SDDG_DENS_TWOBUMP_W)
+        fail(SDDG_ERR_VALIDATION, "the literal SDE form exists for the BASELINE weights (kinds 16-18)");
+    if (cfg.scheme != SDDG_SCHEME_LINEAR)
+        fail(SDDG_ERR_VALIDATION, "the literal SDE form runs the linear scheme");
+    return 40 + (d.kind - SDDG_DENS_RING_W);  // DV_RING_LIT ..
+}
+
 HostDensity host_density(const sddg_density& d) {
     if (d.kind == SDDG_DENS_TABLE) check_table(d);
     return HostDensity::of(d);
@@ -218,7 +231,12 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     a.bridge_thr = 40.0 * cfg.dt * (1.0 + (cfg.precision == SDDG_FP32 ? 1e-5 : 1e-12));
     // inner box: both endpoints farther than s >= sqrt(bridge_thr) from every
     // edge => every d0*d1 > bridge_thr => no bridge draw possible
-    const double sbox = std::sqrt(a.bridge_thr) * (1.0 + 1e-6);
+    // literal SDE: the bridge threshold scales with w (d0 d1 <= 40 w dt),
+    // so the inner box takes w's maximum (ring 11, shock 21, two-bump < 31)
+    const double wmax = cfg.form == SDDG_FORM_LITERAL
+                            ? (d.kind == SDDG_DENS_RING_W ? 11.0 : (d.kind == SDDG_DENS_SHOCK_W ? 21.0 : 31.0))
+                            : 1.0;
+    const double sbox = std::sqrt(a.bridge_thr * wmax) * (1.0 + 1e-6);
     a.box[0] = dom.xmin + sbox;
     a.box[1] = dom.xmax - sbox;
     a.box[2] = dom.ymin + sbox;
@@ -417,7 +435,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     GatherTargets none;
     none.n_peers = 0;
     none.global_index = nullptr;
-    const int dv = drift_variant(d, cfg.precision);
+    const int dv = walk_variant(d, cfg);
     const int64_t n = static_cast<int64_t>(perm.size());
     c->last_ms = 0.0;
     c->last_steps = 0;
@@ -512,7 +530,7 @@ void estimates_host(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     validate_walk(cfg);
     check_domain(dom);
     check_boundary(bd);
-    drift_variant(d, cfg.precision);
+    walk_variant(d, cfg);
     check_positivity(d, dom);
     check_points(dom, px, py, n);
     if (n <= 0) return;
@@ -1273,7 +1291,7 @@ void make_fm_tables(void* out) {
 }
 
 bool walk_variant_supported(int dv, int precision) {
-    if (dv >= 32 && dv <= 36) return true;  // walk_fast.cu: DV_RING_AN .. DV_TABLE_AN
+    if ((dv >= 32 && dv <= 36) || (dv >= 40 && dv <= 42)) return true;  // walk_fast.cu
     return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18) || dv == 20);
 }
 
@@ -1411,7 +1429,7 @@ sddg_status sddg_mc_estimate_batch_device(sddg_ctx* ctx, const sddg_density* den
     validate_walk(*cfg);
     check_domain(*dom);
     check_boundary(*bd);
-    drift_variant(*dens, cfg->precision);
+    walk_variant(*dens, *cfg);
     check_positivity(*dens, *dom);
     if (n > 0) {
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
@@ -1439,7 +1457,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
     validate_walk(*cfg);
     check_domain(*dom);
     check_boundary(*bd);
-    const int dv = drift_variant(*dens, cfg->precision);
+    const int dv = walk_variant(*dens, *cfg);
     check_positivity(*dens, *dom);
     check_points(*dom, &px, &py, 1);
     if (walk_lo < 0 || walk_lo + n > 0x100000000LL)

@@ -113,6 +113,7 @@ namespace rt {
 // validation (runtime.cu)
 void validate_walk(const sddg_walk_config& c);
 int drift_variant(const sddg_density& d, int precision);
+int walk_variant(const sddg_density& d, const sddg_walk_config& cfg);
 HostDensity host_density(const sddg_density& d);
 void check_positivity(const sddg_density& d, const sddg_domain& dom);
 void check_domain(const sddg_domain& d);

@@ -427,7 +427,7 @@ sddg_status sddg_shard_plan(const sddg_density* dens, const sddg_domain* dom, co
     try {
         check_domain(*dom);
         validate_walk(*cfg);
-        drift_variant(*dens, cfg->precision);
+        walk_variant(*dens, *cfg);
         if (nranks < 1) fail(SDDG_ERR_VALIDATION, "shard_plan: nranks must be >= 1");
         check_points(*dom, px, py, n);
         sddg_ctx scratch;  // host-only: the model cache of a throwaway context

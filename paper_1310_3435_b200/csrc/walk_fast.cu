@@ -1,13 +1,15 @@
 // walk_fast.cu -- K1 instantiations with the analytic drift grad(w)/w of the
 // BASELINE densities (DV 32-34) and the reference's builtin five-ring (DV 35,
 // the paper's own workload) and a tabulated density's interpolant gradient
-// (DV 36), fp64 (fastmath.cuh) and fp32 (BASELINE.json configs 1-5 specify
-// analytic gradients).  FMA contraction allowed.
+// (DV 36), and BASELINE's literal SDE (DV 40-42), fp64 (fastmath.cuh) and
+// fp32 (BASELINE.json configs 1-5 specify analytic gradients).  FMA
+// contraction allowed.
 #include "walk_kernel.cuh"
 
 namespace sddg {
 
-#define SDDG_FAST_VARIANTS(X) X(DV_RING_AN) X(DV_SHOCK_AN) X(DV_TWOBUMP_AN) X(DV_FIVE_RING_AN) X(DV_TABLE_AN)
+#define SDDG_FAST_VARIANTS(X) X(DV_RING_AN) X(DV_SHOCK_AN) X(DV_TWOBUMP_AN) X(DV_FIVE_RING_AN) X(DV_TABLE_AN) \
+    X(DV_RING_LIT) X(DV_SHOCK_LIT) X(DV_TWOBUMP_LIT)
 
 cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s) {
     switch (dv) {

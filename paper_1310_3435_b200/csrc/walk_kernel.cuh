@@ -448,6 +448,7 @@ __device__ __forceinline__ StepRand<Real> step_rand(const fm::FmTables& T, const
 template <typename Real>
 struct StepDrift {
     Real c, vx, vy;  // bx, by in vx, vy for the unscaled forms
+    Real s, w;       // literal SDE: noise scale sqrt(w) and w (the bridge's time scale); else 1
     bool ok;
 };
 
@@ -455,7 +456,15 @@ template <int DV, typename Real, int SCHEME>
 __device__ __forceinline__ StepDrift<Real> step_drift(const fm::FmTables& T, const DensityParams& P, Real dt,
                                                       Real x, Real y) {
     StepDrift<Real> d;
-    if constexpr (SCHEME == 0 && DV >= DV_RING_AN) {
+    d.s = Real(1);
+    d.w = Real(1);
+    if constexpr (kLiteral<DV>) {
+        // BASELINE's literal SDE (linear scheme only, validated on the host)
+        drift_lit(DV, T, x, y, dt, d.c, d.vx, d.vy, d.w);
+        if constexpr (sizeof(Real) == 8) d.s = fm::fsqrt_pos(d.w);
+        else d.s = sqrtf(d.w);
+        d.ok = true;
+    } else if constexpr (SCHEME == 0 && DV >= DV_RING_AN) {
         drift_cv<DV>(T, P, x, y, dt, d.c, d.vx, d.vy);
         d.ok = true;  // closed forms: finite everywhere
     } else {
@@ -471,7 +480,12 @@ template <int DV, typename Real, int SCHEME>
 __device__ __forceinline__ void step_update(const StepDrift<Real>& d, const StepRand<Real>& r, Real dt,
                                             Real sq2dt, Real x, Real y, Real& nxp, Real& nyp) {
     constexpr bool FAST = DV >= DV_RING_AN;
-    if constexpr (SCHEME == 0 && FAST) {
+    if constexpr (SCHEME == 0 && kLiteral<DV>) {
+        // x + grad(w) dt + sqrt(2 w dt) z = x + c v + sqrt(w) R (cs, sn)
+        const Real Rs = r.r0 * d.s;
+        nxp = fma(Rs, r.r2, fma(d.c, d.vx, x));
+        nyp = fma(Rs, r.r1, fma(d.c, d.vy, y));
+    } else if constexpr (SCHEME == 0 && FAST) {
         // x + b dt + sqrt(2 dt) z with b dt = c v and sqrt(2 dt) z = R (cs, sn)
         nxp = fma(r.r0, r.r2, fma(d.c, d.vx, x));
         nyp = fma(r.r0, r.r1, fma(d.c, d.vy, y));
@@ -524,7 +538,7 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
                 const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
                 const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
                 const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
-                if constexpr (FAST && sizeof(Real) == 4 &&
+                if constexpr (FAST && sizeof(Real) == 4 && !kLiteral<DV> &&
                               (SDDG_FP32_BRIDGE_OOL_SHOCK || DV != DV_SHOCK_AN)) {
                     // fp32: out of line (A/B +2.4%); fp64 keeps the inline test below
                     // (out of line it costs the step loop a local-memory round trip: -0.5%)
@@ -713,6 +727,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             // tail kernel so both compute every step bit for bit alike)
             Real nxp, nyp;
             bool ok;
+            Real wl = Real(1);  // literal SDE: w at the step's start (the bridge's time scale)
             {
                 uint64_t w0, w1, w2 = 0;
                 if constexpr (SCHEME == 0) {
@@ -724,6 +739,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                 const StepRand<Real> r = step_rand<DV, Real, SCHEME>(T, a, sq2dt, w0, w1, w2);
                 const StepDrift<Real> sd = step_drift<DV, Real, SCHEME>(T, P, dt, x, y);
                 ok = sd.ok;
+                if constexpr (kLiteral<DV>) wl = sd.w;
                 step_update<DV, Real, SCHEME>(sd, r, dt, sq2dt, x, y, nxp, nyp);
             }
             ++step;
@@ -735,8 +751,9 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             Real hx = Real(0), hy = Real(0);
             int edge = 0;
             bool nb;
-            const bool exited = exit_test<DV, Real, SCHEME, BRIDGE>(dom, a, T, thr, dt, x, y, nxp, nyp, in_box,
-                                                                    rng, hx, hy, edge, nb);
+            const bool exited = exit_test<DV, Real, SCHEME, BRIDGE>(
+                dom, a, T, kLiteral<DV> ? thr * wl : thr, kLiteral<DV> ? dt * wl : dt, x, y, nxp, nyp, in_box, rng,
+                hx, hy, edge, nb);
             if (!exited) {
                 x = nxp;
                 y = nyp;

@@ -178,8 +178,10 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
                 Real hx = Real(0), hy = Real(0);
                 int edge = 0;
                 bool nb;
-                const bool exited = exit_test<DV, Real, SCHEME, BRIDGE>(dom, a, T, thr, dt, x, y, nxp, nyp,
-                                                                        in_box, ws, hx, hy, edge, nb);
+                const Real wl = kLiteral<DV> ? sd.w : Real(1);
+                const bool exited = exit_test<DV, Real, SCHEME, BRIDGE>(
+                    dom, a, T, kLiteral<DV> ? thr * wl : thr, kLiteral<DV> ? dt * wl : dt, x, y, nxp, nyp, in_box,
+                    ws, hx, hy, edge, nb);
                 if (exited) {
                     if (lane == 0) {
                         record_exit<Real>(a, c.g, node, epoch, step, edge, hx, hy, max_steps);

@@ -84,7 +84,7 @@ class _Boundary(C.Structure):
 class _WalkCfg(C.Structure):
     _fields_ = [("scheme", C.c_int32), ("precision", C.c_int32), ("dt", C.c_double),
                 ("lambda_", C.c_double), ("walks", C.c_int64), ("seed", C.c_uint64),
-                ("max_steps", C.c_int64), ("bridge_test", C.c_int32), ("reserved", C.c_int32)]
+                ("max_steps", C.c_int64), ("bridge_test", C.c_int32), ("form", C.c_int32)]
 
 
 class _SolverCfg(C.Structure):
@@ -411,12 +411,14 @@ class WalkConfig:
     max_steps: int = 10_000_000
     bridge_test: bool = True
     precision: str = "fp64"
+    form: str = "reference"  # "literal": BASELINE's dX = grad(w) dt + sqrt(2w) dW (SDDG_FORM_LITERAL)
 
     def c(self):
         sch = {"linear": LINEAR, "exponential": EXPONENTIAL}.get(self.scheme, 99)
         prec = {"fp64": FP64, "fp32": FP32}.get(self.precision, 99)
+        form = {"reference": 0, "literal": 1}.get(self.form, 99)
         return _WalkCfg(sch, prec, self.dt, self.lambda_, int(self.walks), int(self.seed),
-                        int(self.max_steps), 1 if self.bridge_test else 0, 0)
+                        int(self.max_steps), 1 if self.bridge_test else 0, form)
 
 
 @dataclass

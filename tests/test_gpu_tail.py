@@ -40,6 +40,7 @@ CASES = [
     ("five_ring_ref_linear", lambda: sdd.MonitorFunction.five_ring(), FIVE, "linear", (0.1, 0.2)),
     ("table_ref_linear", _table, UNIT, "linear", (0.45, 0.55)),
     ("table_fast_exp", lambda: _table().with_grad(sdd.GRAD_ANALYTIC), UNIT, "exponential", (0.45, 0.55)),
+    ("ring_literal_linear", lambda: sdd.MonitorFunction.ring(analytic=True), UNIT, "literal", (0.5, 0.5)),
 ]
 
 
@@ -48,7 +49,8 @@ def test_dumps_identical_with_and_without_tail(ctx, monkeypatch, case):
     name, mk, dom, scheme, p = case
     m = mk()
     bd = sdd.make_boundary_data(m, sdd.GridSpec(dom, 33, 33))
-    cfg = sdd.WalkConfig(scheme=scheme, dt=1e-4, lambda_=1000.0, walks=1, seed=11)
+    cfg = sdd.WalkConfig(scheme="linear" if scheme == "literal" else scheme, dt=1e-4, lambda_=1000.0, walks=1,
+                         seed=11, form="literal" if scheme == "literal" else "reference")
     for n in (700, 4000):  # all walks handed over / handoff once <= 16 per SM remain
         a, b = _both(monkeypatch, lambda: sdd.walk_dump(p, 4242, m, dom, bd, cfg, 0, n, ctx=ctx))
         assert a.tobytes() == b.tobytes(), name
