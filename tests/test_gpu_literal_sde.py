@@ -5,7 +5,11 @@ functions and the exit law -- hence the estimates -- are the same, while
 walks take fewer steps where w > 1.  No reference implementation exists, so
 the check is statistical against the reference form: 4 combined standard
 errors per node and field, exceedances against the null expectation and
-chi^2/dof."""
+chi^2/dof.  The literal form's step has standard deviation
+sqrt(2 w dt): in the shock layer (w up to 21, width 0.02) it needs a step
+about w_max times smaller for the same discretisation error, which the
+shock case uses (at the reference form's dt the literal walks jump the layer
+and the estimates are biased by many standard errors)."""
 import math
 
 import numpy as np
@@ -26,8 +30,10 @@ def _z(a, b):
     return np.concatenate(z)
 
 
-@pytest.mark.parametrize("kind,n,s", [("ring", 65, 2), ("shock", 129, 4), ("two_bump", 129, 4)])
-def test_literal_form_has_the_reference_exit_law(ctx, kind, n, s):
+@pytest.mark.parametrize("kind,n,s,dt,dt_lit,walks", [("ring", 65, 2, 5e-5, 5e-5, 20_000),
+                                                       ("shock", 129, 4, 1e-5, 5e-7, 5_000),
+                                                       ("two_bump", 129, 4, 5e-5, 5e-5, 20_000)])
+def test_literal_form_has_the_reference_exit_law(ctx, kind, n, s, dt, dt_lit, walks):
     m = getattr(sdd.MonitorFunction, kind)(analytic=True)
     spec = sdd.GridSpec(UNIT, n, n)
     lay = sdd.build_layout(spec, s, s)
@@ -35,16 +41,17 @@ def test_literal_form_has_the_reference_exit_law(ctx, kind, n, s):
     sel = np.linspace(0, len(px) - 1, 40).round().astype(int)
     pts, pid = np.stack([px[sel], py[sel]], 1), pid[sel]
     bd = sdd.make_boundary_data(m, spec)
-    ref = sdd.mc_estimate_batch(pts, pid, m, UNIT, bd, sdd.WalkConfig(scheme="linear", dt=5e-5, walks=20_000,
+    ref = sdd.mc_estimate_batch(pts, pid, m, UNIT, bd, sdd.WalkConfig(scheme="linear", dt=dt, walks=walks,
                                                                       seed=1), ctx=ctx)
     zs = []
     for prec, seed in (("fp64", 2), ("fp32", 3)):
         lit = sdd.mc_estimate_batch(pts, pid, m, UNIT, bd,
-                                    sdd.WalkConfig(scheme="linear", dt=5e-5, walks=20_000, seed=seed,
+                                    sdd.WalkConfig(scheme="linear", dt=dt_lit, walks=walks, seed=seed,
                                                    precision=prec, form="literal"), ctx=ctx)
-        assert (lit["edge_hits"].sum(axis=1) == 20_000).all()
-        # the time change: w >= 1 everywhere, so literal walks are no longer
-        assert lit["path_steps"].sum() < ref["path_steps"].sum()
+        assert (lit["edge_hits"].sum(axis=1) == walks).all()
+        # the time change: w >= 1 everywhere, so at equal dt literal walks are no longer
+        if dt_lit == dt:
+            assert lit["path_steps"].sum() < ref["path_steps"].sum()
         zs.append(_z(lit, ref))
     z = np.concatenate(zs)
     exceed = int(np.sum(np.abs(z) > 4))
