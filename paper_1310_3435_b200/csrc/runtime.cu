@@ -347,7 +347,11 @@ std::vector<uint32_t> cost_order(const std::vector<double>& cost, const std::vec
         perm.resize(cost.size());
         for (size_t k = 0; k < cost.size(); ++k) perm[k] = static_cast<uint32_t>(k);
     }
+    const char* ord = std::getenv("SDDG_NODE_ORDER");  // A/B knob: "reverse" (shortest first), "index"
+    if (ord && std::strcmp(ord, "index") == 0) return perm;
+    const bool rev = ord && std::strcmp(ord, "reverse") == 0;
     std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+        if (rev) return cost[a] < cost[b] || (cost[a] == cost[b] && a < b);
         return cost[a] > cost[b] || (cost[a] == cost[b] && a < b);
     });
     return perm;
