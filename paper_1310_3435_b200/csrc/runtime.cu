@@ -466,6 +466,7 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     a.fm_tables = c->fm_tables.p;
     a.walks = W;
     a.walk_lo = 0;
+    a.n_nodes = n_all;
     a.next = &cnt->next;
     a.steps = &cnt->steps;
     a.node_steps = nst;
@@ -1489,6 +1490,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         a.pid = reinterpret_cast<const uint64_t*>(dn + 2);
         a.walks = n;
         a.walk_lo = walk_lo;
+        a.n_nodes = 1;
         a.total = static_cast<uint64_t>(n);
         a.next = &cnt->next;
         a.steps = &cnt->steps;

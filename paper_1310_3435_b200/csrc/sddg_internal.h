@@ -12,6 +12,26 @@
 #include "philox.cuh"
 #include "table_density.h"
 
+// Device-side bounds checks of a checked build (SDDG_CHECKS=1: build tag
+// "chk", tools/checked_tests.sh).  compute-sanitizer is closed on the GPU
+// pool (profiles/r02_compute_sanitizer_refused.log), so the indices each
+// kernel derives from its inputs are asserted instead; a violation prints
+// the condition and traps the kernel (SDDG_ERR_CUDA on the host).
+#if defined(SDDG_CHECKS) && SDDG_CHECKS
+#include <cstdio>
+#define SDDG_CHECK(cond)                                                                        \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("SDDG_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);               \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define SDDG_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace sddg {
 
 constexpr int kWalkBlock = 128;   // threads per walk CTA
@@ -51,6 +71,7 @@ struct WalkArgs {
     const double* py;
     const uint64_t* pid;
     const uint32_t* perm;  // batch slot -> node (longest expected walks first), or null
+    int64_t n_nodes;       // points px/py/pid/node_steps hold (checked builds)
     int64_t walks;
     int64_t walk_lo;
     uint64_t total;

@@ -93,17 +93,22 @@ void nck(ncclResult_t r, const char* what) {
 }
 
 __global__ void pack_kernel(const sddg_estimate* __restrict__ in, const int* __restrict__ nodes, int count,
-                            sddg_estimate* __restrict__ out) {
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < count; s += gridDim.x * blockDim.x)
+                            int64_t n, sddg_estimate* __restrict__ out) {
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < count; s += gridDim.x * blockDim.x) {
+        SDDG_CHECK(nodes[s] >= 0 && nodes[s] < n);
         out[s] = in[nodes[s]];
+    }
+    (void)n;
 }
 
 __global__ void unpack_kernel(const sddg_estimate* __restrict__ recv, const int* __restrict__ nodes, int slots,
-                              sddg_estimate* __restrict__ out) {
+                              int64_t n, sddg_estimate* __restrict__ out) {
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
         const int k = nodes[s];
+        SDDG_CHECK(k < n);
         if (k >= 0) out[k] = recv[s];
     }
+    (void)n;
 }
 
 int blocks_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1024))); }
@@ -214,7 +219,7 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         launches[m] = mc->last_launches;
         const int cnt = static_cast<int>(lists[r].size());
         if (cnt > 0) {
-            pack_kernel<<<blocks_for(cnt), 256, 0, ms_>>>(out, dn + r * maxc, cnt, recv[m] + r * maxc);
+            pack_kernel<<<blocks_for(cnt), 256, 0, ms_>>>(out, dn + r * maxc, cnt, n, recv[m] + r * maxc);
             ck(cudaGetLastError(), "pack launch");
         }
     });
@@ -239,7 +244,7 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
     for (int m = 1; m < nm; ++m) ck(cudaStreamSynchronize(streams[m]), "member sync");
     // 3. records to their node slots on the owner's device
     unpack_kernel<<<blocks_for(R * maxc), 256, 0, st>>>(recv[0], static_cast<int*>(c->t_nodes.p),
-                                                         static_cast<int>(R * maxc), d_out);
+                                                         static_cast<int>(R * maxc), n, d_out);
     ck(cudaGetLastError(), "unpack launch");
     std::vector<int64_t> steps(n);
     ck(cudaMemcpy2DAsync(steps.data(), sizeof(int64_t), reinterpret_cast<const char*>(d_out) +

@@ -586,6 +586,7 @@ __device__ __forceinline__ void record_exit(const WalkArgs& a, uint64_t g, uint3
     const int tn = horiz ? a.tnx : a.tny;
     const double fv = table_at(a.tf[edge], tn, par);
     const double gv = table_at(a.tg[edge], tn, par);
+    SDDG_CHECK(g < a.total && node < static_cast<uint64_t>(a.n_nodes) && edge >= 0 && edge < 4);
     // restarts happen at exactly max_steps: one atomic per finished walk
     if (a.node_steps)
         atomicAdd(a.node_steps + node, static_cast<unsigned long long>(epoch) * max_steps + step);
@@ -704,6 +705,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
         auto start_walk = [&](uint64_t g) {
             const uint64_t slot = g / static_cast<uint64_t>(a.walks);
             const uint32_t node = a.perm ? a.perm[slot] : static_cast<uint32_t>(slot);
+            SDDG_CHECK(g < a.total && node < static_cast<uint64_t>(a.n_nodes));
             L.node = node;
             L.walk = static_cast<uint32_t>(a.walk_lo + (g - slot * a.walks));
             L.epoch = 0;
@@ -770,6 +772,7 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
                     if (*reinterpret_cast<volatile unsigned long long*>(a.next) >= a.total &&
                         *reinterpret_cast<volatile unsigned long long*>(a.live) <= a.cont_cap) {
                         const uint32_t k = atomicAdd(a.n_cont, 1u);
+                        SDDG_CHECK(done < max_steps);
                         if (k < a.cont_cap) {
                             WalkCont& c = a.cont[k];
                             c.x = static_cast<double>(x);

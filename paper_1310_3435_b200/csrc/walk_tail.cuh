@@ -37,6 +37,7 @@ struct WindowStream {
     // draw idx of the window, idx - base in [0, 64); idx may differ per lane
     __device__ __forceinline__ uint64_t word(uint32_t idx) const {
         const uint32_t k = idx - base;
+        SDDG_CHECK(k < 64u);
         const int src = static_cast<int>((k >> 1) & 31u);
         const uint64_t a = __shfl_sync(0xffffffffu, lo, src);
         const uint64_t b = __shfl_sync(0xffffffffu, hi, src);
@@ -134,6 +135,8 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
          ci += gridDim.x * kTailWarps) {
         const WalkCont c = a.cont[ci];
         const uint32_t node = c.node;
+        SDDG_CHECK(ci < a.cont_cap && node < static_cast<uint64_t>(a.n_nodes) && c.g < a.total &&
+                   c.step < max_steps && c.epoch < 1024u);
         const uint64_t pid = a.pid[node];
         Real x = Real(c.x), y = Real(c.y);
         uint32_t epoch = c.epoch, step = c.step, n = c.n;
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
             // ---- steps while the window holds this step's draws and up to 4 exit-test draws
             while (ws.n - base + kDraws + 4u <= 64u) {
                 const uint32_t k = ws.n - base;
+                SDDG_CHECK(k < 64u);
                 const StepRand<Real> r = shfl_rand<Real>(k < 32u ? rr[0] : rr[1], static_cast<int>(k & 31u));
                 const StepDrift<Real> sd = tail_drift<DV, Real, SCHEME>(T, P, dt, x, y);
                 Real nxp, nyp;
