@@ -40,6 +40,12 @@ __global__ void set_next_kernel(Counters* c, unsigned long long v, unsigned long
     c->next = v;
     c->live = live;
     c->n_cont = 0;
+    for (int r = 0; r < kMaxDrain; ++r) c->n_drain[r] = 0;
+}
+
+// drain round start: the walks in flight are the previous round's handoffs
+__global__ void drain_prep_kernel(Counters* c, const unsigned int* n_src, unsigned int cap) {
+    c->live = min(*n_src, cap);
 }
 
 thread_local std::string g_free_err;
@@ -401,33 +407,109 @@ void raise_kernel_error(const Counters& hc) {
                                 std::to_string(hc.err_info) + ", not the compiled SDDG_SMEM_ABS");
 }
 
-// The tail kernel (walk_tail.cuh) for fp64 walks: a handoff buffer of one
-// walk per warp of one 16-warp CTA per SM, for batches of at most
-// kTailWalksPerLane walks per K1 lane (larger batches, whose tail is a small
-// share, keep the plain K1 loop: 1.5 instructions per step fewer).
-// SDDG_NO_TAIL=1: K1 alone.
-constexpr uint64_t kTailWalksPerLane = 32;
+// The batch tail for fp64 walks (batches of at most kTailWalksPerLane walks
+// per K1 lane; larger batches, whose tail is a small share, keep the plain K1
+// loop: 1.5 instructions per step fewer).  Once K1's batch counter has run
+// out, its lanes empty out while the longest walks run on: warps keep issuing
+// every step for a few live lanes.  So at check points (every chunk32 steps)
+// the walks still running move on, in stages:
+//  * drain rounds: K1 resumed on the previous stage's handoffs, packed 32 per
+//    warp and spread over the SMs (SDDG_DRAIN: the per-SM caps, decreasing;
+//    default "256": K1 hands over once <= 256 walks per SM are in flight; a
+//    list "256,64" adds a round that repacks again at 64, ...; "" none).
+//    Config 1: 18.6 -> 16.6 ms (tools/tail_ab.py; a second round or an earlier
+//    first one measured no better);
+//  * the tail kernel (walk_tail.cuh), one warp per walk, for the last
+//    SDDG_TAIL_PER_SM (16) walks per SM.
+// Every stage runs the same step functions on the same draws, so results do
+// not depend on where a walk finished.  SDDG_NO_TAIL=1: K1 alone.
+constexpr uint64_t kTailWalksPerLane = 128;  // one GPU's share of config 2 at N = 8 (62 per lane): -0.8%
 
-void enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt, uint64_t lanes) {
+DrainPlan enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt, uint64_t lanes) {
+    DrainPlan dp;
     a.cont = nullptr;
     a.cont_cap = 0;
+    a.src = nullptr;
+    a.n_src = nullptr;
+    a.src_cap = 0;
     a.chunk32 = a.max_steps32;
-    if (precision != SDDG_FP64 || std::getenv("SDDG_NO_TAIL")) return;
+    if (precision != SDDG_FP64 || std::getenv("SDDG_NO_TAIL")) return dp;
     const char* wpl = std::getenv("SDDG_TAIL_WALKS_PER_LANE");  // A/B knob
     const uint64_t max_wpl = wpl ? std::strtoull(wpl, nullptr, 10) : kTailWalksPerLane;
-    if (a.total > max_wpl * lanes) return;
+    if (a.total > max_wpl * lanes) return dp;
     // K1's check points every chunk32 steps: the largest of 256, 128, 64
     // dividing max_steps (the restart must still fall on a chunk end)
     uint32_t chunk = 256;
     while (chunk >= 64 && a.max_steps32 % chunk != 0) chunk /= 2;
-    if (chunk < 64 || chunk >= a.max_steps32) return;
+    if (chunk < 64 || chunk >= a.max_steps32) return dp;
     a.chunk32 = chunk;
-    const char* per_sm = std::getenv("SDDG_TAIL_PER_SM");  // A/B knob: walks handed over per SM
-    const uint32_t cap = static_cast<uint32_t>(c->sms) * (per_sm ? std::max(1, std::atoi(per_sm)) : 16);
-    a.cont = static_cast<WalkCont*>(c->tail_cont.ensure(sizeof(WalkCont) * cap));
-    a.cont_cap = cap;
+    const uint32_t sms = static_cast<uint32_t>(c->sms);
+    const char* per_sm = std::getenv("SDDG_TAIL_PER_SM");  // A/B knob: walks handed to K1t per SM
+    const uint32_t tail_sm = per_sm ? static_cast<uint32_t>(std::max(1, std::atoi(per_sm))) : 16u;
+    std::vector<uint32_t> caps;  // per SM, decreasing, above the tail's
+    const char* drain = std::getenv("SDDG_DRAIN");
+    std::string spec = drain ? drain : "256";
+    for (size_t p = 0; p < spec.size();) {
+        const size_t q = std::min(spec.find(',', p), spec.size());
+        const long v = std::strtol(spec.substr(p, q - p).c_str(), nullptr, 10);
+        if (v > static_cast<long>(tail_sm) && (caps.empty() || static_cast<uint32_t>(v) < caps.back()) &&
+            static_cast<uint64_t>(v) * sms < lanes && caps.size() < static_cast<size_t>(kMaxDrain))
+            caps.push_back(static_cast<uint32_t>(v));
+        p = q + 1;
+    }
+    caps.push_back(tail_sm);
+    dp.rounds = static_cast<int>(caps.size()) - 1;
+    size_t total = 0;
+    for (uint32_t v : caps) total += static_cast<size_t>(v) * sms;
+    WalkCont* buf = static_cast<WalkCont*>(c->tail_cont.ensure(sizeof(WalkCont) * total));
+    for (size_t r = 0; r < caps.size(); ++r) {
+        dp.cap[r] = caps[r] * sms;
+        dp.buf[r] = buf;
+        buf += dp.cap[r];
+    }
+    a.cont = dp.buf[0];
+    a.cont_cap = dp.cap[0];
     a.n_cont = &cnt->n_cont;
     a.live = &cnt->live;
+    return dp;
+}
+
+// K1 on a batch set up by set_next_kernel, then its drain rounds and the tail
+// kernel; `after_k1` (optional) is recorded between K1 and the rest.  Returns
+// the kernels launched.
+int launch_walk_stages(sddg_ctx* c, int dv, int precision, const WalkArgs& a, const DrainPlan& dp, int grid,
+                       Counters* cnt, cudaStream_t st, cudaEvent_t after_k1) {
+    ck(launch_walk(dv, precision, a, grid, st), "walk kernel launch");
+    if (!a.cont) return 1;
+    if (after_k1) ck(cudaEventRecord(after_k1, st), "event");
+    int launches = 1;
+    WalkArgs b = a;
+    const unsigned int* n_prev = &cnt->n_cont;
+    for (int r = 1; r <= dp.rounds; ++r) {
+        b.src = dp.buf[r - 1];
+        b.n_src = n_prev;
+        b.src_cap = dp.cap[r - 1];
+        b.cont = dp.buf[r];
+        b.cont_cap = dp.cap[r];
+        b.n_cont = &cnt->n_drain[r - 1];
+        drain_prep_kernel<<<1, 1, 0, st>>>(cnt, b.n_src, b.src_cap);
+        ck(cudaGetLastError(), "drain prep");
+        // one CTA per SM holding its share of the handoffs, 32 walks per warp
+        const uint32_t per_sm = (b.src_cap + c->sms - 1) / c->sms;
+        const int block = static_cast<int>(std::min<uint32_t>((per_sm + 31) / 32 * 32, static_cast<uint32_t>(kDrainBlock)));
+        const int g = static_cast<int>((b.src_cap + block - 1) / block);
+        ck(launch_walk(dv, precision, b, g, st, block), "drain round launch");
+        n_prev = b.n_cont;
+        launches += 2;
+    }
+    b.src = nullptr;
+    b.n_src = nullptr;
+    b.src_cap = 0;
+    b.cont = dp.buf[dp.rounds];
+    b.cont_cap = dp.cap[dp.rounds];
+    b.n_cont = const_cast<unsigned int*>(n_prev);
+    ck(launch_walk_tail(dv, b, st), "tail kernel launch");
+    return launches + 1;
 }
 
 // Walks + finalize for n device-resident nodes; estimates to d_out.
@@ -492,16 +574,15 @@ void run_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         a.total = static_cast<uint64_t>(nb) * W;
         const auto [grid, blk] = walk_grid(c, dv, cfg.precision, a.total);
         const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
-        enable_tail(c, a, cfg.precision, cnt, lanes);
+        const DrainPlan dp = enable_tail(c, a, cfg.precision, cnt, lanes);
         set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaGetLastError(), "set_next");
         ck(cudaEventRecord(c->bev[3 * bi], st), "event");
-        ck(launch_walk(dv, cfg.precision, a, grid, st), "walk kernel launch");
-        ck(cudaEventRecord(c->bev[3 * bi + 1], st), "event");
-        ck(launch_walk_tail(dv, a, st), "tail kernel launch");
+        launches += launch_walk_stages(c, dv, cfg.precision, a, dp, grid, cnt, st, c->bev[3 * bi + 1]);
+        if (!a.cont) ck(cudaEventRecord(c->bev[3 * bi + 1], st), "event");
         ck(cudaEventRecord(c->bev[3 * bi + 2], st), "event");
         ck(launch_reduce(rf, rg, rm, W, nb, dperm + b, nst, d_out, st, gt ? *gt : none), "reduce launch");
-        launches += a.cont ? 4 : 3;
+        launches += 2;
     }
     Counters hc;
     ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "read counters");
@@ -1300,10 +1381,10 @@ bool walk_variant_supported(int dv, int precision) {
     return precision == SDDG_FP64 && ((dv >= 0 && dv <= 4) || (dv >= 16 && dv <= 18) || dv == 20);
 }
 
-cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s, int block) {
     if (!walk_variant_supported(dv, precision)) return cudaErrorInvalidValue;
-    if (dv >= 32) return launch_walk_fast(dv, precision, a, grid, s);
-    return launch_walk_ref(dv, a, grid, s);
+    if (dv >= 32) return launch_walk_fast(dv, precision, a, grid, s, block);
+    return launch_walk_ref(dv, a, grid, s, block);
 }
 
 cudaError_t launch_walk_tail(int dv, const WalkArgs& a, cudaStream_t s) {
@@ -1499,11 +1580,10 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         a.dump = dd;
         const auto [grid, blk] = walk_grid(ctx, dv, cfg->precision, a.total);
         const unsigned long long lanes = static_cast<unsigned long long>(grid) * blk;
-        enable_tail(ctx, a, cfg->precision, cnt, lanes);
+        const DrainPlan dp = enable_tail(ctx, a, cfg->precision, cnt, lanes);
         set_next_kernel<<<1, 1, 0, st>>>(cnt, lanes, std::min<unsigned long long>(lanes, a.total));
         ck(cudaEventRecord(ctx->ev0, st), "event");
-        ck(launch_walk(dv, cfg->precision, a, grid, st), "walk kernel launch");
-        ck(launch_walk_tail(dv, a, st), "tail kernel launch");
+        const int nl = launch_walk_stages(ctx, dv, cfg->precision, a, dp, grid, cnt, st, nullptr);
         ck(cudaEventRecord(ctx->ev1, st), "event");
         Counters hc;
         ck(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st), "d2h");
@@ -1513,7 +1593,7 @@ sddg_status sddg_walk_dump(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
         cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
         ctx->last_ms = ms;
         ctx->last_steps = static_cast<int64_t>(hc.steps);
-        ctx->last_launches = a.cont ? 3 : 2;
+        ctx->last_launches = nl + 1;
         ctx->last_handoffs = a.cont ? std::min<int64_t>(hc.n_cont, a.cont_cap) : 0;
         ctx->last_tail_ms = 0.0;
         raise_kernel_error(hc);

@@ -57,11 +57,21 @@ struct DevBuf {
     }
 };
 
+constexpr int kMaxDrain = 4;  // drain rounds between K1 and the tail kernel
+// The stages after K1 of a small fp64 batch (runtime.cu enable_tail): handoff
+// caps (total walks) and buffers of K1 (0), the drain rounds (1..rounds) and
+// the tail kernel's input (rounds)
+struct DrainPlan {
+    int rounds = 0;
+    uint32_t cap[kMaxDrain + 1] = {};
+    struct WalkCont* buf[kMaxDrain + 1] = {};
+};
 struct Counters {
     unsigned long long next, steps, err_info;
     int err_flag;
-    unsigned int n_cont;     // walks handed to the tail kernel
+    unsigned int n_cont;     // walks handed over by K1
     unsigned long long live;  // walks in flight once the batch counter has run out
+    unsigned int n_drain[kMaxDrain];  // walks handed over by drain round r
 };
 
 // Expected first-exit time T(x) of the walk dX = grad(w)/w dt + sqrt(2) dW

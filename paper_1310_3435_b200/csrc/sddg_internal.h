@@ -34,6 +34,7 @@
 
 namespace sddg {
 
+constexpr int kDrainBlock = 256;  // threads per CTA of a drain round (walk_kernel.cuh DRAIN)
 constexpr int kWalkBlock = 128;   // threads per walk CTA
 #ifndef SDDG_WALK_MIN_BLOCKS
 #define SDDG_WALK_MIN_BLOCKS 8
@@ -92,6 +93,11 @@ struct WalkArgs {
     uint32_t cont_cap;
     unsigned int* n_cont;
     unsigned long long* live;
+    // drain round (K1 resumed on a previous round's handoffs, packed 32 per
+    // warp): src[0 .. min(*n_src, src_cap)); null: a fresh batch
+    const struct WalkCont* src;
+    const unsigned int* n_src;
+    uint32_t src_cap;
     double inv_dt;          // 1/dt: performance-mode bridge exponent d0 d1 / dt as a multiply
     double half_inv_lambda; // 1/(2 lambda): performance-mode Exp(lambda) step from -2 ln u
 };
@@ -101,16 +107,17 @@ void make_fm_tables(void* host_tables7680);
 
 // walk_ref.cu (fp64, -fmad=false) and walk_fast.cu (analytic drifts, fp64 + fp32)
 bool walk_variant_supported(int dv, int precision);
-cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
+// block > 0: CTAs of that many threads (a drain round), else the variant's own
+cudaError_t launch_walk(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s, int block = 0);
 // the tail kernel of an fp64 walk batch (walk_tail.cuh), after launch_walk
 cudaError_t launch_walk_tail(int dv, const WalkArgs& a, cudaStream_t s);
 cudaError_t launch_walk_tail_ref(int dv, const WalkArgs& a, cudaStream_t s);
 cudaError_t launch_walk_tail_fast(int dv, const WalkArgs& a, cudaStream_t s);
 cudaError_t walk_occupancy(int dv, int precision, int* blocks_per_sm, int* block);
 // the two TUs' own dispatchers
-cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s, int block);
 cudaError_t occupancy_walk_ref(int dv, int* b, int* block);
-cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s, int block);
 cudaError_t occupancy_walk_fast(int dv, int precision, int* b, int* block);
 
 // reduce.cu: K2 fixed chunk-order finalize, one CTA per node; with peers,

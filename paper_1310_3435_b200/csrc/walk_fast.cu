@@ -11,10 +11,10 @@ namespace sddg {
 #define SDDG_FAST_VARIANTS(X) X(DV_RING_AN) X(DV_SHOCK_AN) X(DV_TWOBUMP_AN) X(DV_FIVE_RING_AN) X(DV_TABLE_AN) \
     X(DV_RING_LIT) X(DV_SHOCK_LIT) X(DV_TWOBUMP_LIT)
 
-cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_walk_fast(int dv, int precision, const WalkArgs& a, int grid, cudaStream_t s, int block) {
     switch (dv) {
-#define X(V) case V: return precision == SDDG_FP64 ? launch_variant<V, double>(a, grid, s) \
-                                                   : launch_variant<V, float>(a, grid, s);
+#define X(V) case V: return precision == SDDG_FP64 ? launch_variant<V, double>(a, grid, s, block) \
+                                                   : launch_variant<V, float>(a, grid, s, block);
         SDDG_FAST_VARIANTS(X)
 #undef X
     }

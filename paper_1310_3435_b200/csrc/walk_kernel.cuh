@@ -653,10 +653,14 @@ static_assert(sizeof(fm::FmTables) % 16 == 0, "LaneState alignment after the tab
 // the step loop counts chunks of a.chunk32 steps with check points between
 // them.  Without TAIL the loop is the plain one (1.5 instructions per step
 // fewer: the large batches, where the tail is a negligible share).
-template <int DV, typename Real, int SCHEME, bool BRIDGE, bool TAIL = false>
-__global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Real>())
+// DRAIN: a drain round (a.src set): the same loop on a few walks per SM, where
+// a step's latency, not issue, bounds it -- so compiled for kDrainBlock-thread
+// CTAs, with the registers to overlap the step's random-number and drift chains.
+template <int DV, typename Real, int SCHEME, bool BRIDGE, bool TAIL = false, bool DRAIN = false>
+__global__ void __launch_bounds__(DRAIN ? kDrainBlock : walk_block<DV, Real>(), DRAIN ? 1 : walk_min_blocks<DV, Real>())
     walk_kernel(const __grid_constant__ WalkArgs a) {
     static_assert(!TAIL || kTailHandoff<Real>, "tail handoff is fp64 only");
+    static_assert(!DRAIN || TAIL, "drain rounds hand over to the tail kernel");
     constexpr bool FAST = DV >= DV_RING_AN;
     using Ops = RealOps<Real, FAST>;
     const Dom<Real> dom = walk_dom<Real>(a);
@@ -698,7 +702,17 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
     LaneState& L = lane_state[threadIdx.x];
     L.g = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     L.steps = 0;
-    if (L.g < a.total) {
+    // drain round: walk ci of the previous round's handoffs, 32 per warp, the
+    // warps dealt round-robin over the CTAs (one CTA per SM)
+    uint32_t ci = 0;
+    bool have = L.g < a.total;
+    if constexpr (DRAIN) {
+        {
+            ci = (((threadIdx.x >> 5) * gridDim.x + blockIdx.x) << 5) + (threadIdx.x & 31);
+            have = ci < min(*a.n_src, a.src_cap);
+        }
+    }
+    if (have) {
         Real x, y;
         LaneStream rng;
         // ---- walk setup (re-entered for every new walk)
@@ -714,7 +728,32 @@ __global__ void __launch_bounds__(walk_block<DV, Real>(), walk_min_blocks<DV, Re
             y = Real(a.py[node]);
             rng.init(a.rk, a.pid[node], L.walk, 0);
         };
-        start_walk(L.g);
+        bool resumed = false;
+        if constexpr (DRAIN) {
+            {
+                // the walk as handed over at a check point: position, stream
+                // position (and the cached half block of an odd one), chunks done
+                const WalkCont c = a.src[ci];
+                SDDG_CHECK(c.g < a.total && c.node < static_cast<uint64_t>(a.n_nodes) && c.epoch < 1024u &&
+                           c.step < max_steps && c.step % a.chunk32 == 0);
+                L.g = c.g;
+                L.node = c.node;
+                L.walk = c.walk;
+                L.epoch = c.epoch;
+                L.base = c.step;
+                x = Real(c.x);
+                y = Real(c.y);
+                rng.init(a.rk, a.pid[c.node], c.walk, c.epoch);
+                rng.n = c.n;
+                if (c.n & 1u) {
+                    const PhiloxWords w = rng.block(a.rk, c.n >> 1);
+                    rng.cw2 = w.w2;
+                    rng.cw3 = w.w3;
+                }
+                resumed = true;
+            }
+        }
+        if (!resumed) start_walk(L.g);
         bool in_box = box_test<DV, Real>(dom, x, y);
         uint32_t step = 0;
         // `step` counts the steps of the current chunk of a.chunk32 steps;
@@ -835,8 +874,8 @@ constexpr size_t walk_smem() {
     return walk_table_bytes<DV, Real>() + sizeof(LaneState) * walk_block<DV, Real>();
 }
 
-template <int DV, typename Real, int SCHEME, bool BRIDGE, bool TAIL = false>
-cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
+template <int DV, typename Real, int SCHEME, bool BRIDGE, bool TAIL = false, bool DRAIN = false>
+cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s, int block = 0) {
     constexpr size_t sm = walk_smem<DV, Real>();
     if constexpr (sm > 48 * 1024) {
         // once per device and variant (a process may drive several devices
@@ -845,14 +884,17 @@ cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_relaxed)) {
-            const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE, TAIL>,
+            const cudaError_t e = cudaFuncSetAttribute(walk_kernel<DV, Real, SCHEME, BRIDGE, TAIL, DRAIN>,
                                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        static_cast<int>(sm));
             if (e != cudaSuccess) return e;
             if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_relaxed);
         }
     }
-    walk_kernel<DV, Real, SCHEME, BRIDGE, TAIL><<<grid, walk_block<DV, Real>(), sm, s>>>(a);
+    // a drain round: CTAs of `block` threads, smem for their lanes only
+    const int blk = DRAIN ? std::min(block, kDrainBlock) : walk_block<DV, Real>();
+    walk_kernel<DV, Real, SCHEME, BRIDGE, TAIL, DRAIN>
+        <<<grid, blk, walk_table_bytes<DV, Real>() + sizeof(LaneState) * blk, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -863,8 +905,13 @@ cudaError_t launch_one(const WalkArgs& a, int grid, cudaStream_t s) {
 namespace sddg {
 
 template <int DV, typename Real>
-cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_variant(const WalkArgs& a, int grid, cudaStream_t s, int block = 0) {
     if constexpr (kTailHandoff<Real>) {
+        if (a.src) {
+            if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false, true, true>(a, grid, s, block);
+            if (a.bridge) return launch_one<DV, Real, 0, true, true, true>(a, grid, s, block);
+            return launch_one<DV, Real, 0, false, true, true>(a, grid, s, block);
+        }
         if (a.cont) {
             if (a.scheme == SDDG_SCHEME_EXPONENTIAL) return launch_one<DV, Real, 1, false, true>(a, grid, s);
             if (a.bridge) return launch_one<DV, Real, 0, true, true>(a, grid, s);

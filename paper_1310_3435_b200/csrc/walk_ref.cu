@@ -12,9 +12,9 @@ namespace sddg {
 #define SDDG_REF_VARIANTS(X) X(DV_CONSTANT) X(DV_RUNNING) X(DV_HUANG_SLOAN) X(DV_MACKENZIE) \
     X(DV_FIVE_RING) X(DV_RING_FD) X(DV_SHOCK_FD) X(DV_TWOBUMP_FD) X(DV_TABLE_FD)
 
-cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s) {
+cudaError_t launch_walk_ref(int dv, const WalkArgs& a, int grid, cudaStream_t s, int block) {
     switch (dv) {
-#define X(V) case V: return launch_variant<V, double>(a, grid, s);
+#define X(V) case V: return launch_variant<V, double>(a, grid, s, block);
         SDDG_REF_VARIANTS(X)
 #undef X
     }

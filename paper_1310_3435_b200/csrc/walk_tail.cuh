@@ -85,16 +85,6 @@ __device__ __forceinline__ StepDrift<Real> tail_drift(const fm::FmTables& T, con
     }
 }
 
-template <typename Real>
-__device__ __forceinline__ StepRand<Real> shfl_rand(const StepRand<Real>& r, int src) {
-    StepRand<Real> o;
-    o.edt = __shfl_sync(0xffffffffu, r.edt, src);
-    o.r0 = __shfl_sync(0xffffffffu, r.r0, src);
-    o.r1 = __shfl_sync(0xffffffffu, r.r1, src);
-    o.r2 = __shfl_sync(0xffffffffu, r.r2, src);
-    return o;
-}
-
 template <int DV, typename Real, int SCHEME, bool BRIDGE>
 __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __grid_constant__ WalkArgs a) {
     static_assert(sizeof(Real) == 8, "the tail kernel runs fp64 walks");
@@ -121,7 +111,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
     }
 #endif
     const uint32_t ncont = min(*reinterpret_cast<volatile unsigned int*>(a.n_cont), a.cont_cap);
-    if (blockIdx.x * kTailWarps >= ncont) return;
+    if (blockIdx.x >= ncont) return;
     if constexpr (walk_uses_tables<DV, Real>()) {
         const double2* src = reinterpret_cast<const double2*>(a.fm_tables);
         double2* dst = reinterpret_cast<double2*>(dyn_smem);
@@ -131,8 +121,17 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
     }
     const uint32_t lane = threadIdx.x & 31;
     constexpr uint32_t kDraws = kStepDraws<SCHEME>;
-    for (uint32_t ci = blockIdx.x * kTailWarps + (threadIdx.x >> 5); ci < ncont;
-         ci += gridDim.x * kTailWarps) {
+    // the warp's step randoms of the current window, slot = draw offset: read
+    // by every lane at one broadcast address (no shuffle, whose divergence
+    // check and latency would sit on the step chain)
+    StepRand<Real>* const rbuf = reinterpret_cast<StepRand<Real>*>(
+                                     reinterpret_cast<char*>(dyn_smem) + walk_table_bytes<DV, Real>()) +
+                                 64 * (threadIdx.x >> 5);
+    // walks round-robin over the SMs first, then over the CTA's warps (warp w
+    // issues on SM sub-partition w % 4): a tail of a few hundred walks runs one
+    // walk per sub-partition, where a step costs its dependency chain (~230
+    // clocks, tools/op_latency.cu), not four walks' share of the FP64 pipe
+    for (uint32_t ci = (threadIdx.x >> 5) * gridDim.x + blockIdx.x; ci < ncont; ci += gridDim.x * kTailWarps) {
         const WalkCont c = a.cont[ci];
         const uint32_t node = c.node;
         SDDG_CHECK(ci < a.cont_cap && node < static_cast<uint64_t>(a.n_nodes) && c.g < a.total &&
@@ -142,6 +141,12 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
         uint32_t epoch = c.epoch, step = c.step, n = c.n;
         uint64_t extra = 0;  // steps of the epochs restarted here
         bool in_box = box_test<DV, Real>(dom, x, y);
+        // the drift at the walk's position is computed one step ahead: right
+        // after the update, before the exit test's branch, so its dependent
+        // chain overlaps the step's bookkeeping and branches instead of
+        // following them (a pure function of the position: values unchanged;
+        // the speculative one at an exit position is never used)
+        StepDrift<Real> sd = tail_drift<DV, Real, SCHEME>(T, P, dt, x, y);
         bool done = false;
         while (!done) {
             // ---- window: 32 Philox blocks of the stream (seed, pid, walk, epoch)
@@ -151,7 +156,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
             WindowStream ws{n, base, join64(w.w0, w.w1), join64(w.w2, w.w3)};
             // this lane's step randoms at draw positions base + lane, base + lane + 32
             // (the last few positions run past the window: never used)
-            StepRand<Real> rr[2];
+            __syncwarp();  // the previous window's reads are done
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const uint32_t s0 = base + lane + 32u * e;
@@ -159,18 +164,14 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
                 const uint64_t w0 = ws.word(min(s0, lim));
                 const uint64_t w1 = ws.word(min(s0 + 1u, lim));
                 const uint64_t w2 = kDraws > 2 ? ws.word(min(s0 + 2u, lim)) : 0ull;
-                rr[e] = step_rand<DV, Real, SCHEME>(T, a, sq2dt, w0, w1, w2);
+                rbuf[lane + 32u * e] = step_rand<DV, Real, SCHEME>(T, a, sq2dt, w0, w1, w2);
             }
+            __syncwarp();
+            uint32_t k = ws.n - base;
+            StepRand<Real> r = rbuf[k & 63u];
             // ---- steps while the window holds this step's draws and up to 4 exit-test draws
-            while (ws.n - base + kDraws + 4u <= 64u) {
-                const uint32_t k = ws.n - base;
+            while (k + kDraws + 4u <= 64u) {
                 SDDG_CHECK(k < 64u);
-                const StepRand<Real> r = shfl_rand<Real>(k < 32u ? rr[0] : rr[1], static_cast<int>(k & 31u));
-                const StepDrift<Real> sd = tail_drift<DV, Real, SCHEME>(T, P, dt, x, y);
-                Real nxp, nyp;
-                step_update<DV, Real, SCHEME>(sd, r, dt, sq2dt, x, y, nxp, nyp);
-                ws.n += kDraws;
-                ++step;
                 if (!sd.ok) {
                     if (lane == 0) {
                         atomicCAS(a.err_flag, 0, 3);  // EvaluationError
@@ -179,6 +180,15 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
                     done = true;
                     break;
                 }
+                Real nxp, nyp;
+                step_update<DV, Real, SCHEME>(sd, r, dt, sq2dt, x, y, nxp, nyp);
+                ws.n += kDraws;
+                ++step;
+                // the next step's randoms, assuming the exit test draws nothing
+                // (k past the window: stale, and the loop refills instead)
+                k = ws.n - base;
+                StepRand<Real> rn = rbuf[k & 63u];
+                const StepDrift<Real> sn = tail_drift<DV, Real, SCHEME>(T, P, dt, nxp, nyp);
                 Real hx = Real(0), hy = Real(0);
                 int edge = 0;
                 bool nb;
@@ -197,6 +207,12 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
                 x = nxp;
                 y = nyp;
                 in_box = nb;
+                sd = sn;
+                if (ws.n - base != k) {  // the exit test drew: reload
+                    k = ws.n - base;
+                    rn = rbuf[k & 63u];
+                }
+                r = rn;
                 if (step >= max_steps) {
                     // restart on the next epoch's stream (run_walk, sde.cpp:154-182)
                     extra += step;
@@ -211,6 +227,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
                     x = Real(a.px[node]);
                     y = Real(a.py[node]);
                     in_box = box_test<DV, Real>(dom, x, y);
+                    sd = tail_drift<DV, Real, SCHEME>(T, P, dt, x, y);
                     step = 0;
                     ws.n = 0;
                     break;  // new key: a new window
@@ -223,7 +240,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
 
 template <int DV, typename Real, int SCHEME, bool BRIDGE>
 cudaError_t launch_tail_one(const WalkArgs& a, cudaStream_t s) {
-    constexpr size_t sm = walk_table_bytes<DV, Real>();
+    constexpr size_t sm = walk_table_bytes<DV, Real>() + sizeof(StepRand<Real>) * 64 * kTailWarps;
     if constexpr (sm > 48 * 1024) {
         static std::atomic<bool> attr[64];
         int dev = 0;
@@ -237,11 +254,11 @@ cudaError_t launch_tail_one(const WalkArgs& a, cudaStream_t s) {
         }
     }
     // one CTA per SM (cont_cap = 16 per SM by default); a larger cap queues
-    // the walks of a warp (grid-stride over the continuations)
+    // walks on a warp (strided over the continuations)
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = std::min<unsigned>((a.cont_cap + kTailWarps - 1) / kTailWarps, static_cast<unsigned>(sms));
+    const unsigned grid = std::min<unsigned>(a.cont_cap, static_cast<unsigned>(sms));
     walk_tail_kernel<DV, Real, SCHEME, BRIDGE><<<grid, kTailWarps * 32, sm, s>>>(a);
     return cudaGetLastError();
 }

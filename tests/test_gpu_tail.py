@@ -71,7 +71,7 @@ def test_estimates_and_path_steps_identical(ctx, monkeypatch):
     (a, sa), (b, sb) = _both(monkeypatch, run)
     assert a.tobytes() == b.tobytes()
     assert sa["path_steps"] == sb["path_steps"] == int(a["path_steps"].sum())
-    assert sa["launches"] == sb["launches"] + 1  # the tail kernel
+    assert sa["launches"] >= sb["launches"] + 1  # the tail kernel (+ drain rounds)
 
 
 def test_restarts_in_the_tail(ctx, monkeypatch):

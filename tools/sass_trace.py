@@ -16,8 +16,8 @@ from collections import Counter
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_1310_3435_b200", "_lib", "libsddg.so")
-KERNELS = {"fp64_ring": "_ZN4sddg11walk_kernelILi32EdLi0ELb1ELb0EEEvNS_8WalkArgsE",
-           "fp32_shock": "_ZN4sddg11walk_kernelILi33EfLi0ELb1ELb0EEEvNS_8WalkArgsE"}
+KERNELS = {"fp64_ring": "_ZN4sddg11walk_kernelILi32EdLi0ELb1ELb0ELb0EEEvNS_8WalkArgsE",
+           "fp32_shock": "_ZN4sddg11walk_kernelILi33EfLi0ELb1ELb0ELb0EEEvNS_8WalkArgsE"}
 FP64 = ("DFMA", "DMUL", "DADD", "DSETP")
 
 
