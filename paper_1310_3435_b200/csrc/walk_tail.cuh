@@ -170,6 +170,10 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
             uint32_t k = ws.n - base;
             StepRand<Real> r = rbuf[k & 63u];
             // ---- steps while the window holds this step's draws and up to 4 exit-test draws
+#ifndef SDDG_TAIL_UNROLL
+#define SDDG_TAIL_UNROLL 1
+#endif
+            SDDG_UNROLL(SDDG_TAIL_UNROLL)
             while (k + kDraws + 4u <= 64u) {
                 SDDG_CHECK(k < 64u);
                 if (!sd.ok) {

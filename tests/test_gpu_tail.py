@@ -96,3 +96,26 @@ def test_numerical_error_raised_from_the_tail(ctx, monkeypatch):
     monkeypatch.delenv("SDDG_NO_TAIL", raising=False)
     with pytest.raises(sdd.NumericalError):
         sdd.mc_estimate((0.5, 0.5), 1, m, UNIT, bd, cfg, ctx=ctx)
+
+
+@pytest.mark.parametrize("drain,rounds", [("", 0), ("256,64,32", 3), ("2000", 0)])
+def test_drain_rounds_identical(ctx, monkeypatch, drain, rounds):
+    # a batch larger than K1's lanes, so its counter runs out while walks are
+    # in flight: drain rounds (K1 resumed on its handoffs, repacked) none,
+    # three, or a cap above K1's lane count (ignored); estimates, per-node
+    # path-steps and the step total unchanged
+    m = sdd.MonitorFunction.ring(analytic=True)
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(UNIT, 33, 33))
+    cfg = sdd.WalkConfig(scheme="linear", dt=1e-4, walks=50_000, seed=5)
+    pts = [(0.45, 0.5), (0.5, 0.2), (0.3, 0.7), (0.6, 0.6)]
+    monkeypatch.setenv("SDDG_NO_TAIL", "1")
+    ref = sdd.mc_estimate_batch(pts, [1, 2, 3, 4], m, UNIT, bd, cfg, ctx=ctx)
+    s_ref = ctx.last_stats()
+    monkeypatch.delenv("SDDG_NO_TAIL")
+    monkeypatch.setenv("SDDG_DRAIN", drain)
+    e = sdd.mc_estimate_batch(pts, [1, 2, 3, 4], m, UNIT, bd, cfg, ctx=ctx)
+    st = ctx.last_stats()
+    assert e.tobytes() == ref.tobytes()
+    assert st["path_steps"] == s_ref["path_steps"]
+    assert st["launches"] == s_ref["launches"] + 1 + 2 * rounds
+    assert st["tail_handoffs"] > 0
