@@ -641,6 +641,9 @@ def main():
             plan = sdd.plan_interface_points(place, k, m, lay)
             wc = sdd.WalkConfig(scheme="linear", dt=dt, walks=walks, seed=1, precision=args.precision)
             sc = sdd.SolverConfig(tol=1e-10, method="rbsor")
+            # warm-up with 1,000 paths per node (module loads, buffers of this shape)
+            sdd.solve_sdd(m, lay, plan, sdd.WalkConfig(scheme="linear", dt=dt, walks=1000, seed=2,
+                                                       precision=args.precision), sc, ctx=ctx)
             r = sdd.solve_sdd(m, lay, plan, wc, sc, ctx=ctx)
             mesh[name] = {"t_stoc_s": r.t_stoc, "t_sub_s": r.t_sub, "t_total_s": r.t_stoc + r.t_sub,
                           "mc_points": r.mc_points, "paths_per_node": walks,

@@ -194,6 +194,13 @@ sddg_status sddg_probe_onchip_bandwidth(sddg_ctx* ctx, double* l2_gbps, double* 
  * against the CUDA library; slot 5: max ulp error of log on (0.9, 1). */
 sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[6]);
 
+/* Diagnostics: n operand pairs (random over the parity mode's guarded range,
+ * quotients just below 1 with the dividend near the top of its binade,
+ * operands outside the guard, zeros, subnormals) through the parity mode's
+ * shared-reciprocal division; *mismatches = results that differ from the
+ * library's correctly rounded a / b in any bit (expected 0). */
+sddg_status sddg_selftest_division(sddg_ctx* ctx, int64_t n, uint64_t* mismatches);
+
 /* ------------------------------------------------------------- walk seams */
 
 /* Replaces the per-node loop of sdd::mc_estimate calls

@@ -148,6 +148,7 @@ cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double*
 }  // namespace sddg
 
 // ---- accuracy self-test of fastmath.cuh against the CUDA library
+#include "density.cuh"
 #include "fastmath.cuh"
 
 namespace sddg {
@@ -217,6 +218,59 @@ cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long*
     fastmath_check<<<static_cast<unsigned>(blocks), 256, sm>>>(
         n, static_cast<const fm::FmTables*>(tables), d);
     e = cudaMemcpy(host_maxulp6, d, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
+
+// ---- the parity mode's shared-reciprocal division (density.cuh
+// div_rn_shared) against the library's correctly rounded a / b, bit for bit:
+// random operands over the guarded range, quotients near the top of the binade
+// with a/b < 1 (where q0 = RN(a RN(1/b)) is furthest off), operands outside
+// the guard (library fallback), zeros of both signs and subnormals.
+__global__ void division_check(int64_t n, unsigned long long* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t h = static_cast<uint64_t>(i) * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+        auto mix = [&h]() {
+            h ^= h >> 31;
+            h *= 0xBF58476D1CE4E5B9ull;
+            h ^= h >> 29;
+            h *= 0x94D049BB133111EBull;
+            h ^= h >> 32;
+            return h;
+        };
+        const uint64_t r1 = mix(), r2 = mix(), r3 = mix();
+        const uint64_t m1 = r1 & 0xFFFFFFFFFFFFFull, m2 = r2 & 0xFFFFFFFFFFFFFull;
+        const int kind = static_cast<int>(r3 & 7u);
+        double a, b;
+        if (kind <= 3) {  // a, b in [1, 2) x 2^e, e in [-60, 60)
+            a = __longlong_as_double(static_cast<long long>((uint64_t(1023 + (r3 >> 8) % 120 - 60) << 52) | m1));
+            b = __longlong_as_double(static_cast<long long>((uint64_t(1023 + (r3 >> 16) % 120 - 60) << 52) | m2));
+        } else if (kind <= 5) {  // a near 2 in its binade, b slightly above a: a/b just below 1
+            a = __longlong_as_double(static_cast<long long>((uint64_t(1023) << 52) | (0xFFFFFFFFFFFFFull - (m1 >> 30))));
+            b = a * (1.0 + 0x1p-40 * static_cast<double>(m2 >> 20));
+        } else if (kind == 6) {  // wide exponents, inside and outside the guard
+            a = __longlong_as_double(static_cast<long long>((uint64_t(1 + (r3 >> 8) % 2045) << 52) | m1));
+            b = __longlong_as_double(static_cast<long long>((uint64_t(1 + (r3 >> 24) % 2045) << 52) | m2));
+        } else {  // zeros and subnormals
+            a = (r3 >> 8) & 1u ? 0.0 : __longlong_as_double(static_cast<long long>(m1));
+            b = __longlong_as_double(static_cast<long long>((uint64_t(1023 + (r3 >> 16) % 40 - 20) << 52) | m2));
+        }
+        if ((r3 >> 40) & 1u) a = -a;
+        if ((r3 >> 41) & 1u) b = -b;
+        const double q = div_rn_shared(a, b, 1.0 / b), lib = a / b;
+        if (__double_as_longlong(q) != __double_as_longlong(lib) && !(q == 0.0 && lib == 0.0))
+            atomicAdd(bad, 1ull);
+    }
+}
+
+cudaError_t division_selftest(int64_t n, unsigned long long* host_bad) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(unsigned long long));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, sizeof(unsigned long long));
+    division_check<<<148 * 8, 256>>>(n, d);
+    e = cudaMemcpy(host_bad, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     cudaFree(d);
     return e;
 }

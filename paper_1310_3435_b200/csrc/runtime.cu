@@ -1497,6 +1497,15 @@ sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[6]
     API_END(ctx)
 }
 
+sddg_status sddg_selftest_division(sddg_ctx* ctx, int64_t n, uint64_t* mismatches) {
+    API_BEGIN(ctx)
+    if (n < 0 || !mismatches) fail(SDDG_ERR_VALIDATION, "selftest_division: n >= 0 and an output pointer");
+    unsigned long long m = 0;
+    ck(division_selftest(n, &m), "division self-test");
+    *mismatches = m;
+    API_END(ctx)
+}
+
 sddg_status sddg_mc_estimate_batch(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                                    const sddg_boundary* bd, const sddg_walk_config* cfg,
                                    const double* px, const double* py, const uint64_t* pid,

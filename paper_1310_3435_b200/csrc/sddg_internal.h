@@ -209,5 +209,6 @@ cudaError_t launch_linf(const double* X, const double* Y, const double* RX, cons
 cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tflops);
 cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double* smem_gbps);
 cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long* host_maxulp5);
+cudaError_t division_selftest(int64_t n, unsigned long long* host_bad);
 
 }  // namespace sddg

@@ -419,6 +419,17 @@ def test_fastmath_accuracy(ctx):
     assert log_abs_near1 <= 4096, list(m)  # cancellation near u = 1: <= 1e-12 relative
 
 
+def test_parity_division_correctly_rounded(ctx):
+    # density.cuh div_rn_shared (the parity mode's drift quotients from one
+    # shared reciprocal) equals the library's a / b in every bit on 2^28
+    # operand pairs, including the quotients just below 1 with the dividend
+    # near the top of its binade, where RN(a RN(1/b)) is furthest from a/b
+    import ctypes as C
+    bad = C.c_uint64(0)
+    sdd._check(sdd.lib().sddg_selftest_division(ctx.handle, C.c_int64(1 << 28), C.byref(bad)), ctx.handle)
+    assert bad.value == 0
+
+
 def test_config3_fp32_vs_fp64_exceedances_against_null(ctx):
     # at config 3's 14,273 nodes x 2 fields, count |z| > 4 between
     # independent fp32 and fp64 estimates against the H0 expectation
