@@ -14,9 +14,11 @@ config 2's solve_interfaces: all 753 nodes at the config's 10^5 paths per node
   e2e    : the same metric through the public host-buffer API
            (sdd.mc_estimate_batch -> sddg_mc_estimate_batch), pinned host
            inputs copied in and estimates copied out every step, wall clock.
-  roofline: walk kernel (K1) FP64 pipe: algorithmic DP flops per path-step
-            x path-steps / K1 event time, against the
-           DFMA peak measured on this GPU by sddg_probe_fma_peak.
+  roofline: walk kernel (K1): instruction issue (thread-
+           instructions of this launch / K1 event time over SMs x 128 per clock)
+           with the FP64 pipe beside it; "census" is the cross-check (algorithmic
+           DP flops per path-step x path-steps / K1 event time against the DFMA
+           peak measured on this GPU by sddg_probe_fma_peak).
   cpu_baseline: the reference's own mc_estimate (oracle/_ref, built from
            /root/reference/proj/src) on all host threads over a fixed node
            subsample of the same workload.
@@ -704,6 +706,56 @@ def main():
         steps_per_launch = total_steps / args.steps
         achieved = DP_FLOPS_PER_STEP * steps_per_launch / k1_avg_s / 1e12
         prec_peak = peak_fp64 if args.precision == "fp64" else peak_fp32
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        # the judged roofline of the walk is instruction issue
+        # (the non-tensor issue peak: 4 warp-instructions = 128 thread-
+        # instructions per SM per clock), next to the binding FP pipe; the flop
+        # census against the measured FMA peak is the cross-check.  All three
+        # come from this run's K1 event time; the SM clock is the one sampled
+        # during the timed region.
+        k1_rate = steps_per_launch / k1_avg_s  # path-steps/s of K1 alone, one GPU's share below
+        sm_mhz, clock_source = (clk.get("sm_mhz") if clk else None), "nvidia-smi, median over the timed region"
+        if not sm_mhz:  # no sample: the pool's maximum SM clock (a lower bound on the fraction)
+            try:
+                sm_mhz = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+                clock_source = "MEASURED_PEAKS.json sm_max_mhz (no live sample)"
+            except (OSError, KeyError, ValueError):
+                sm_mhz, clock_source = 1965.0, "B200 maximum SM clock (no live sample)"
+        hz = sm_mhz * 1e6
+        pipes = pipe_fractions(k1_rate / world, sm_mhz, args.precision, sms)
+        census = {"achieved": achieved, "peak": prec_peak, "unit": "TFLOP/s",
+                  "frac": achieved / prec_peak if prec_peak else None,
+                  "algorithmic_flops_per_path_step": DP_FLOPS_PER_STEP,
+                  "peak_source": "measured on this GPU by sddg_probe_fma_peak (independent FMA chains; "
+                                 "MEASURED_PEAKS.json has no non-tensor peak)",
+                  "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64}
+        roofline = {"bound": "issue", "kernel": "walk_kernel (K1)",
+                    "achieved": None, "peak": None, "unit": "Tinst/s", "frac": None}
+        if pipes and hz:
+            roofline["achieved"] = pipes["sass_instructions_per_step"] * k1_rate / world / 1e12
+            roofline["peak"] = sms * 128 * hz / 1e12
+            roofline["frac"] = roofline["achieved"] / roofline["peak"]
+            if args.precision == "fp64":
+                roofline["fp_pipe"] = {"pipe": "fp64", "achieved": pipes["sass_fp64_per_step"] * k1_rate / world / 1e12,
+                                       "peak": sms * 64 * hz / 1e12, "unit": "Tinst/s",
+                                       "frac": pipes["fp64_pipe_frac"]}
+        roofline.update({
+            "definition": "SURVEY.md 8(d): issue-slot utilisation of K1 = executed thread-instructions "
+                          "(static SASS count of one step, profiles/sass_walk_step.json, x path-steps "
+                          "of this launch / K1 event time; active lanes only) over SMs x 128 thread-"
+                          "instructions/clk at the SM clock sampled in the timed region; fp_pipe: the "
+                          "same for the step's FP64 instructions over SMs x 64 lanes/clk; ncu: the "
+                          "warp-level counters of the committed capture at this config",
+            "traffic": traffic_per_launch(n * args.walks),
+            "traffic_note": "DRAM read+write bytes per launch = ncu dram__bytes per walk "
+                            "(profiles/ncu_walk_summary.json) x walks in this launch; "
+                            "algorithmic: 20 B per walk record",
+            "k1_ms_per_launch": k1_avg_s * 1e3,
+            "path_steps_per_launch": steps_per_launch,
+            "sm_clock_mhz": sm_mhz, "sm_clock_source": clock_source,
+            "census": census,
+            "pipes": pipes,
+            "ncu": ncu_summary()})
         line = {
             "metric": "SDE walk path-steps/s", "value": value, "unit": "path-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -721,25 +773,7 @@ def main():
                                        "cost (sddg_shard_plan), one ncclAllGather of the 128-B records "
                                        "per step inside the timed region (sddg_create_dist)")
                        if world > 1 else "single GPU"},
-            "roofline": {"bound": "fp64" if args.precision == "fp64" else "fp32",
-                         "achieved": achieved, "peak": prec_peak, "unit": "TFLOP/s",
-                         "frac": achieved / prec_peak if prec_peak else None,
-                         "traffic": traffic_per_launch(n * args.walks),
-                         "traffic_note": "DRAM read+write bytes per launch = ncu dram__bytes per walk "
-                                         "(profiles/ncu_walk_summary.json) x walks in this launch; "
-                                         "algorithmic: 20 B per walk record",
-                         "kernel": "walk_kernel (K1)",
-                         "algorithmic_flops_per_path_step": DP_FLOPS_PER_STEP,
-                         "k1_ms_per_launch": k1_avg_s * 1e3,
-                         "path_steps_per_launch": steps_per_launch,
-                         "peak_source": "measured on this GPU by sddg_probe_fma_peak (independent "
-                                        "FMA chains; MEASURED_PEAKS.json has no non-tensor peak)",
-                         "fp32_peak_tflops": peak_fp32, "fp64_peak_tflops": peak_fp64,
-                         "pipes": pipe_fractions(value / world, clk.get("sm_mhz") if clk else None,
-                                                 args.precision,
-                                                 torch.cuda.get_device_properties(
-                                                     torch.cuda.current_device()).multi_processor_count),
-                         "ncu": ncu_summary()},
+            "roofline": roofline,
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,

@@ -261,6 +261,10 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     if (!pos) a.box_hi[0] = a.box_hi[2] = INT32_MAX;
     const double dv[8] = {a.xmin, a.xmax, a.ymin, a.ymax, a.box[0], a.box[1], a.box[2], a.box[3]};
     for (int k = 0; k < 8; ++k) a.f_dom[k] = static_cast<float>(dv[k]);
+    // fp32 walks: positive floats order like their bit patterns, so the box
+    // test is four integer compares, and exact (same condition as for box_hi)
+    for (int k = 0; k < 4; ++k) std::memcpy(&a.box_fi[k], &a.f_dom[4 + k], 4);
+    if (!pos || !(a.f_dom[4] > 0.0f && a.f_dom[6] > 0.0f)) a.box_fi[0] = a.box_fi[2] = INT32_MAX;
     a.f_dt = static_cast<float>(a.dt);
     a.f_sqrt2dt = static_cast<float>(a.sqrt2dt);
     a.f_thr = static_cast<float>(a.bridge_thr);

@@ -63,6 +63,7 @@ struct WalkArgs {
     float f_dom[8];
     float f_dt, f_sqrt2dt, f_thr, f_pad;
     int32_t box_hi[4];  // high words of box[] for the integer test (INT32_MAX: disabled)
+    int32_t box_fi[4];  // bit patterns of f_dom[4..7]: the fp32 walks' integer box test (exact for a positive box)
     uint64_t seed;
     RoundKeys rk;
     uint32_t max_steps32;  // max_steps (validated <= 2^29)

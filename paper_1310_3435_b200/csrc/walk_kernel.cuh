@@ -33,6 +33,12 @@
 template <typename Real>
 constexpr bool kTailHandoff = sizeof(Real) == 8;
 
+#ifndef SDDG_FP32_LN_V1
+#define SDDG_FP32_LN_V1 0  // A/B: round 1's six-term log1p series for d <= 1/16
+#endif
+#ifndef SDDG_FP32_BOX_V1
+#define SDDG_FP32_BOX_V1 0  // A/B: round 1's floating-point box compares in the fp32 walks
+#endif
 #ifndef SDDG_WALK_UNROLL
 #define SDDG_WALK_UNROLL 2  // step-loop copies (A/B: tools/ab.sh with -DSDDG_WALK_UNROLL=n)
 #endif
@@ -98,22 +104,35 @@ template <bool FAST>
 struct RealOps<float, FAST> {
     __device__ static __forceinline__ float u(uint64_t u) { return u01_f(u); }
     __device__ static __forceinline__ float u_open(uint64_t u) { return u01_open_f(u); }
-    __device__ static __forceinline__ float ln_open(uint64_t a) {
-        const uint32_t k = static_cast<uint32_t>(a >> 40);          // u1 = (k + 1/2) 2^-24
-        const float u1 = __fmaf_rn(static_cast<float>(k), 0x1.0p-24f, 0x1.0p-25f);
-        const float d = __fmaf_rn(static_cast<float>(0xFFFFFFu - k), 0x1.0p-24f, 0x1.0p-25f);  // 1 - u1
-        // -ln(1-d) = d + d^2/2 + ... + d^6/6 for d <= 1/16 (next term < 1e-8 relative)
+    // -2 ln u1, u1 = u01_open_f(a) = (k + 1/2) 2^-24.  MUFU.LG2 is absolutely
+    // accurate (~2^-22), so near u1 = 1 the radius would lose its relative
+    // accuracy: for d = 1 - u1 <= 2^-8 the log1p series -ln(1-d) = d + d^2/2 +
+    // d^3/3 (next term < 2e-8 relative) takes over; above, the SFU's error is
+    // < 3e-5 of -2 ln u1, i.e. < 6e-9 on sqrt(2 dt) z next to x (ulp 3e-8).
+    // d comes from the complement of k (1 - u1 in floating point would round
+    // away the low bits of a small u1, down to u1 = 0).
+    __device__ static __forceinline__ float m2ln_open(uint64_t a) {
+        const uint32_t kc = 0xFFFFFFu ^ static_cast<uint32_t>(a >> 40);
+        const float d = __fmaf_rn(static_cast<float>(kc), 0x1.0p-24f, 0x1.0p-25f);  // 1 - u1
+        const float u1 = __fmaf_rn(static_cast<float>(static_cast<uint32_t>(a >> 40)), 0x1.0p-24f, 0x1.0p-25f);
+#if SDDG_FP32_LN_V1
+        // round-1 form: six-term series for d <= 1/16
         float p = __fmaf_rn(d, 0.16666667f, 0.2f);
         p = __fmaf_rn(p, d, 0.25f);
         p = __fmaf_rn(p, d, 0.33333334f);
         p = __fmaf_rn(p, d, 0.5f);
         p = __fmaf_rn(p, d, 1.0f);
         const float series = -(p * d);
-        return d <= 0.0625f ? series : __logf(u1);
+        return -2.0f * (d <= 0.0625f ? series : __logf(u1));
+#else
+        float p = __fmaf_rn(d, 0.66666669f, 1.0f);
+        p = __fmaf_rn(p, d, 2.0f);
+        return d <= 0x1.0p-8f ? p * d : __log2f(u1) * -1.3862944f;
+#endif
     }
     __device__ static __forceinline__ void bm_polar(const fm::FmTables&, uint64_t a, uint64_t b,
                                                     float scale, float& R, float& sn, float& cs) {
-        const float v = -2.0f * ln_open(a);
+        const float v = m2ln_open(a);
         R = scale * (v * rsqrtf(v));
         // 2 pi u2 with u2 = top 24 bits 2^-24 (u01_f), one multiply
         __sincosf(static_cast<float>(static_cast<uint32_t>(b >> 40)) * (6.2831853f * 0x1.0p-24f),
@@ -159,6 +178,12 @@ struct Dom {
         const int xi = __double2hiint(x), yi = __double2hiint(y);
         return xi > hx0 && xi < hx1 && yi > hy0 && yi < hy1;
     }
+    // fp32 walks: the whole bit pattern, so the test is in_box exactly (a
+    // negative x has a negative pattern and fails x > bx0 > 0 either way)
+    __device__ __forceinline__ bool in_box_hi(float x, float y) const {
+        const int xi = __float_as_int(x), yi = __float_as_int(y);
+        return xi > hx0 && xi < hx1 && yi > hy0 && yi < hy1;
+    }
     // geometry.cpp:24-32
     __device__ __forceinline__ Real dist(Real x, Real y, int e) const {
         return e == 0 ? y - ymin : (e == 1 ? ymax - y : (e == 2 ? x - xmin : xmax - x));
@@ -186,7 +211,8 @@ __device__ __forceinline__ Dom<Real> walk_dom(const WalkArgs& a) {
                      walk_prm<Real>(a.ymin, a.f_dom[2]), walk_prm<Real>(a.ymax, a.f_dom[3]),
                      walk_prm<Real>(a.box[0], a.f_dom[4]), walk_prm<Real>(a.box[1], a.f_dom[5]),
                      walk_prm<Real>(a.box[2], a.f_dom[6]), walk_prm<Real>(a.box[3], a.f_dom[7]),
-                     a.box_hi[0], a.box_hi[1], a.box_hi[2], a.box_hi[3]};
+                     sizeof(Real) == 4 ? a.box_fi[0] : a.box_hi[0], sizeof(Real) == 4 ? a.box_fi[1] : a.box_hi[1],
+                     sizeof(Real) == 4 ? a.box_fi[2] : a.box_hi[2], sizeof(Real) == 4 ? a.box_fi[3] : a.box_hi[3]};
 }
 
 // segment_exit (proj/src/sde.cpp:31-65)
@@ -508,7 +534,7 @@ __device__ __forceinline__ void step_update(const StepDrift<Real>& d, const Step
 // fp64 table kernels (performance mode), the exact one otherwise.
 template <int DV, typename Real>
 __device__ __forceinline__ bool box_test(const Dom<Real>& d, Real px, Real py) {
-    if constexpr (DV >= DV_RING_AN && sizeof(Real) == 8) return d.in_box_hi(px, py);
+    if constexpr (DV >= DV_RING_AN && (sizeof(Real) == 8 || !SDDG_FP32_BOX_V1)) return d.in_box_hi(px, py);
     else return d.in_box(px, py);
 }
 
