@@ -268,6 +268,9 @@ void fill_args(WalkArgs& a, const sddg_density& d, const sddg_domain& dom,
     a.f_dt = static_cast<float>(a.dt);
     a.f_sqrt2dt = static_cast<float>(a.sqrt2dt);
     a.f_thr = static_cast<float>(a.bridge_thr);
+    a.f_kd = d.kind == SDDG_DENS_RING_W    ? static_cast<float>(-8000.0 * a.dt)
+             : d.kind == SDDG_DENS_SHOCK_W ? static_cast<float>(1.0 / (-160.0 * a.dt))
+                                           : static_cast<float>(-3000.0 * a.dt);
     a.seed = cfg.seed;
     a.rk = make_round_keys(cfg.seed);
     a.max_steps32 = static_cast<uint32_t>(cfg.max_steps);  // <= 2^29 (validate_walk)

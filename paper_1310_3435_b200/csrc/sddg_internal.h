@@ -61,7 +61,8 @@ struct WalkArgs {
     // converting the doubles in the step loop): xmin, xmax, ymin, ymax, box[4],
     // dt, sqrt2dt, bridge_thr
     float f_dom[8];
-    float f_dt, f_sqrt2dt, f_thr, f_pad;
+    float f_dt, f_sqrt2dt, f_thr;
+    float f_kd;  // fp32 linear-scheme drift constant times dt: ring -8000 dt, shock 1/(-160 dt), two-bump -3000 dt
     int32_t box_hi[4];  // high words of box[] for the integer test (INT32_MAX: disabled)
     int32_t box_fi[4];  // bit patterns of f_dom[4..7]: the fp32 walks' integer box test (exact for a positive box)
     uint64_t seed;

@@ -39,6 +39,9 @@ constexpr bool kTailHandoff = sizeof(Real) == 8;
 #ifndef SDDG_FP32_BOX_V1
 #define SDDG_FP32_BOX_V1 0  // A/B: round 1's floating-point box compares in the fp32 walks
 #endif
+#ifndef SDDG_SHOCK64_LIGHT
+#define SDDG_SHOCK64_LIGHT 0
+#endif
 #ifndef SDDG_WALK_UNROLL
 #define SDDG_WALK_UNROLL 2  // step-loop copies (A/B: tools/ab.sh with -DSDDG_WALK_UNROLL=n)
 #endif
@@ -133,7 +136,11 @@ struct RealOps<float, FAST> {
     __device__ static __forceinline__ void bm_polar(const fm::FmTables&, uint64_t a, uint64_t b,
                                                     float scale, float& R, float& sn, float& cs) {
         const float v = m2ln_open(a);
+#if SDDG_FP32_LN_V1
         R = scale * (v * rsqrtf(v));
+#else
+        R = scale * sqrt_approx(v);  // one MUFU.SQRT (v >= 2^-24 > 0)
+#endif
         // 2 pi u2 with u2 = top 24 bits 2^-24 (u01_f), one multiply
         __sincosf(static_cast<float>(static_cast<uint32_t>(b >> 40)) * (6.2831853f * 0x1.0p-24f),
                   &sn, &cs);
@@ -491,7 +498,10 @@ __device__ __forceinline__ StepDrift<Real> step_drift(const fm::FmTables& T, con
         else d.s = sqrtf(d.w);
         d.ok = true;
     } else if constexpr (SCHEME == 0 && DV >= DV_RING_AN) {
-        drift_cv<DV>(T, P, x, y, dt, d.c, d.vx, d.vy);
+        if constexpr (sizeof(Real) == 4 && (DV == DV_RING_AN || DV == DV_SHOCK_AN || DV == DV_TWOBUMP_AN))
+            drift_cv<DV, true>(T, P, x, y, dt, d.c, d.vx, d.vy);
+        else
+            drift_cv<DV>(T, P, x, y, dt, d.c, d.vx, d.vy);
         d.ok = true;  // closed forms: finite everywhere
     } else {
         d.c = Real(0);
@@ -644,7 +654,11 @@ constexpr bool kBigTables = sizeof(fm::FmTables) > 24 * 1024;
 // drifts that need more than 64 registers in the fp64 table kernel
 template <int DV>
 __host__ __device__ constexpr bool walk_heavy_drift() {
+#if SDDG_SHOCK64_LIGHT  // A/B: the one-reciprocal shock drift in the 1024-thread, 64-register shape
+    return DV == DV_FIVE_RING_AN || DV == DV_TABLE_AN;
+#else
     return DV == DV_SHOCK_AN || DV == DV_FIVE_RING_AN || DV == DV_TABLE_AN;
+#endif
 }
 template <int DV, typename Real>
 __host__ __device__ constexpr int walk_block() {
@@ -690,7 +704,7 @@ __global__ void __launch_bounds__(DRAIN ? kDrainBlock : walk_block<DV, Real>(), 
     constexpr bool FAST = DV >= DV_RING_AN;
     using Ops = RealOps<Real, FAST>;
     const Dom<Real> dom = walk_dom<Real>(a);
-    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab};
+    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab, a.f_kd};
     const Real dt = walk_prm<Real>(a.dt, a.f_dt);
     const Real sq2dt = walk_prm<Real>(a.sqrt2dt, a.f_sqrt2dt);
     const Real thr = walk_prm<Real>(a.bridge_thr, a.f_thr);

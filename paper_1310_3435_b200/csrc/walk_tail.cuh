@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1) walk_tail_kernel(const __g
     const Dom<Real> dom{Real(a.xmin), Real(a.xmax), Real(a.ymin), Real(a.ymax),
                         Real(a.box[0]), Real(a.box[1]), Real(a.box[2]), Real(a.box[3]),
                         a.box_hi[0], a.box_hi[1], a.box_hi[2], a.box_hi[3]};
-    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab};
+    const DensityParams P{a.R, a.alpha, a.fd_h, 1.0 / (2.0 * a.fd_h), a.tab, a.f_kd};
     const Real dt = Real(a.dt);
     const Real sq2dt = Real(a.sqrt2dt);
     const Real thr = Real(a.bridge_thr);
