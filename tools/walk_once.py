@@ -1,5 +1,8 @@
 """Run one walk batch of a BASELINE config (for ncu captures):
-python tools/walk_once.py {config2|config3|config5} {fp64|fp32} WALKS"""
+python tools/walk_once.py {config2|config3|config5|five|fivelin} {fp64|fp32} WALKS
+(five: the paper-table workload's walks -- five-ring density on [-1,1]^2, 77^2
+grid split 4x4, exponential stepping lambda = 1000; fivelin: the same nodes
+with the linear scheme, dt = 1e-4)"""
 import os
 import sys
 
@@ -11,7 +14,12 @@ from paper_1310_3435_b200 import sdd  # noqa: E402
 cfgname, prec, walks = sys.argv[1], sys.argv[2], int(sys.argv[3])
 ctx = sdd.Context(0)
 UNIT = sdd.RectDomain(0, 1, 0, 1)
-if cfgname == "config3":
+scheme, lam = "linear", 1000.0
+if cfgname in ("five", "fivelin"):
+    UNIT = sdd.RectDomain(-1, 1, -1, 1)
+    m, grid, subs, dt = sdd.MonitorFunction.five_ring(analytic=True), 77, 4, 1e-4
+    scheme = "exponential" if cfgname == "five" else "linear"
+elif cfgname == "config3":
     m, grid, subs, dt = sdd.MonitorFunction.shock(analytic=True), 1025, 8, 1e-5
 elif cfgname == "config2":
     m, grid, subs, dt = sdd.MonitorFunction.ring(analytic=True), 129, 4, 2e-5
@@ -26,7 +34,7 @@ else:
     lay = sdd.build_layout(spec, subs, subs)
     px, py, pid = sdd.interface_nodes(m, lay, sdd.plan_interface_points("all", 0, m, lay))
     pts = np.stack([px, py], 1)
-cfg = sdd.WalkConfig(scheme="linear", dt=dt, walks=walks, seed=1, precision=prec)
+cfg = sdd.WalkConfig(scheme=scheme, dt=dt, lambda_=lam, walks=walks, seed=1, precision=prec)
 for _ in range(2):
     sdd.mc_estimate_batch(pts, pid, m, UNIT, bd, cfg, ctx=ctx)
     st = ctx.last_stats()
