@@ -684,7 +684,11 @@ __host__ __device__ constexpr int walk_min_blocks() {
 #define SDDG_SHOCK32_MIN_BLOCKS 7  // 7 x 128 threads per SM: ptxas keeps the shock fp32 loop <= 72 registers
 #endif
     if constexpr (DV == DV_SHOCK_AN && sizeof(Real) == 4) return SDDG_SHOCK32_MIN_BLOCKS;
-    return (walk_heavy_drift<DV>() || DV < DV_RING_AN) ? 5 : kWalkMinBlocks;
+#ifndef SDDG_REF_MIN_BLOCKS
+#define SDDG_REF_MIN_BLOCKS 5  // reference-mode (parity) kernels: 128-thread CTAs per SM (A/B)
+#endif
+    if constexpr (DV < DV_RING_AN) return SDDG_REF_MIN_BLOCKS;
+    return walk_heavy_drift<DV>() ? 5 : kWalkMinBlocks;
 }
 
 template <int DV, typename Real>

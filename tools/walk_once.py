@@ -21,6 +21,8 @@ if cfgname in ("five", "fivelin"):
     scheme = "exponential" if cfgname == "five" else "linear"
 elif cfgname == "config3":
     m, grid, subs, dt = sdd.MonitorFunction.shock(analytic=True), 1025, 8, 1e-5
+elif cfgname == "config2fd":  # the parity mode: the reference's FD drift of rho = 1/w
+    m, grid, subs, dt = sdd.MonitorFunction.ring(analytic=False), 129, 4, 2e-5
 elif cfgname == "config2":
     m, grid, subs, dt = sdd.MonitorFunction.ring(analytic=True), 129, 4, 2e-5
 else:
