@@ -685,7 +685,10 @@ __host__ __device__ constexpr int walk_min_blocks() {
 #endif
     if constexpr (DV == DV_SHOCK_AN && sizeof(Real) == 4) return SDDG_SHOCK32_MIN_BLOCKS;
 #ifndef SDDG_REF_MIN_BLOCKS
-#define SDDG_REF_MIN_BLOCKS 5  // reference-mode (parity) kernels: 128-thread CTAs per SM (A/B)
+// reference-mode (parity) kernels: 128-thread CTAs per SM.  A/B (tools/ab_walk.sh, profiles/r02_ref_blocks_ab.log):
+// 3/4/5/6/7/8/10 CTAs -> FD ring 2.43/2.55/2.68/2.70/2.74/2.77/2.75e10 at 2,000 paths (8: +8% at 1e4 paths);
+// the 64-register cap spills 40-130 B, and the warps to hide the FP64 chains are worth more
+#define SDDG_REF_MIN_BLOCKS 8
 #endif
     if constexpr (DV < DV_RING_AN) return SDDG_REF_MIN_BLOCKS;
     return walk_heavy_drift<DV>() ? 5 : kWalkMinBlocks;

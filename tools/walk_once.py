@@ -1,5 +1,5 @@
 """Run one walk batch of a BASELINE config (for ncu captures):
-python tools/walk_once.py {config2|config3|config5|five|fivelin} {fp64|fp32} WALKS
+python tools/walk_once.py {config2|config2fd|config3|config5|five|fivelin|fiveref} {fp64|fp32} WALKS
 (five: the paper-table workload's walks -- five-ring density on [-1,1]^2, 77^2
 grid split 4x4, exponential stepping lambda = 1000; fivelin: the same nodes
 with the linear scheme, dt = 1e-4)"""
@@ -15,10 +15,15 @@ cfgname, prec, walks = sys.argv[1], sys.argv[2], int(sys.argv[3])
 ctx = sdd.Context(0)
 UNIT = sdd.RectDomain(0, 1, 0, 1)
 scheme, lam = "linear", 1000.0
-if cfgname in ("five", "fivelin"):
+if cfgname in ("five", "fivelin", "fiveref"):  # fiveref: the reference-mode drift (parity mode)
     UNIT = sdd.RectDomain(-1, 1, -1, 1)
-    m, grid, subs, dt = sdd.MonitorFunction.five_ring(analytic=True), 77, 4, 1e-4
-    scheme = "exponential" if cfgname == "five" else "linear"
+    m, grid, subs, dt = sdd.MonitorFunction.five_ring(analytic=cfgname != "fiveref"), 77, 4, 1e-4
+    scheme = "linear" if cfgname == "fivelin" else "exponential"
+elif cfgname == "config3fd":  # shock, the reference's FD drift
+    m, grid, subs, dt = sdd.MonitorFunction.shock(analytic=False), 1025, 8, 1e-5
+elif cfgname == "running":  # the reference README's running-example density (a builtin drift), exponential
+    m, grid, subs, dt = sdd.MonitorFunction.by_name("running"), 129, 4, 2e-5
+    scheme, lam = "exponential", 1000.0
 elif cfgname == "config3":
     m, grid, subs, dt = sdd.MonitorFunction.shock(analytic=True), 1025, 8, 1e-5
 elif cfgname == "config2fd":  # the parity mode: the reference's FD drift of rho = 1/w
