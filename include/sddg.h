@@ -245,11 +245,18 @@ sddg_status sddg_nccl_unique_id(sddg_nccl_id* id);
  * collective over all ranks).  nranks = 1 still runs the NCCL exchange. */
 sddg_status sddg_create_dist(int32_t device, int32_t rank, int32_t nranks, const sddg_nccl_id* id,
                              sddg_ctx** out);
-/* One process for n GPUs (ncclCommInitAll, one host thread per device).  A
- * device listed twice runs as separate ranks exchanging by device copies. */
+/* One process for n GPUs (one host thread per device).  Only the owner
+ * (devices[0]) needs the records, so when every device can store into the
+ * owner's memory (peer access over NVLink) the exchange is fused into the
+ * reduce kernel: each finished record is written straight to the owner's
+ * output through peer memory, with no collective.  Without peer access:
+ * ncclCommInitAll and one all-gather (SDDG_TEAM_NCCL=1 forces this).  A
+ * device listed twice runs as separate ranks on that device (the sharded
+ * path on one GPU: fused stores, or device copies with SDDG_TEAM_COPY=1). */
 sddg_status sddg_create_multi(int32_t n, const int32_t* devices, sddg_ctx** out);
 /* This context's first global rank, the rank count, the GPUs this process
- * drives, and whether the exchange is NCCL (1) or a device copy (0). */
+ * drives, and whether the exchange is NCCL (1) or peer stores / device
+ * copies inside one process (0). */
 sddg_status sddg_team_info(const sddg_ctx* ctx, int32_t* rank, int32_t* nranks,
                            int32_t* local_devices, int32_t* nccl);
 /* Host: the node shard plan the sharded calls use.  cost[k] = expected

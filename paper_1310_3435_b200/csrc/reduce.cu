@@ -107,7 +107,7 @@ reduce_kernel(const double* __restrict__ rf, const double* __restrict__ rg,
         // fused all-gather: store the finished record straight into every
         // rank's gather buffer (NVLink peer memory opened through CUDA IPC)
         if (gt.n_peers > 0) {
-            const int64_t slot = gt.global_index[k];
+            const int64_t slot = gt.global_index ? gt.global_index[k] : static_cast<int64_t>(k);
 #pragma unroll 1
             for (int p = 0; p < gt.n_peers; ++p) gt.peers[p][slot] = e;
         }

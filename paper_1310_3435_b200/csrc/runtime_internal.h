@@ -164,7 +164,12 @@ struct Team {
     int nranks = 1;
     int rank0 = 0;
     std::vector<sddg_ctx*> members;  // members[0] is the owning context itself
-    std::vector<ncclComm_t> comms;   // one per member, or empty (copy exchange)
+    std::vector<ncclComm_t> comms;   // one per member, or empty (peer-store or copy exchange)
+    // one process, every member's device can store into the owner's memory
+    // (the same device, or peer access over NVLink): each member's K2 writes
+    // its finished records straight into the owner's output at their node
+    // index -- the reduce and the gather are one kernel, no NCCL call
+    bool fused = false;
 };
 
 namespace sddg {

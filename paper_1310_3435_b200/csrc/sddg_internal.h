@@ -142,7 +142,7 @@ struct LaneState {
 };
 struct GatherTargets {
     int n_peers;                     // 0: no fused gather
-    const int64_t* global_index;     // local node k -> slot in the gather buffers (device)
+    const int64_t* global_index;     // local node k -> slot in the gather buffers (device); null: slot k
     sddg_estimate* peers[kMaxPeers];  // device pointers (local or IPC-mapped peer memory)
 };
 cudaError_t launch_reduce(const double* rf, const double* rg, const uint32_t* meta,

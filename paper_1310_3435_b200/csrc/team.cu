@@ -15,10 +15,16 @@
 //    ranges; the fields are joined by a second all-gather.
 //
 // One process per GPU (sddg_create_dist, ncclCommInitRank) or one process
-// for all of them (sddg_create_multi, ncclCommInitAll, one host thread per
-// device).  A device listed twice in sddg_create_multi is driven as two
-// independent ranks whose exchange is a device copy (no NCCL): the sharded
-// path on a single GPU, for tests.
+// for all of them (sddg_create_multi, one host thread per device).  In one
+// process only the owner's buffer needs the records, so when every member
+// device can store into the owner's memory (peer access over NVLink, or the
+// same device) the exchange is fused into K2: reduce_kernel writes each
+// finished record into the owner's output at its node index through peer
+// memory (GatherTargets, reduce.cu) -- no pack, no collective, no scatter.
+// Without peer access sddg_create_multi falls back to ncclCommInitAll and
+// the all-gather (SDDG_TEAM_NCCL=1 forces it).  A device listed twice is
+// driven as independent ranks (the sharded path on a single GPU, for tests):
+// fused stores by default, device copies with SDDG_TEAM_COPY=1.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -183,6 +189,55 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         for (size_t i = 0; i < lists[r].size(); ++i) all_nodes[r * maxc + i] = static_cast<int>(lists[r][i]);
     const size_t rec = sizeof(sddg_estimate);
     const int nm = static_cast<int>(T.members.size());
+    if (T.fused) {
+        // K2 fused with the gather: member m reduces its nodes and stores each
+        // record at d_out[node] on the owner's device (member 0 does so
+        // anyway).  run_estimates ends with a stream synchronise, so every
+        // peer store has landed when for_members returns.
+        std::vector<double> fms(nm, 0.0);
+        std::vector<int64_t> fl(nm, 0);
+        for_members(T, [&](int m) {
+            sddg_ctx* mc = T.members[m];
+            const int r = T.rank0 + m;
+            cudaStream_t ms_ = m == 0 ? st : mc->stream;
+            const double* px = d_px;
+            const double* py = d_py;
+            const uint64_t* pid = d_pid;
+            sddg_estimate* out = d_out;
+            GatherTargets gt;
+            gt.n_peers = 0;
+            gt.global_index = nullptr;
+            if (m > 0) {
+                char* b = static_cast<char*>(mc->t_pts.ensure(n * (2 * sizeof(double) + sizeof(uint64_t))));
+                ck(cudaMemcpyPeerAsync(b, mc->device, d_px, c->device, n * sizeof(double), ms_), "peer copy");
+                ck(cudaMemcpyPeerAsync(b + n * sizeof(double), mc->device, d_py, c->device, n * sizeof(double), ms_),
+                   "peer copy");
+                ck(cudaMemcpyPeerAsync(b + 2 * n * sizeof(double), mc->device, d_pid, c->device,
+                                       n * sizeof(uint64_t), ms_),
+                   "peer copy");
+                px = reinterpret_cast<const double*>(b);
+                py = px + n;
+                pid = reinterpret_cast<const uint64_t*>(py + n);
+                out = static_cast<sddg_estimate*>(mc->est.ensure(rec * n));
+                gt.n_peers = 1;
+                gt.peers[0] = d_out;  // the owner's records, through peer memory
+            }
+            const std::vector<uint32_t> order = cost_order(cost, &lists[r]);
+            run_estimates(mc, d, dom, bd, cfg, px, py, pid, n, order, out, ms_, gt.n_peers ? &gt : nullptr);
+            fms[m] = mc->last_ms;
+            fl[m] = mc->last_launches;
+        });
+        std::vector<int64_t> steps(n);
+        ck(cudaMemcpy2DAsync(steps.data(), sizeof(int64_t),
+                             reinterpret_cast<const char*>(d_out) + offsetof(sddg_estimate, path_steps), rec,
+                             sizeof(int64_t), n, cudaMemcpyDeviceToHost, st),
+           "d2h path steps");
+        ck(cudaStreamSynchronize(st), "team estimates");
+        c->last_steps = std::accumulate(steps.begin(), steps.end(), int64_t(0));
+        c->last_ms = *std::max_element(fms.begin(), fms.end());
+        c->last_launches = std::accumulate(fl.begin(), fl.end(), int64_t(0));
+        return;
+    }
     std::vector<sddg_estimate*> recv(nm);
     std::vector<cudaStream_t> streams(nm);
     std::vector<double> ms(nm, 0.0);
@@ -387,7 +442,19 @@ sddg_status sddg_create_multi(int32_t n, const int32_t* devices, sddg_ctx** out)
     try {
         const std::set<int32_t> distinct(devices, devices + n);
         std::vector<ncclComm_t> comms;
-        if (n > 1 && static_cast<int32_t>(distinct.size()) == n) {
+        // can every member store into the owner's (devices[0]) memory?
+        bool peer_ok = true;
+        for (int m = 1; m < n; ++m) {
+            int ok = devices[m] == devices[0] ? 1 : 0;
+            if (!ok) cudaDeviceCanAccessPeer(&ok, devices[m], devices[0]);
+            peer_ok = peer_ok && ok;
+        }
+        const char* force_nccl = std::getenv("SDDG_TEAM_NCCL");
+        const char* force_copy = std::getenv("SDDG_TEAM_COPY");
+        const bool all_distinct = static_cast<int32_t>(distinct.size()) == n;
+        const bool fused = n > 1 && peer_ok && !(force_nccl && *force_nccl == '1' && all_distinct) &&
+                           !(force_copy && *force_copy == '1' && !all_distinct);
+        if (n > 1 && all_distinct && !fused) {
             comms.resize(n);
             nck(nccl().CommInitAll(comms.data(), n, devices), "ncclCommInitAll");
         }
@@ -406,7 +473,7 @@ sddg_status sddg_create_multi(int32_t n, const int32_t* devices, sddg_ctx** out)
                 }
             ck(cudaSetDevice(devices[0]), "cudaSetDevice");
         }
-        members[0]->team = new Team{n, 0, members, comms};
+        members[0]->team = new Team{n, 0, members, comms, fused};
     } catch (const Fail& f) {
         for (sddg_ctx* q : members) sddg_destroy(q);
         return team_fail(f);

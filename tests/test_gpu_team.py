@@ -4,10 +4,13 @@ box: the sharded path must be bit-identical to a single-device context.
 * sddg_create_dist with one rank: the NCCL exchange (ncclCommInitRank +
   in-place ncclAllGather of the 128-B records) over a one-rank communicator;
 * sddg_create_multi with device 0 listed 2-3 times: several independent
-  ranks driven from one process (one host thread each), exchanging by device
-  copies -- every shard boundary, the pack/scatter kernels and the subdomain
-  ranges run exactly as on several GPUs, without any kernel waiting on
-  another (B200_PROFILING.md on single-GPU stand-ins).
+  ranks driven from one process (one host thread each).  By default the
+  exchange is fused into K2 (each member's reduce kernel stores its records
+  into the owner's output, as over NVLink peer memory); with SDDG_TEAM_COPY=1
+  the members pack, copy and scatter as the NCCL fallback does -- every shard
+  boundary, the pack/scatter kernels and the subdomain ranges run exactly as
+  on several GPUs, without any kernel waiting on another (SURVEY.md 8(e);
+  B200_PROFILING.md on single-GPU stand-ins).
 * the cost model behind the shards against measured per-node path-steps.
 """
 import numpy as np
@@ -33,6 +36,18 @@ def multi3():
     c.close()
 
 
+@pytest.fixture(scope="module")
+def multi3copy():
+    import os
+    os.environ["SDDG_TEAM_COPY"] = "1"  # read when the context is made
+    try:
+        c = sdd.Context.multi([0, 0, 0])
+    finally:
+        del os.environ["SDDG_TEAM_COPY"]
+    yield c
+    c.close()
+
+
 def _config2_sample(k=90):
     m = sdd.MonitorFunction.ring(analytic=True)
     spec = sdd.GridSpec(UNIT, 129, 129)
@@ -48,7 +63,7 @@ def test_team_info(ctx, dist1, multi3):
     assert multi3.team_info() == {"rank": 0, "nranks": 3, "local_devices": 3, "nccl": False}
 
 
-@pytest.mark.parametrize("which", ["dist1", "multi3"])
+@pytest.mark.parametrize("which", ["dist1", "multi3", "multi3copy"])
 def test_sharded_estimates_bit_identical(ctx, request, which):
     team = request.getfixturevalue(which)
     m, spec, pts, pid = _config2_sample()
@@ -84,7 +99,7 @@ def test_sharded_device_api_bit_identical(ctx, dist1, multi3):
         assert out.cpu().numpy().tobytes() == want.tobytes()
 
 
-@pytest.mark.parametrize("which", ["dist1", "multi3"])
+@pytest.mark.parametrize("which", ["dist1", "multi3", "multi3copy"])
 def test_sharded_solve_sdd_bit_identical(ctx, request, which):
     team = request.getfixturevalue(which)
     m = sdd.MonitorFunction.ring()
