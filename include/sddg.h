@@ -201,6 +201,16 @@ sddg_status sddg_selftest_fastmath(sddg_ctx* ctx, int64_t n, uint64_t max_ulp[6]
  * library's correctly rounded a / b in any bit (expected 0). */
 sddg_status sddg_selftest_division(sddg_ctx* ctx, int64_t n, uint64_t* mismatches);
 
+/* Diagnostics: the performance-mode drifts grad(w)/w of a BASELINE density
+ * (SDDG_DENS_RING_W, _SHOCK_W, _TWOBUMP_W) at n pseudo-random points of the
+ * rectangle dom, against the density's definition evaluated with the fp64
+ * library.  out[0]: max abs error of the fp64 table form; out[1]: of the fp32
+ * SFU forms (as used by the exponential scheme, and with the host-precomputed
+ * constant of the linear scheme); out[2]: max relative error of the fp32
+ * walks' Box-Muller radius argument -2 ln u1; out[3]: max |drift| seen. */
+sddg_status sddg_selftest_drift(sddg_ctx* ctx, int32_t kind, const sddg_domain* dom, int64_t n,
+                                double out[4]);
+
 /* ------------------------------------------------------------- walk seams */
 
 /* Replaces the per-node loop of sdd::mc_estimate calls

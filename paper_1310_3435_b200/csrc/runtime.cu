@@ -1513,6 +1513,17 @@ sddg_status sddg_selftest_division(sddg_ctx* ctx, int64_t n, uint64_t* mismatche
     API_END(ctx)
 }
 
+sddg_status sddg_selftest_drift(sddg_ctx* ctx, int32_t kind, const sddg_domain* dom, int64_t n, double out[4]) {
+    API_BEGIN(ctx)
+    if (n < 1 || !out || !dom) fail(SDDG_ERR_VALIDATION, "selftest_drift: n >= 1, a domain and an output pointer");
+    if (kind != SDDG_DENS_RING_W && kind != SDDG_DENS_SHOCK_W && kind != SDDG_DENS_TWOBUMP_W)
+        fail(SDDG_ERR_VALIDATION, "selftest_drift: a BASELINE density (ring, shock, two-bump)");
+    check_domain(*dom);
+    const double box[4] = {dom->xmin, dom->xmax, dom->ymin, dom->ymax};
+    ck(drift_selftest(kind, n, ctx->fm_tables.p, box, out), "drift self-test");
+    API_END(ctx)
+}
+
 sddg_status sddg_mc_estimate_batch(sddg_ctx* ctx, const sddg_density* dens, const sddg_domain* dom,
                                    const sddg_boundary* bd, const sddg_walk_config* cfg,
                                    const double* px, const double* py, const uint64_t* pid,

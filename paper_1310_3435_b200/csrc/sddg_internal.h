@@ -212,5 +212,8 @@ cudaError_t probe_fma_tflops(int precision, int sms, cudaStream_t st, double* tf
 cudaError_t probe_onchip_gbps(int sms, cudaStream_t st, double* l2_gbps, double* smem_gbps);
 cudaError_t fastmath_selftest(int64_t n, const void* tables, unsigned long long* host_maxulp5);
 cudaError_t division_selftest(int64_t n, unsigned long long* host_bad);
+// walk_fast.cu: performance-mode drifts (fp64 table forms, fp32 SFU forms) and the
+// fp32 radius argument against their definitions evaluated with the fp64 library
+cudaError_t drift_selftest(int kind, int64_t n, const void* tables, const double box[4], double host_out[4]);
 
 }  // namespace sddg

@@ -40,4 +40,114 @@ cudaError_t occupancy_walk_fast(int dv, int precision, int* b, int* block) {
     return cudaErrorInvalidValue;
 }
 
+// ---- self-test of the performance-mode drifts (same translation unit and
+// flags as the walk kernels): grad(w)/w of the BASELINE densities from their
+// definitions with the CUDA library in fp64, against the
+// fp64 table forms and the fp32 SFU forms of density.cuh, and the fp32
+// Box-Muller radius argument -2 ln u1 against the fp64 library.
+namespace {
+
+__device__ void drift_definition(int kind, double x, double y, double& bx, double& by) {
+    if (kind == SDDG_DENS_RING_W) {
+        const double dx = x - 0.5, dy = y - 0.5, q = dx * dx + dy * dy - 0.0625;
+        const double e = exp(-200.0 * q * q), g = -8000.0 * q * e / (1.0 + 10.0 * e);
+        bx = g * dx;
+        by = g * dy;
+    } else if (kind == SDDG_DENS_SHOCK_W) {
+        const double s = 50.0 * (y - 0.5 - 0.15 * sinpi(2.0 * x));
+        const double ch = cosh(s), sech2 = 1.0 / (ch * ch);
+        const double g = -40.0 * sech2 * tanh(s) / (1.0 + 20.0 * sech2);
+        bx = g * (-15.0 * kPiD * cospi(2.0 * x));
+        by = g * 50.0;
+    } else {
+        const double ax = x - 0.3, ay = y - 0.3, cx = x - 0.7, cy = y - 0.6;
+        const double e1 = exp(-100.0 * (ax * ax + ay * ay)), e2 = exp(-100.0 * (cx * cx + cy * cy));
+        const double g = -3000.0 / (1.0 + 15.0 * (e1 + e2));
+        bx = g * (e1 * ax + e2 * cx);
+        by = g * (e1 * ay + e2 * cy);
+    }
+}
+
+__device__ void atomic_max_pos(double* slot, double v) {  // v >= 0: bit patterns order like values
+    atomicMax(reinterpret_cast<unsigned long long*>(slot), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+template <int DV>
+__device__ void drift_check_point(const fm::FmTables& T, const DensityParams& P, int kind, double x, double y,
+                                  float kd_pre, double* out) {
+    double bx, by;
+    drift_definition(kind, x, y, bx, by);
+    double c, vx, vy;
+    drift_cv<DV>(T, P, x, y, 1.0, c, vx, vy);
+    atomic_max_pos(out + 0, fmax(fabs(c * vx - bx), fabs(c * vy - by)));
+    // fp32 from the fp32-rounded point (the error of the form, not of the input)
+    const float xf = static_cast<float>(x), yf = static_cast<float>(y);
+    drift_definition(kind, xf, yf, bx, by);
+    float cf, vxf, vyf;
+    drift_cv<DV>(T, P, xf, yf, 1.0f, cf, vxf, vyf);
+    atomic_max_pos(out + 1, fmax(fabs(double(cf) * vxf - bx), fabs(double(cf) * vyf - by)));
+    // the walk's form: constant times dt precomputed on the host (dt = 1e-5)
+    DensityParams Q = P;
+    Q.kd = kd_pre;
+    drift_cv<DV, true>(T, Q, xf, yf, 1e-5f, cf, vxf, vyf);
+    atomic_max_pos(out + 1, fmax(fabs(double(cf) * vxf * 1e5 - bx), fabs(double(cf) * vyf * 1e5 - by)));
+    atomic_max_pos(out + 3, fmax(fabs(bx), fabs(by)));
+}
+
+__global__ void drift_check(int kind, int64_t n, const fm::FmTables* __restrict__ tg, double x0, double x1,
+                            double y0, double y1, double* out) {
+    extern __shared__ double tsm[];
+    const fm::FmTables& T = *reinterpret_cast<const fm::FmTables*>(tsm);
+#ifdef SDDG_SMEM_ABS
+    // the table reads of this translation unit use fixed shared-window offsets
+    if (static_cast<uint32_t>(__cvta_generic_to_shared(tsm)) != static_cast<uint32_t>(SDDG_SMEM_ABS)) {
+        if (threadIdx.x == 0) atomic_max_pos(out + 0, 1e300);
+        return;
+    }
+#endif
+    for (int k = threadIdx.x; k < static_cast<int>(sizeof(fm::FmTables) / 8); k += blockDim.x)
+        tsm[k] = reinterpret_cast<const double*>(tg)[k];
+    __syncthreads();
+    const DensityParams P{0.0, 0.0, 1e-6, 5e5, TableDensity{}, 0.f};
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t h = static_cast<uint64_t>(i) * 0x9E3779B97F4A7C15ull + 0x2545F4914F6CDD1Dull;
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        const double x = x0 + (x1 - x0) * u01_d(h);
+        h *= 0x94D049BB133111EBull;
+        h ^= h >> 32;
+        const double y = y0 + (y1 - y0) * u01_d(h);
+        if (kind == SDDG_DENS_RING_W)
+            drift_check_point<DV_RING_AN>(T, P, kind, x, y, static_cast<float>(-8000.0 * 1e-5), out);
+        else if (kind == SDDG_DENS_SHOCK_W)
+            drift_check_point<DV_SHOCK_AN>(T, P, kind, x, y, static_cast<float>(1.0 / (-160.0 * 1e-5)), out);
+        else
+            drift_check_point<DV_TWOBUMP_AN>(T, P, kind, x, y, static_cast<float>(-3000.0 * 1e-5), out);
+        // -2 ln u1 of the fp32 walks against the fp64 library, relative
+        const double got = RealOps<float, true>::m2ln_open(h);
+        const uint32_t k24 = static_cast<uint32_t>(h >> 40);
+        const double u1 = (static_cast<double>(k24) + 0.5) * 0x1.0p-24;
+        atomic_max_pos(out + 2, fabs(got / (-2.0 * log(u1)) - 1.0));
+    }
+}
+
+}  // namespace
+
+cudaError_t drift_selftest(int kind, int64_t n, const void* tables, const double box[4], double host_out[4]) {
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 4 * sizeof(double));
+    if (e != cudaSuccess) return e;
+    cudaMemset(d, 0, 4 * sizeof(double));
+    constexpr int sm = static_cast<int>(sizeof(fm::FmTables));
+    cudaFuncSetAttribute(drift_check, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 4);
+    drift_check<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), 256, sm>>>(
+        kind, n, static_cast<const fm::FmTables*>(tables), box[0], box[1], box[2], box[3], d);
+    e = cudaMemcpy(host_out, d, 4 * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e;
+}
+
 }  // namespace sddg

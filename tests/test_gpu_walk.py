@@ -419,6 +419,34 @@ def test_fastmath_accuracy(ctx):
     assert log_abs_near1 <= 4096, list(m)  # cancellation near u = 1: <= 1e-12 relative
 
 
+@pytest.mark.parametrize("kind", [sdd.RING_W, sdd.SHOCK_W, sdd.TWOBUMP_W])
+def test_performance_mode_drifts_match_their_definitions(ctx, kind):
+    # grad(w)/w from the density's definition (fp64 library) against the fp64
+    # table form and the fp32 SFU forms (ring as K q/(1/e + 10), shock with one
+    # reciprocal in E = exp(2s), the host-precomputed constants), on 2^22
+    # points of the unit square and of a rectangle reaching beyond it (the
+    # caps of the exponent arguments), and the fp32 radius argument -2 ln u1
+    import ctypes as C
+
+    class Dom(C.Structure):
+        _fields_ = [("xmin", C.c_double), ("xmax", C.c_double), ("ymin", C.c_double), ("ymax", C.c_double)]
+
+    fn = sdd.lib().sddg_selftest_drift
+    fn.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
+    fn.restype = C.c_int32
+    for box in ((0.0, 1.0, 0.0, 1.0), (-2.0, 3.0, -3.0, 4.0)):
+        out = (C.c_double * 4)()
+        d = Dom(*box)
+        sdd._check(fn(ctx.handle, int(kind), C.byref(d), 1 << 22, out), ctx.handle)
+        e64, e32, eln, bmax = list(out)
+        assert np.isfinite([e64, e32, eln, bmax]).all(), list(out)
+        assert bmax > 1.0  # the sample reaches the layer
+        assert e64 <= 1e-12 * max(bmax, 1.0), list(out)
+        assert e32 <= 2e-5 * max(bmax, 1.0), list(out)
+        assert eln <= 5e-5, list(out)  # < 3e-5 from the SFU above d = 2^-8, 2e-8 from the series below
+    print("drift self-test", int(kind), list(out))
+
+
 def test_parity_division_correctly_rounded(ctx):
     # density.cuh div_rn_shared (the parity mode's drift quotients from one
     # shared reciprocal) equals the library's a / b in every bit on 2^28
