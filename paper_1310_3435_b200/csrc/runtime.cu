@@ -1858,17 +1858,20 @@ sddg_status sddg_invert_mesh(sddg_ctx* ctx, const double* xi, const double* eta,
     cudaStream_t st = ctx->stream;
     double* din = static_cast<double*>(ctx->m_in.ensure(2 * N * sizeof(double)));
     double* dout = static_cast<double*>(ctx->m_out.ensure(2 * M * sizeof(double)));
-    int* derr = static_cast<int*>(ctx->m_misc.ensure(64));
+    if (2.0 * (nx - 1.0) * (ny - 1.0) > 2147483647.0 || static_cast<double>(m_xi) * m_eta > 1073741823.0)
+        fail(SDDG_ERR_VALIDATION, "invert_mesh: more than 2^31 forward triangles or 2^30 targets");
+    // 16 ints of error words, then the kernels' scratch
+    int* derr = static_cast<int*>(ctx->m_misc.ensure(sizeof(int) * (16 + invert_scratch_ints(m_xi, m_eta))));
     ck(cudaMemcpyAsync(din, xi, N * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
     ck(cudaMemcpyAsync(din + N, eta, N * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
-    ck(cudaMemsetAsync(derr, 0, 2 * sizeof(int), st), "memset");
+    ck(cudaMemsetAsync(derr, 0, 4 * sizeof(int), st), "memset");
     const double ghx = (dom->xmax - dom->xmin) / (nx - 1), ghy = (dom->ymax - dom->ymin) / (ny - 1);
     ck(cudaEventRecord(ctx->ev0, st), "event");
     ck(launch_invert(din, din + N, nx, ny, dom->xmin, dom->ymin, ghx, ghy, m_xi, m_eta, dout,
-                     dout + M, derr, derr + 1, st),
+                     dout + M, derr + 16, derr, derr + 1, st),
        "invert launch");
     ck(cudaEventRecord(ctx->ev1, st), "event");
-    int herr[2] = {0, 0};
+    int herr[4] = {0, 0, 0, 0};
     ck(cudaMemcpyAsync(herr, derr, sizeof(herr), cudaMemcpyDeviceToHost, st), "d2h");
     ck(cudaMemcpyAsync(x, dout, M * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
     ck(cudaMemcpyAsync(y, dout + M, M * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
@@ -1876,8 +1879,11 @@ sddg_status sddg_invert_mesh(sddg_ctx* ctx, const double* xi, const double* eta,
     float ms = 0.f;
     cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
     ctx->last_ms = ms;
-    ctx->last_launches = 1;
-    ctx->last_steps = 0;
+    ctx->last_launches = 5;
+    // diagnostics of the fix-up pass: targets located again sequentially
+    // (last_stats' step count) and rows it visited (the tail-handoff count)
+    ctx->last_steps = herr[3];
+    ctx->last_handoffs = herr[2];
     if (herr[0] == 8)
         fail(SDDG_ERR_INVERSION, "invert_mesh: a target in row " + std::to_string(herr[1]) +
                                      " is not covered by the forward tessellation");

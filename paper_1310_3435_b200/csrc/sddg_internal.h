@@ -199,9 +199,12 @@ size_t pm_scratch_doubles(const int* blocks_host, int nblocks);
 cudaError_t loess_run(const double* d_in, double* d_out, int n, int span, int* d_err, cudaStream_t s);
 
 // mesh.cu: K4 inversion, K5 quality
+// scratch: invert_scratch_ints(m_xi, m_eta) ints (lattice and per-target triangles, row marks);
+// err[0], err_row: error code and row; err[2], err[3]: rows the fix-up pass visited, targets it located again
+size_t invert_scratch_ints(int m_xi, int m_eta);
 cudaError_t launch_invert(const double* xi, const double* eta, int nx, int ny, double gx0,
                           double gy0, double ghx, double ghy, int m_xi, int m_eta, double* X,
-                          double* Y, int* err, int* err_row, cudaStream_t s);
+                          double* Y, int* scratch, int* err, int* err_row, cudaStream_t s);
 cudaError_t launch_quality(const double* X, const double* Y, int m_xi, int m_eta, double* qbuf,
                            double* out2, int* err, cudaStream_t s);
 cudaError_t launch_linf(const double* X, const double* Y, const double* RX, const double* RY,

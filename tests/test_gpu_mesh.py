@@ -1,7 +1,12 @@
 """GPU inversion (K4) and quality statistics (K5) against the reference's
 invert_mesh / quality_report outputs (tests/golden, made by the reference).
 BASELINE.json: mesh-quality statistics must match within 1e-6; the kernels
-keep the reference's operation order, so they match bit for bit."""
+keep the reference's operation order, so they match bit for bit.
+
+K4 locates all targets in parallel and reproduces the reference's hint chain
+by construction (csrc/mesh.cu); the cases at the end run it against the
+reference's own invert_mesh (oracle/_ref) on inputs where the hint matters:
+targets on mesh vertices and edges, a folded mesh, a strongly adapted one."""
 import numpy as np
 import pytest
 
@@ -88,3 +93,58 @@ def test_invert_validation(ctx):
     bad[3] = np.nan
     with pytest.raises(sdd.EvaluationError):
         sdd.invert_mesh(bad, np.zeros(81), spec, 9, 9, ctx=ctx)
+
+
+def _ref_dom(box=(0.0, 1.0, 0.0, 1.0)):
+    from oracle import bindings as B
+    return B.Domain(*box)
+
+
+def _forward_solution(n, kind, rng):
+    """(xi, eta) node values of a forward solution on the n x n unit-square grid."""
+    x, y = np.meshgrid(np.linspace(0, 1, n), np.linspace(0, 1, n))
+    if kind == "identity":            # every target of an n x n target grid is a mesh vertex
+        xi, eta = x.copy(), y.copy()
+    elif kind == "symmetric":         # the mesh line i = mid is the line xi = 1/2 exactly
+        xi = x + 0.08 * np.sin(2 * np.pi * x) * (1 + 0.5 * np.sin(np.pi * y))
+        eta = y + 0.05 * np.sin(2 * np.pi * y)
+    elif kind == "adapted":           # strong concentration: cells 20x smaller than the uniform guess
+        xi = np.tanh(6 * (x - 0.5)) / np.tanh(3.0) * 0.5 + 0.5 + 0.02 * np.sin(np.pi * x) * np.sin(2 * np.pi * y)
+        eta = np.tanh(5 * (y - 0.4)) - np.tanh(5 * (0 - 0.4))
+        eta = eta / eta[-1, 0] + 0.02 * np.sin(2 * np.pi * x) * np.sin(np.pi * y)
+    else:                             # noisy: interior nodes jittered until some cells fold
+        h = 1.0 / (n - 1)
+        xi, eta = x.copy(), y.copy()
+        xi[1:-1, 1:-1] += rng.uniform(-0.7 * h, 0.7 * h, (n - 2, n - 2))
+        eta[1:-1, 1:-1] += rng.uniform(-0.7 * h, 0.7 * h, (n - 2, n - 2))
+    return xi.ravel(), eta.ravel()
+
+
+@pytest.mark.parametrize("kind,n,m", [("identity", 33, 33), ("identity", 33, 65), ("symmetric", 65, 65),
+                                      ("adapted", 129, 97), ("adapted", 257, 257), ("noisy", 41, 41),
+                                      ("noisy", 41, 83)])
+def test_invert_equals_reference_where_the_hint_matters(ctx, refimpl, kind, n, m):
+    rng = np.random.default_rng(11)
+    xi, eta = _forward_solution(n, kind, rng)
+    spec = sdd.GridSpec(UNIT, n, n)
+    try:
+        wx, wy = refimpl.invert_mesh(xi, eta, n, n, _ref_dom(), m, m, threads=4)
+    except Exception as exc:  # noqa: BLE001 -- the reference rejects the mesh: so must we
+        with pytest.raises(sdd.InversionError):
+            sdd.invert_mesh(xi, eta, spec, m, m, ctx=ctx)
+        assert "invert_mesh" in str(exc)
+        return
+    mesh = sdd.invert_mesh(xi, eta, spec, m, m, ctx=ctx)
+    assert np.array_equal(mesh.x, wx) and np.array_equal(mesh.y, wy)
+
+
+def test_invert_uncovered_target_raises(ctx, refimpl):
+    # a forward solution that does not reach xi = 1: the reference's
+    # InversionError, on the same input
+    n = 17
+    x, y = np.meshgrid(np.linspace(0, 1, n), np.linspace(0, 1, n))
+    xi, eta = (0.9 * x).ravel(), y.ravel()
+    with pytest.raises(Exception, match="not covered"):
+        refimpl.invert_mesh(xi, eta, n, n, _ref_dom(), n, n)
+    with pytest.raises(sdd.InversionError):
+        sdd.invert_mesh(xi, eta, sdd.GridSpec(UNIT, n, n), n, n, ctx=ctx)
