@@ -42,6 +42,12 @@ constexpr bool kTailHandoff = sizeof(Real) == 8;
 #ifndef SDDG_SHOCK64_HEAVY
 #define SDDG_SHOCK64_HEAVY 0
 #endif
+#ifndef SDDG_BRIDGE_SINGLE
+#define SDDG_BRIDGE_SINGLE 1  // 0: round 1's band path of the fp64 performance mode (A/B: -4.5%)
+#endif
+#ifndef SDDG_BRIDGE_EXP_BOUND
+#define SDDG_BRIDGE_EXP_BOUND 1  // fp64 performance mode: skip the bridge test's exponential when a polynomial bound decides (0: A/B)
+#endif
 #ifndef SDDG_WALK_UNROLL
 #define SDDG_WALK_UNROLL 2  // step-loop copies (A/B: tools/ab.sh with -DSDDG_WALK_UNROLL=n)
 #endif
@@ -289,6 +295,15 @@ __device__ __forceinline__ bool edge_crossing(const Dom<Real>& d, Real x0, Real 
         const Real ex = SCHEME == 0 ? d0 * d1 / par : par * (d1 < d0 ? d1 : d0);
         if (ex > Real(40)) continue;
         const Real u = RealOps<Real, FAST>::u(rng.next_one(rk));
+#if SDDG_BRIDGE_EXP_BOUND
+        // exp(-ex) <= 1 / (1 + ex + ex^2/2): a draw above that bound cannot
+        // fire, and most do not come near it -- the exponential is evaluated
+        // only for the few that do (same decisions: the margin covers the
+        // rounding of the bound by many orders)
+        if constexpr (FAST && sizeof(Real) == 8) {
+            if (u * fma(ex, fma(ex, Real(0.5), Real(1)), Real(1)) >= Real(1.000001)) continue;
+        }
+#endif
         if (u < RealOps<Real, FAST>::ex(T, -ex)) {
             const Real sum = d0 + d1;
             const Real s = sum > Real(0) ? d0 / sum : Real(0);
@@ -548,6 +563,50 @@ __device__ __forceinline__ bool box_test(const Dom<Real>& d, Real px, Real py) {
     else return d.in_box(px, py);
 }
 
+// The band path of the fp64 performance mode (a step with an end outside the
+// inner box), same decisions as segment_exit + edge_crossing:
+//  * the four products p_e = d0 d1 decide everything first: an end outside
+//    the domain makes one of them <= 0 (the start is strictly inside), an
+//    edge can draw only if p_e <= 40 dt;
+//  * all but corner steps have ONE edge that can draw.  Its exponent is p_e /
+//    dt -- the quotient edge_crossing forms from the same two distances -- and
+//    with one candidate the edge order cannot matter: no sort, one division
+//    instead of four;
+//  * exp(-ex) <= 1 / (1 + ex + ex^2/2): most draws lie above that bound and
+//    cannot fire; the exponential decides the few that do not (the margin
+//    covers the bound's rounding by many orders).
+template <typename Stream>
+__device__ __forceinline__ bool band_exit_fp64(const Dom<double>& dom, const WalkArgs& a, const fm::FmTables& T,
+                                               double thr, double dt, double x, double y, double nxp,
+                                               double nyp, Stream& rng, double& hx, double& hy, int& edge) {
+    const double pB = (y - dom.ymin) * (nyp - dom.ymin);
+    const double pT = (dom.ymax - y) * (dom.ymax - nyp);
+    const double pL = (x - dom.xmin) * (nxp - dom.xmin);
+    const double pR = (dom.xmax - x) * (dom.xmax - nxp);
+    const bool qB = pB <= thr, qT = pT <= thr, qL = pL <= thr, qR = pR <= thr;
+    if (!(qB || qT || qL || qR)) return false;
+    if (!(pB > 0.0 && pT > 0.0 && pL > 0.0 && pR > 0.0)) {  // !inside(nxp, nyp)
+        segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+        return true;
+    }
+    if (int(qB) + int(qT) + int(qL) + int(qR) != 1)
+        return edge_crossing<double, true, 0>(dom, x, y, nxp, nyp, dt, a.rk, T, rng, hx, hy, edge);
+    const int e = qB ? 0 : (qT ? 1 : (qL ? 2 : 3));
+    const double ex = (qB ? pB : (qT ? pT : (qL ? pL : pR))) / dt;
+    if (ex > 40.0) return false;
+    const double u = RealOps<double, true>::u(rng.next_one(a.rk));
+    if (u * fma(ex, fma(ex, 0.5, 1.0), 1.0) >= 1.000001) return false;
+    if (!(u < RealOps<double, true>::ex(T, -ex))) return false;
+    const double d0 = dom.dist(x, y, e), d1 = dom.dist(nxp, nyp, e);
+    const double sum = d0 + d1;
+    const double sc = sum > 0.0 ? d0 / sum : 0.0;
+    hx = x + sc * (nxp - x);
+    hy = y + sc * (nyp - y);
+    dom.project(e, hx, hy);
+    edge = e;
+    return true;
+}
+
 // Exit test of the step (x, y) -> (nxp, nyp): explicit exit (segment_exit,
 // sde.cpp:31-65) or the scheme's edge-crossing draws (sde.cpp:72-121), from
 // the stream `rng` (the lane's own Philox stream in K1, the warp's window in
@@ -565,7 +624,9 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
         // box means no exit and no bridge draw (the common step)
         nb = box_test<DV, Real>(dom, nxp, nyp);
         if (!(nb && in_box)) {
-            if (!dom.inside(nxp, nyp)) {
+            if constexpr (SDDG_BRIDGE_SINGLE && FAST && sizeof(Real) == 8 && !kLiteral<DV>) {
+                exited = band_exit_fp64(dom, a, T, thr, dt, x, y, nxp, nyp, rng, hx, hy, edge);
+            } else if (!dom.inside(nxp, nyp)) {
                 segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
                 exited = true;
             } else {
