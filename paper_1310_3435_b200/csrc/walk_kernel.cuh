@@ -45,6 +45,12 @@ constexpr bool kTailHandoff = sizeof(Real) == 8;
 #ifndef SDDG_BRIDGE_SINGLE
 #define SDDG_BRIDGE_SINGLE 1  // 0: round 1's band path of the fp64 performance mode (A/B: -4.5%)
 #endif
+#ifndef SDDG_BRIDGE_SINGLE_REF
+#define SDDG_BRIDGE_SINGLE_REF 1  // the same band path in the reference-mode (parity) kernels (0: A/B, -10%)
+#endif
+#ifndef SDDG_BRIDGE_DIV_BY
+#define SDDG_BRIDGE_DIV_BY 0
+#endif
 #ifndef SDDG_BRIDGE_EXP_BOUND
 #define SDDG_BRIDGE_EXP_BOUND 1  // fp64 performance mode: skip the bridge test's exponential when a polynomial bound decides (0: A/B)
 #endif
@@ -575,28 +581,46 @@ __device__ __forceinline__ bool box_test(const Dom<Real>& d, Real px, Real py) {
 //  * exp(-ex) <= 1 / (1 + ex + ex^2/2): most draws lie above that bound and
 //    cannot fire; the exponential decides the few that do not (the margin
 //    covers the bound's rounding by many orders).
-template <typename Stream>
+// Reference mode (FAST false) takes the same shortcuts where they cannot
+// change a decision: one candidate edge needs no sort, and the bound only
+// skips exponentials whose comparison is already decided; it keeps the
+// reference's own inside test.
+template <bool FAST, typename Stream>
 __device__ __forceinline__ bool band_exit_fp64(const Dom<double>& dom, const WalkArgs& a, const fm::FmTables& T,
                                                double thr, double dt, double x, double y, double nxp,
                                                double nyp, Stream& rng, double& hx, double& hy, int& edge) {
+    if constexpr (!FAST) {
+        if (!dom.inside(nxp, nyp)) {
+            segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+            return true;
+        }
+    }
     const double pB = (y - dom.ymin) * (nyp - dom.ymin);
     const double pT = (dom.ymax - y) * (dom.ymax - nyp);
     const double pL = (x - dom.xmin) * (nxp - dom.xmin);
     const double pR = (dom.xmax - x) * (dom.xmax - nxp);
     const bool qB = pB <= thr, qT = pT <= thr, qL = pL <= thr, qR = pR <= thr;
     if (!(qB || qT || qL || qR)) return false;
-    if (!(pB > 0.0 && pT > 0.0 && pL > 0.0 && pR > 0.0)) {  // !inside(nxp, nyp)
-        segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
-        return true;
+    if constexpr (FAST) {
+        if (!(pB > 0.0 && pT > 0.0 && pL > 0.0 && pR > 0.0)) {  // !inside(nxp, nyp)
+            segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
+            return true;
+        }
     }
     if (int(qB) + int(qT) + int(qL) + int(qR) != 1)
-        return edge_crossing<double, true, 0>(dom, x, y, nxp, nyp, dt, a.rk, T, rng, hx, hy, edge);
+        return edge_crossing<double, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T, rng, hx, hy, edge);
     const int e = qB ? 0 : (qT ? 1 : (qL ? 2 : 3));
-    const double ex = (qB ? pB : (qT ? pT : (qL ? pL : pR))) / dt;
+    const double pe = qB ? pB : (qT ? pT : (qL ? pL : pR));
+#if SDDG_BRIDGE_DIV_BY
+    // the same correctly rounded quotient from the host's RN(1/dt) (density.cuh div_rn_by)
+    const double ex = pe > 0x1p-500 ? div_rn_by(pe, dt, a.inv_dt) : pe / dt;
+#else
+    const double ex = pe / dt;
+#endif
     if (ex > 40.0) return false;
-    const double u = RealOps<double, true>::u(rng.next_one(a.rk));
+    const double u = RealOps<double, FAST>::u(rng.next_one(a.rk));
     if (u * fma(ex, fma(ex, 0.5, 1.0), 1.0) >= 1.000001) return false;
-    if (!(u < RealOps<double, true>::ex(T, -ex))) return false;
+    if (!(u < RealOps<double, FAST>::ex(T, -ex))) return false;
     const double d0 = dom.dist(x, y, e), d1 = dom.dist(nxp, nyp, e);
     const double sum = d0 + d1;
     const double sc = sum > 0.0 ? d0 / sum : 0.0;
@@ -624,8 +648,8 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
         // box means no exit and no bridge draw (the common step)
         nb = box_test<DV, Real>(dom, nxp, nyp);
         if (!(nb && in_box)) {
-            if constexpr (SDDG_BRIDGE_SINGLE && FAST && sizeof(Real) == 8 && !kLiteral<DV>) {
-                exited = band_exit_fp64(dom, a, T, thr, dt, x, y, nxp, nyp, rng, hx, hy, edge);
+            if constexpr (SDDG_BRIDGE_SINGLE && sizeof(Real) == 8 && !kLiteral<DV> && (FAST || SDDG_BRIDGE_SINGLE_REF)) {
+                exited = band_exit_fp64<FAST>(dom, a, T, thr, dt, x, y, nxp, nyp, rng, hx, hy, edge);
             } else if (!dom.inside(nxp, nyp)) {
                 segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
                 exited = true;
