@@ -48,6 +48,12 @@ constexpr bool kTailHandoff = sizeof(Real) == 8;
 #ifndef SDDG_BRIDGE_SINGLE_REF
 #define SDDG_BRIDGE_SINGLE_REF 1  // the same band path in the reference-mode (parity) kernels (0: A/B, -10%)
 #endif
+#ifndef SDDG_BRIDGE_SINGLE_F32
+#define SDDG_BRIDGE_SINGLE_F32 1  // the same band path in the fp32 shock kernel, whose bridge test is inline (0: A/B, -7%)
+#endif
+#ifndef SDDG_FP32_BAND_INLINE_ALL
+#define SDDG_FP32_BAND_INLINE_ALL 1  // band_exit inline in every fp32 kernel (0: bridge_rare out of line for ring/two-bump, A/B -5%)
+#endif
 #ifndef SDDG_BRIDGE_DIV_BY
 #define SDDG_BRIDGE_DIV_BY 0
 #endif
@@ -569,8 +575,9 @@ __device__ __forceinline__ bool box_test(const Dom<Real>& d, Real px, Real py) {
     else return d.in_box(px, py);
 }
 
-// The band path of the fp64 performance mode (a step with an end outside the
-// inner box), same decisions as segment_exit + edge_crossing:
+// The band path (a step with an end outside the inner box) of the fp64 walks
+// and of the fp32 kernels with an inline bridge test, same decisions as
+// segment_exit + edge_crossing:
 //  * the four products p_e = d0 d1 decide everything first: an end outside
 //    the domain makes one of them <= 0 (the start is strictly inside), an
 //    edge can draw only if p_e <= 40 dt;
@@ -585,45 +592,48 @@ __device__ __forceinline__ bool box_test(const Dom<Real>& d, Real px, Real py) {
 // change a decision: one candidate edge needs no sort, and the bound only
 // skips exponentials whose comparison is already decided; it keeps the
 // reference's own inside test.
-template <bool FAST, typename Stream>
-__device__ __forceinline__ bool band_exit_fp64(const Dom<double>& dom, const WalkArgs& a, const fm::FmTables& T,
-                                               double thr, double dt, double x, double y, double nxp,
-                                               double nyp, Stream& rng, double& hx, double& hy, int& edge) {
+template <typename Real, bool FAST, typename Stream>
+__device__ __forceinline__ bool band_exit(const Dom<Real>& dom, const WalkArgs& a, const fm::FmTables& T, Real thr,
+                                          Real dt, Real x, Real y, Real nxp, Real nyp, Stream& rng, Real& hx,
+                                          Real& hy, int& edge) {
     if constexpr (!FAST) {
         if (!dom.inside(nxp, nyp)) {
             segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
             return true;
         }
     }
-    const double pB = (y - dom.ymin) * (nyp - dom.ymin);
-    const double pT = (dom.ymax - y) * (dom.ymax - nyp);
-    const double pL = (x - dom.xmin) * (nxp - dom.xmin);
-    const double pR = (dom.xmax - x) * (dom.xmax - nxp);
+    const Real pB = (y - dom.ymin) * (nyp - dom.ymin);
+    const Real pT = (dom.ymax - y) * (dom.ymax - nyp);
+    const Real pL = (x - dom.xmin) * (nxp - dom.xmin);
+    const Real pR = (dom.xmax - x) * (dom.xmax - nxp);
     const bool qB = pB <= thr, qT = pT <= thr, qL = pL <= thr, qR = pR <= thr;
     if (!(qB || qT || qL || qR)) return false;
     if constexpr (FAST) {
-        if (!(pB > 0.0 && pT > 0.0 && pL > 0.0 && pR > 0.0)) {  // !inside(nxp, nyp)
+        if (!(pB > Real(0) && pT > Real(0) && pL > Real(0) && pR > Real(0))) {  // !inside(nxp, nyp)
             segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
             return true;
         }
     }
     if (int(qB) + int(qT) + int(qL) + int(qR) != 1)
-        return edge_crossing<double, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T, rng, hx, hy, edge);
+        return edge_crossing<Real, FAST, 0>(dom, x, y, nxp, nyp, dt, a.rk, T, rng, hx, hy, edge);
     const int e = qB ? 0 : (qT ? 1 : (qL ? 2 : 3));
-    const double pe = qB ? pB : (qT ? pT : (qL ? pL : pR));
-#if SDDG_BRIDGE_DIV_BY
-    // the same correctly rounded quotient from the host's RN(1/dt) (density.cuh div_rn_by)
-    const double ex = pe > 0x1p-500 ? div_rn_by(pe, dt, a.inv_dt) : pe / dt;
+    const Real pe = qB ? pB : (qT ? pT : (qL ? pL : pR));
+#if SDDG_BRIDGE_DIV_BY  // A/B (-0.5%): the same correctly rounded quotient from the host's RN(1/dt)
+    Real ex;
+    if constexpr (sizeof(Real) == 8) ex = pe > 0x1p-500 ? div_rn_by(pe, dt, a.inv_dt) : pe / dt;
+    else ex = pe / dt;
 #else
-    const double ex = pe / dt;
+    const Real ex = pe / dt;
 #endif
-    if (ex > 40.0) return false;
-    const double u = RealOps<double, FAST>::u(rng.next_one(a.rk));
-    if (u * fma(ex, fma(ex, 0.5, 1.0), 1.0) >= 1.000001) return false;
-    if (!(u < RealOps<double, FAST>::ex(T, -ex))) return false;
-    const double d0 = dom.dist(x, y, e), d1 = dom.dist(nxp, nyp, e);
-    const double sum = d0 + d1;
-    const double sc = sum > 0.0 ? d0 / sum : 0.0;
+    if (ex > Real(40)) return false;
+    const Real u = RealOps<Real, FAST>::u(rng.next_one(a.rk));
+    // the margin covers the rounding of the bound and of the exponential it stands in for
+    if (u * fma(ex, fma(ex, Real(0.5), Real(1)), Real(1)) >= (sizeof(Real) == 8 ? Real(1.000001) : Real(1.0001)))
+        return false;
+    if (!(u < RealOps<Real, FAST>::ex(T, -ex))) return false;
+    const Real d0 = dom.dist(x, y, e), d1 = dom.dist(nxp, nyp, e);
+    const Real sum = d0 + d1;
+    const Real sc = sum > Real(0) ? d0 / sum : Real(0);
     hx = x + sc * (nxp - x);
     hy = y + sc * (nyp - y);
     dom.project(e, hx, hy);
@@ -648,8 +658,13 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
         // box means no exit and no bridge draw (the common step)
         nb = box_test<DV, Real>(dom, nxp, nyp);
         if (!(nb && in_box)) {
-            if constexpr (SDDG_BRIDGE_SINGLE && sizeof(Real) == 8 && !kLiteral<DV> && (FAST || SDDG_BRIDGE_SINGLE_REF)) {
-                exited = band_exit_fp64<FAST>(dom, a, T, thr, dt, x, y, nxp, nyp, rng, hx, hy, edge);
+            // fp32: the kernels whose bridge test is inline (the shock drift; the
+            // others call bridge_rare out of line, below)
+            constexpr bool kInline32 = sizeof(Real) == 4 && FAST && SDDG_BRIDGE_SINGLE_F32 &&
+                                       (SDDG_FP32_BAND_INLINE_ALL || !(SDDG_FP32_BRIDGE_OOL_SHOCK || DV != DV_SHOCK_AN));
+            if constexpr (SDDG_BRIDGE_SINGLE && !kLiteral<DV> &&
+                          ((sizeof(Real) == 8 && (FAST || SDDG_BRIDGE_SINGLE_REF)) || kInline32)) {
+                exited = band_exit<Real, FAST>(dom, a, T, thr, dt, x, y, nxp, nyp, rng, hx, hy, edge);
             } else if (!dom.inside(nxp, nyp)) {
                 segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
                 exited = true;
