@@ -39,7 +39,8 @@ def main():
     line = [l for l in open(plain) if l.startswith("{")][-1]
     bench = json.loads(line)
     steps = bench["roofline"]["path_steps_per_launch"]
-    walks = bench["config"]["nodes_per_rank"] * bench["config"]["paths_per_node_per_step"]
+    cfg = bench["config"]
+    walks = cfg.get("nodes", cfg.get("nodes_per_rank")) * cfg["paths_per_node_per_step"]
     m = {k: {"unit": col[k][0], "value": col[k][1]} for k in METRICS if k in col}
     dram = (float(col["dram__bytes_read.sum"][1]) + float(col["dram__bytes_write.sum"][1]))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[col["dram__bytes_read.sum"][0]]
