@@ -42,8 +42,10 @@ def main():
     cfg = bench["config"]
     walks = cfg.get("nodes", cfg.get("nodes_per_rank")) * cfg["paths_per_node_per_step"]
     m = {k: {"unit": col[k][0], "value": col[k][1]} for k in METRICS if k in col}
-    dram = (float(col["dram__bytes_read.sum"][1]) + float(col["dram__bytes_write.sum"][1]))
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[col["dram__bytes_read.sum"][0]]
+    unit = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    # read and write may come in different units
+    dram = sum(float(col[k][1]) * unit[col[k][0]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    scale = 1
     stalls = {s: float(col[f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio"][1])
               for s in STALLS if f"smsp__average_warps_issue_stalled_{s}_per_issue_active.ratio" in col}
     out = {"command": command, "kernel": note, "metrics": m,
