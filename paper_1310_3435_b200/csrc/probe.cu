@@ -261,6 +261,11 @@ __global__ void division_check(int64_t n, unsigned long long* bad) {
         const double q = div_rn_shared(a, b, 1.0 / b), lib = a / b;
         if (__double_as_longlong(q) != __double_as_longlong(lib) && !(q == 0.0 && lib == 0.0))
             atomicAdd(bad, 1ull);
+        // the unguarded forms on the operand ranges they are used with
+        if (kind <= 5) {
+            if (__double_as_longlong(rcp_rn_normal(b)) != __double_as_longlong(1.0 / b)) atomicAdd(bad, 1ull);
+            if (__double_as_longlong(div_rn_by(a, b, 1.0 / b)) != __double_as_longlong(lib)) atomicAdd(bad, 1ull);
+        }
     }
 }
 
