@@ -54,6 +54,10 @@ constexpr bool kTailHandoff = sizeof(Real) == 8;
 #ifndef SDDG_FP32_BAND_INLINE_ALL
 #define SDDG_FP32_BAND_INLINE_ALL 1  // band_exit inline in every fp32 kernel (0: bridge_rare out of line for ring/two-bump, A/B -5%)
 #endif
+#ifndef SDDG_EXP_MASK_REF
+#define SDDG_EXP_MASK_REF 1  // exponential scheme, reference mode: the qualifying-edge mask (sort only for two or more); A/B:
+                             // running example +18%, FD shock +21%, FD ring +1%; the register-bound five-ring kernel loses 10% and keeps edge_crossing
+#endif
 #ifndef SDDG_BRIDGE_DIV_BY
 #define SDDG_BRIDGE_DIV_BY 0
 #endif
@@ -410,7 +414,7 @@ __device__ __noinline__ BridgeRes bridge_rare(Real x0, Real y0, Real x1, Real y1
 // so this runs on nearly every step: the qualifying set is a bitmask, the
 // edge sort runs only when two or more edges qualify, and the draws share one
 // rolled loop.  Skipped edges draw nothing, as in edge_crossing.
-template <typename Real, typename Stream>
+template <typename Real, bool FAST, typename Stream>
 __device__ __forceinline__ bool bridge_exp_fast(const Dom<Real>& d, Real x0, Real y0, Real x1, Real y1,
                                                 Real nu2, const RoundKeys& rk, const fm::FmTables& T,
                                                 Stream& rng, Real& hx, Real& hy, int& edge) {
@@ -429,8 +433,8 @@ __device__ __forceinline__ bool bridge_exp_fast(const Dom<Real>& d, Real x0, Rea
         if (!((mask >> e) & 1)) continue;
         const Real d0 = d.dist(x0, y0, e), d1 = d.dist(x1, y1, e);
         const Real ex = nu2 * (d1 < d0 ? d1 : d0);
-        const Real u = RealOps<Real, true>::u(rng.next_one(rk));
-        if (u < RealOps<Real, true>::ex(T, -ex)) {
+        const Real u = RealOps<Real, FAST>::u(rng.next_one(rk));
+        if (u < RealOps<Real, FAST>::ex(T, -ex)) {
             const Real sum = d0 + d1;
             const Real sc = sum > Real(0) ? d0 / sum : Real(0);
             hx = x0 + sc * (x1 - x0);
@@ -662,7 +666,8 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
             // others call bridge_rare out of line, below)
             constexpr bool kInline32 = sizeof(Real) == 4 && FAST && SDDG_BRIDGE_SINGLE_F32 &&
                                        (SDDG_FP32_BAND_INLINE_ALL || !(SDDG_FP32_BRIDGE_OOL_SHOCK || DV != DV_SHOCK_AN));
-            if constexpr (SDDG_BRIDGE_SINGLE && !kLiteral<DV> &&
+            // (the literal SDE passes its own threshold and time scale, w dt: same path)
+            if constexpr (SDDG_BRIDGE_SINGLE &&
                           ((sizeof(Real) == 8 && (FAST || SDDG_BRIDGE_SINGLE_REF)) || kInline32)) {
                 exited = band_exit<Real, FAST>(dom, a, T, thr, dt, x, y, nxp, nyp, rng, hx, hy, edge);
             } else if (!dom.inside(nxp, nyp)) {
@@ -702,8 +707,9 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
     } else if (!dom.inside(nxp, nyp)) {
         segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
         exited = true;
-    } else if constexpr (SCHEME == 1 && FAST && sizeof(Real) == 8) {
-        exited = bridge_exp_fast<Real, Stream>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx, hy, edge);
+    } else if constexpr (SCHEME == 1 && sizeof(Real) == 8 && (FAST || (SDDG_EXP_MASK_REF && DV != DV_FIVE_RING))) {
+        // (reference mode too: the same edges draw in the same order, so every decision is the same)
+        exited = bridge_exp_fast<Real, FAST, Stream>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx, hy, edge);
     } else if constexpr (SCHEME == 1) {
         exited = edge_crossing<Real, FAST, 1>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx, hy, edge);
     }

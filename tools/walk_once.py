@@ -41,6 +41,7 @@ else:
     lay = sdd.build_layout(spec, subs, subs)
     px, py, pid = sdd.interface_nodes(m, lay, sdd.plan_interface_points("all", 0, m, lay))
     pts = np.stack([px, py], 1)
+scheme = os.environ.get("SDDG_ONCE_SCHEME", scheme)  # e.g. exponential on a linear-scheme workload
 cfg = sdd.WalkConfig(scheme=scheme, dt=dt, lambda_=lam, walks=walks, seed=1, precision=prec)
 for _ in range(2):
     sdd.mc_estimate_batch(pts, pid, m, UNIT, bd, cfg, ctx=ctx)
