@@ -58,6 +58,9 @@ constexpr bool kTailHandoff = sizeof(Real) == 8;
 #define SDDG_EXP_MASK_REF 1  // exponential scheme, reference mode: the qualifying-edge mask (sort only for two or more); A/B:
                              // running example +18%, FD shock +21%, FD ring +1%; the register-bound five-ring kernel loses 10% and keeps edge_crossing
 #endif
+#ifndef SDDG_EXP_MASK_F32
+#define SDDG_EXP_MASK_F32 0  // A/B: the same in the fp32 walks (-8% to -19%: kept off)
+#endif
 #ifndef SDDG_BRIDGE_DIV_BY
 #define SDDG_BRIDGE_DIV_BY 0
 #endif
@@ -707,7 +710,8 @@ __device__ __forceinline__ bool exit_test(const Dom<Real>& dom, const WalkArgs& 
     } else if (!dom.inside(nxp, nyp)) {
         segment_exit(dom, x, y, nxp, nyp, hx, hy, edge);
         exited = true;
-    } else if constexpr (SCHEME == 1 && sizeof(Real) == 8 && (FAST || (SDDG_EXP_MASK_REF && DV != DV_FIVE_RING))) {
+    } else if constexpr (SCHEME == 1 && ((sizeof(Real) == 8 && (FAST || (SDDG_EXP_MASK_REF && DV != DV_FIVE_RING))) ||
+                                         (sizeof(Real) == 4 && FAST && SDDG_EXP_MASK_F32))) {
         // (reference mode too: the same edges draw in the same order, so every decision is the same)
         exited = bridge_exp_fast<Real, FAST, Stream>(dom, x, y, nxp, nyp, Real(a.nu2), a.rk, T, rng, hx, hy, edge);
     } else if constexpr (SCHEME == 1) {
