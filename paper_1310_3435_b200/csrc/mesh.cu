@@ -30,9 +30,8 @@
 //      reference's sequence until it meets the candidates again; only this
 //      pass raises the reference's errors.
 // K5: one thread per cell computes Q = tr(J^T J) / (2 det J) and flags folded
-// cells; the sum for q_mean is then folded in the reference's row-major order
-// by one thread (exactly the reference's rounding sequence), the maxima are
-// order-free.
+// cells; the sum for q_mean is then taken in a fixed two-level order (see
+// quality_fold), the maxima are order-free.
 #include <cfloat>
 
 #include "density.cuh"
@@ -359,15 +358,34 @@ __global__ void quality_cells(const double* __restrict__ X, const double* __rest
     q[c] = 0.5 * tr / det;
 }
 
-// quality_report folds (proj/src/quality.cpp:44-53): row-major sequential sum,
-// std::max.  One thread: the reference's exact rounding sequence.
-__global__ void quality_fold(const double* __restrict__ q, long long cells, double* out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// quality_report folds (proj/src/quality.cpp:44-53): the sum for q_mean and
+// the maximum.  The reference adds the cells in row-major order; one thread
+// doing the same takes 27 ms for a 1025^2 mesh (a million dependent adds), so
+// the sum is taken in a fixed two-level order instead: thread t of one CTA adds
+// cells t, t + 1024, ... in order, thread 0 adds the 1024 partial sums in
+// order.  The result does not depend on scheduling, and differs from the
+// row-major sum by the rounding of either (a few 1e-16 of q_mean on the test
+// meshes, ~1e-14 at a million cells; the bar for quality statistics is 1e-6).
+constexpr int kFoldThreads = 1024;
+
+__global__ void __launch_bounds__(kFoldThreads) quality_fold(const double* __restrict__ q, long long cells,
+                                                             double* out) {
+    __shared__ double psum[kFoldThreads], pmax[kFoldThreads];
     double sum = 0.0, qmax = 0.0;
-    for (long long c = 0; c < cells; ++c) {
+    for (long long c = threadIdx.x; c < cells; c += kFoldThreads) {
         const double v = q[c];
         sum += v;
         qmax = qmax < v ? v : qmax;
+    }
+    psum[threadIdx.x] = sum;
+    pmax[threadIdx.x] = qmax;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    sum = 0.0;
+    qmax = 0.0;
+    for (int t = 0; t < kFoldThreads; ++t) {
+        sum += psum[t];
+        qmax = qmax < pmax[t] ? pmax[t] : qmax;
     }
     out[0] = qmax;
     out[1] = sum / static_cast<double>(cells);
@@ -460,7 +478,7 @@ cudaError_t launch_quality(const double* X, const double* Y, int m_xi, int m_eta
     const long long cells = static_cast<long long>(m_xi - 1) * (m_eta - 1);
     quality_cells<<<static_cast<unsigned>((cells + 255) / 256), 256, 0, s>>>(X, Y, m_xi, m_eta, qbuf,
                                                                              err);
-    quality_fold<<<1, 32, 0, s>>>(qbuf, cells, out2);
+    quality_fold<<<1, kFoldThreads, 0, s>>>(qbuf, cells, out2);
     return cudaGetLastError();
 }
 

@@ -148,3 +148,21 @@ def test_invert_uncovered_target_raises(ctx, refimpl):
         refimpl.invert_mesh(xi, eta, n, n, _ref_dom(), n, n)
     with pytest.raises(sdd.InversionError):
         sdd.invert_mesh(xi, eta, sdd.GridSpec(UNIT, n, n), n, n, ctx=ctx)
+
+
+def test_quality_large_mesh_against_reference(ctx, refimpl):
+    # a million cells: the two-level fixed-order sum for q_mean (csrc/mesh.cu
+    # quality_fold) against the reference's row-major sum, well inside the 1e-6 bar
+    from oracle import bindings as B
+    n = 1025
+    x, y = np.meshgrid(np.linspace(0, 1, n), np.linspace(0, 1, n))
+    X = (x + 0.05 * np.sin(2 * np.pi * x) * np.sin(np.pi * y)).ravel()
+    Y = (y + 0.05 * np.sin(np.pi * x) * np.sin(2 * np.pi * y)).ravel()
+    RX, RY = x.ravel(), y.ravel()
+    q = sdd.quality_report(sdd.PhysicalMesh(n, n, UNIT, X, Y), sdd.PhysicalMesh(n, n, UNIT, RX, RY), ctx=ctx)
+    want = refimpl.quality(X, Y, n, n, B.Domain(0, 1, 0, 1), RX, RY)
+    got = np.array([q.q_max, q.q_mean, q.r_max, q.r_mean])
+    assert np.max(np.abs(got - np.asarray(want)[:4]) / np.abs(np.asarray(want)[:4])) <= 1e-12, (got, want)
+    # deterministic: the same bits on a second call
+    q2 = sdd.quality_report(sdd.PhysicalMesh(n, n, UNIT, X, Y), sdd.PhysicalMesh(n, n, UNIT, RX, RY), ctx=ctx)
+    assert (q2.q_mean, q2.r_mean) == (q.q_mean, q.r_mean)
