@@ -196,6 +196,10 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
         // peer store has landed when for_members returns.
         std::vector<double> fms(nm, 0.0);
         std::vector<int64_t> fl(nm, 0);
+        // the records land in a buffer of the library's own on the owner's
+        // device (peer access covers it whatever allocator the caller's d_out
+        // comes from); one small device copy then fills d_out
+        sddg_estimate* gathered = static_cast<sddg_estimate*>(c->t_recv.ensure(rec * std::max<int64_t>(n, 1)));
         for_members(T, [&](int m) {
             sddg_ctx* mc = T.members[m];
             const int r = T.rank0 + m;
@@ -203,7 +207,7 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
             const double* px = d_px;
             const double* py = d_py;
             const uint64_t* pid = d_pid;
-            sddg_estimate* out = d_out;
+            sddg_estimate* out = gathered;
             GatherTargets gt;
             gt.n_peers = 0;
             gt.global_index = nullptr;
@@ -220,16 +224,17 @@ void team_estimates(sddg_ctx* c, const sddg_density& d, const sddg_domain& dom,
                 pid = reinterpret_cast<const uint64_t*>(py + n);
                 out = static_cast<sddg_estimate*>(mc->est.ensure(rec * n));
                 gt.n_peers = 1;
-                gt.peers[0] = d_out;  // the owner's records, through peer memory
+                gt.peers[0] = gathered;  // the owner's records, through peer memory
             }
             const std::vector<uint32_t> order = cost_order(cost, &lists[r]);
             run_estimates(mc, d, dom, bd, cfg, px, py, pid, n, order, out, ms_, gt.n_peers ? &gt : nullptr);
             fms[m] = mc->last_ms;
             fl[m] = mc->last_launches;
         });
+        ck(cudaMemcpyAsync(d_out, gathered, rec * n, cudaMemcpyDeviceToDevice, st), "records to the caller");
         std::vector<int64_t> steps(n);
         ck(cudaMemcpy2DAsync(steps.data(), sizeof(int64_t),
-                             reinterpret_cast<const char*>(d_out) + offsetof(sddg_estimate, path_steps), rec,
+                             reinterpret_cast<const char*>(gathered) + offsetof(sddg_estimate, path_steps), rec,
                              sizeof(int64_t), n, cudaMemcpyDeviceToHost, st),
            "d2h path steps");
         ck(cudaStreamSynchronize(st), "team estimates");
