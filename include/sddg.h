@@ -456,7 +456,13 @@ sddg_status sddg_solve_sdd(sddg_ctx* ctx, const sddg_density* dens, const sddg_d
 /* Replaces sdd::invert_mesh (proj/include/sdd/invert.hpp:14): the physical
  * mesh x, y (m_xi*m_eta, index b*m_xi + a) of the uniform computational grid
  * from the solution xi, eta on the nx x ny grid over dom.  Bit-identical to
- * the reference (same walk/scan point location, same rounding sequence). */
+ * the reference: every target is located in parallel, and the reference's
+ * sequential hint chain (each target's walk starts at its predecessor's
+ * triangle, which decides targets on mesh edges and in folded cells) is
+ * reproduced by construction (csrc/mesh.cu); same point-location arithmetic
+ * and rounding sequence.  Diagnostics afterwards: sddg_last_stats' step count =
+ * targets the sequential fix-up pass located again, sddg_last_tail_stats'
+ * handoffs = rows it visited. */
 sddg_status sddg_invert_mesh(sddg_ctx* ctx, const double* xi, const double* eta, int32_t nx,
                              int32_t ny, const sddg_domain* dom, int32_t m_xi, int32_t m_eta,
                              double* x, double* y);
