@@ -878,16 +878,19 @@ Layout build_layout(const sddg_domain& dom, int nx, int ny, int sx, int sy) {
     return L;
 }
 
-void mark_extrema(const std::vector<double>& v, std::vector<char>& marks) {
-    const int n = static_cast<int>(v.size());
-    double vmax = 0.0;
-    for (double x : v) vmax = std::max(vmax, std::abs(x));
-    const double floor_mag = 1e-9 * vmax;
-    for (int i = 1; i + 1 < n; ++i) {
-        if (std::abs(v[i]) < floor_mag) continue;
-        const bool is_max = v[i] > v[i - 1] && v[i] > v[i + 1];
-        const bool is_min = v[i] < v[i - 1] && v[i] < v[i + 1];
-        if (is_max || is_min) marks[i] = 1;
+// Interior samples that are strict local peaks or dips of a series, skipping
+// those smaller than 1e-9 of its largest magnitude (the reference's guard
+// against roundoff wiggles in flat stretches, decomposition.cpp:65-79)
+void flag_extrema(const std::vector<double>& series, std::vector<char>& flag) {
+    double top = 0.0;
+    for (size_t i = 0; i < series.size(); ++i) top = std::max(top, std::fabs(series[i]));
+    const double guard = 1e-9 * top;
+    for (size_t i = 1; i + 1 < series.size(); ++i) {
+        const double before = series[i - 1], here = series[i], after = series[i + 1];
+        if (std::fabs(here) < guard) continue;
+        const bool peak = here > before && here > after;
+        const bool dip = here < before && here < after;
+        if (peak || dip) flag[i] = 1;
     }
 }
 
@@ -911,24 +914,23 @@ std::vector<std::vector<int>> plan(const sddg_density& d, const Layout& L, int s
             }
             nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
         } else if (strategy == SDDG_PLACE_OPTIMAL) {
-            const double hstep = line.vertical ? L.hy() : L.hx();
-            std::vector<double> d1(n), d2(n, 0.0);
+            // the feature rule (decomposition.cpp:82-108): nodes where rho' along
+            // the line (analytic) or rho'' (central difference of rho') has a
+            // strict extremum, at least two nodes apart; the middle node if none
+            const double spacing = line.vertical ? L.hy() : L.hx();
+            std::vector<double> slope(n), curv(n, 0.0);
             for (int p = 0; p < n; ++p) {
-                const double x = line.vertical ? L.dom.xmin + line.fixed * L.hx() : L.dom.xmin + p * L.hx();
-                const double y = line.vertical ? L.dom.ymin + p * L.hy() : L.dom.ymin + line.fixed * L.hy();
+                const int i = line.vertical ? line.fixed : p, j = line.vertical ? p : line.fixed;
                 double gx, gy;
-                h.grad(x, y, gx, gy);
-                d1[p] = line.vertical ? gy : gx;
+                h.grad(L.dom.xmin + i * L.hx(), L.dom.ymin + j * L.hy(), gx, gy);
+                slope[p] = line.vertical ? gy : gx;
             }
-            for (int p = 1; p + 1 < n; ++p) d2[p] = (d1[p + 1] - d1[p - 1]) / (2.0 * hstep);
-            std::vector<char> marks(n, 0);
-            mark_extrema(d1, marks);
-            mark_extrema(d2, marks);
-            for (int p = 1; p + 1 < n; ++p) {
-                if (!marks[p]) continue;
-                if (!nodes.empty() && p - nodes.back() < 2) continue;
-                nodes.push_back(p);
-            }
+            for (int p = 1; p + 1 < n; ++p) curv[p] = (slope[p + 1] - slope[p - 1]) / (2.0 * spacing);
+            std::vector<char> feature(n, 0);
+            flag_extrema(slope, feature);
+            flag_extrema(curv, feature);
+            for (int p = 1; p + 1 < n; ++p)
+                if (feature[p] && (nodes.empty() || p - nodes.back() >= 2)) nodes.push_back(p);
             if (nodes.empty()) nodes.push_back(n / 2);
         } else if (strategy == SDDG_PLACE_EQUIDISTRIBUTED) {
             // BASELINE config 4: grid nodes nearest to equal shares
