@@ -984,37 +984,35 @@ std::vector<std::vector<double>> boundary_tables(const sddg_density& d, const sd
     if (mode != SDDG_BC_REFERENCE) fail(SDDG_ERR_VALIDATION, "unknown bc_mode");
     const HostDensity h = host_density(d);
     // solve_1d_boundary (proj/src/detsolver.cpp:20-48)
-    auto solve1d = [&](int edge) {
-        const bool horiz = edge < 2;
-        const int n = horiz ? nx : ny;
-        std::vector<double> rho(n), u(n);
+    // the 1-D equidistribution of rho along an edge (solve_1d_boundary,
+    // detsolver.cpp:20-48): the cumulative trapezoid of rho over the edge's
+    // nodes, normalised to end at exactly 1 (the spacing cancels)
+    auto edge_table = [&](int edge) {
+        const bool along_x = edge < 2;
+        const int n = along_x ? nx : ny;
+        const int fixed = edge == 1 ? ny - 1 : (edge == 3 ? nx - 1 : 0);
+        std::vector<double> cum(n, 0.0);
+        double prev = 0.0;
         for (int k = 0; k < n; ++k) {
-            double x, y;
-            switch (edge) {
-                case 0: x = dom.xmin + k * hx; y = dom.ymin + 0 * hy; break;
-                case 1: x = dom.xmin + k * hx; y = dom.ymin + (ny - 1) * hy; break;
-                case 2: x = dom.xmin + 0 * hx; y = dom.ymin + k * hy; break;
-                default: x = dom.xmin + (nx - 1) * hx; y = dom.ymin + k * hy; break;
-            }
-            rho[k] = h.rho(x, y);
-            if (!(rho[k] > 0.0))
-                fail(SDDG_ERR_EVALUATION, "solve_1d_boundary: non-positive density on an edge");
+            const int i = along_x ? k : fixed, j = along_x ? fixed : k;
+            const double r = h.rho(dom.xmin + i * hx, dom.ymin + j * hy);
+            if (!(r > 0.0)) fail(SDDG_ERR_EVALUATION, "solve_1d_boundary: non-positive density on an edge");
+            if (k > 0) cum[k] = cum[k - 1] + 0.5 * (prev + r);
+            prev = r;
         }
-        u[0] = 0.0;
-        for (int k = 1; k < n; ++k) u[k] = u[k - 1] + 0.5 * (rho[k - 1] + rho[k]);
-        const double total = u[n - 1];
-        for (int k = 1; k < n - 1; ++k) u[k] /= total;
-        u[n - 1] = 1.0;
-        return u;
+        const double total = cum[n - 1];
+        for (int k = 1; k < n - 1; ++k) cum[k] /= total;
+        cum[n - 1] = 1.0;
+        return cum;
     };
-    t[0] = solve1d(0);
-    t[1] = solve1d(1);
+    t[0] = edge_table(0);
+    t[1] = edge_table(1);
     t[2] = std::vector<double>(ny, 0.0);
     t[3] = std::vector<double>(ny, 1.0);
     t[4] = std::vector<double>(nx, 0.0);
     t[5] = std::vector<double>(nx, 1.0);
-    t[6] = solve1d(2);
-    t[7] = solve1d(3);
+    t[6] = edge_table(2);
+    t[7] = edge_table(3);
     return t;
 }
 
