@@ -1085,72 +1085,83 @@ void spline_fill(const std::vector<int>& xs, std::vector<double>& v) {
     }
 }
 
+// v[q] for a < q < b on the straight line between v[a] and v[b], with the
+// reference's weights (1 - t) v[a] + t v[b], t = (q - a) / (b - a)
+// (decomposition.cpp:218-226)
+void blend_between(std::vector<double>& v, int a, int b) {
+    for (int q = a + 1; q < b; ++q) {
+        const double t = static_cast<double>(q - a) / (b - a);
+        v[q] = (1.0 - t) * v[a] + t * v[b];
+    }
+}
+
+// The interface values of every line from the Monte Carlo estimates
+// (decomposition.cpp:176-246): each line is anchored at its two boundary
+// nodes (read from the boundary tables, so they equal the subdomain corner
+// data bit for bit), takes the estimates at its Monte Carlo nodes, and is
+// filled between neighbouring known nodes -- linearly as in the reference, or
+// by a natural cubic spline through the known nodes (BASELINE config 4).
+// Where a horizontal and a vertical line cross at a node that was not
+// estimated, the vertical line's value is the one both carry.
 IfcResult fill_interfaces(const Layout& L, const NodeSet& ns, const sddg_boundary& bd,
                           const sddg_estimate* est, int interp = SDDG_INTERP_LINEAR) {
     if (interp != SDDG_INTERP_LINEAR && interp != SDDG_INTERP_SPLINE)
         fail(SDDG_ERR_VALIDATION, "unknown interface interpolation");
     IfcResult out;
     out.mc_points = static_cast<int64_t>(ns.px.size());
-    for (size_t k = 0; k < ns.px.size(); ++k) {
+    for (int64_t k = 0; k < out.mc_points; ++k) {
         out.restarts += est[k].restarts;
-        if (est[k].warn) ++out.warnings;
+        out.warnings += est[k].warn ? 1 : 0;
     }
-    const size_t nl = L.lines.size();
-    out.xi.resize(nl);
-    out.eta.resize(nl);
-    out.sxi.resize(nl);
-    out.seta.resize(nl);
-    for (size_t l = 0; l < nl; ++l) {
+    const size_t n_lines = L.lines.size();
+    out.xi.assign(n_lines, {});
+    out.eta.assign(n_lines, {});
+    out.sxi.assign(n_lines, {});
+    out.seta.assign(n_lines, {});
+    for (size_t l = 0; l < n_lines; ++l) {
         const Line& ln = L.lines[l];
-        const int n = ln.length, fi = ln.fixed;
-        std::vector<double> xi(n, 0.0), eta(n, 0.0), sx(n, 0.0), se(n, 0.0);
-        std::vector<char> known(n, 0);
-        xi[0] = ln.vertical ? bd.f[0][fi] : bd.f[2][fi];
-        eta[0] = ln.vertical ? bd.g[0][fi] : bd.g[2][fi];
-        xi[n - 1] = ln.vertical ? bd.f[1][fi] : bd.f[3][fi];
-        eta[n - 1] = ln.vertical ? bd.g[1][fi] : bd.g[3][fi];
-        known[0] = known[n - 1] = 1;
-        for (int pos = 1; pos + 1 < n; ++pos) {
-            auto it = ns.index_of.find(line_node_gid(L, ln, pos));
-            if (it == ns.index_of.end()) continue;
-            const sddg_estimate& e = est[it->second];
+        const int last = ln.length - 1, at = ln.fixed;
+        // a vertical line runs from the bottom edge to the top one, a
+        // horizontal line from the left edge to the right one
+        const int e0 = ln.vertical ? 0 : 2, e1 = ln.vertical ? 1 : 3;
+        std::vector<double>&xi = out.xi[l], &eta = out.eta[l], &sx = out.sxi[l], &se = out.seta[l];
+        xi.assign(ln.length, 0.0);
+        eta.assign(ln.length, 0.0);
+        sx.assign(ln.length, 0.0);
+        se.assign(ln.length, 0.0);
+        xi[0] = bd.f[e0][at];
+        eta[0] = bd.g[e0][at];
+        xi[last] = bd.f[e1][at];
+        eta[last] = bd.g[e1][at];
+        std::vector<int> knots(1, 0);  // the nodes whose values are known, in order
+        for (int pos = 1; pos < last; ++pos) {
+            const auto hit = ns.index_of.find(line_node_gid(L, ln, pos));
+            if (hit == ns.index_of.end()) continue;
+            const sddg_estimate& e = est[hit->second];
             xi[pos] = e.xi;
             eta[pos] = e.eta;
             sx[pos] = e.se_xi;
             se[pos] = e.se_eta;
-            known[pos] = 1;
+            knots.push_back(pos);
         }
-        int prev = 0;
-        for (int pos = 1; pos < n; ++pos) {
-            if (!known[pos]) continue;
-            for (int q = prev + 1; q < pos; ++q) {
-                const double t = static_cast<double>(q - prev) / (pos - prev);
-                xi[q] = (1.0 - t) * xi[prev] + t * xi[pos];
-                eta[q] = (1.0 - t) * eta[prev] + t * eta[pos];
-            }
-            prev = pos;
+        knots.push_back(last);
+        for (size_t k = 0; k + 1 < knots.size(); ++k) {
+            blend_between(xi, knots[k], knots[k + 1]);
+            blend_between(eta, knots[k], knots[k + 1]);
         }
         if (interp == SDDG_INTERP_SPLINE) {
-            std::vector<int> knots;
-            for (int pos = 0; pos < n; ++pos)
-                if (known[pos]) knots.push_back(pos);
             spline_fill(knots, xi);
             spline_fill(knots, eta);
         }
-        out.xi[l] = std::move(xi);
-        out.eta[l] = std::move(eta);
-        out.sxi[l] = std::move(sx);
-        out.seta[l] = std::move(se);
     }
-    for (size_t lv = 0; lv < nl; ++lv) {
-        if (!L.lines[lv].vertical) continue;
-        for (size_t lh = 0; lh < nl; ++lh) {
-            if (L.lines[lh].vertical) continue;
-            const int iv = L.lines[lv].fixed, jh = L.lines[lh].fixed;
-            const uint64_t g = static_cast<uint64_t>(jh) * L.nx + iv;
-            if (ns.index_of.count(g)) continue;
-            out.xi[lh][iv] = out.xi[lv][jh];
-            out.eta[lh][iv] = out.eta[lv][jh];
+    for (size_t h = 0; h < n_lines; ++h) {
+        if (L.lines[h].vertical) continue;
+        for (size_t v = 0; v < n_lines; ++v) {
+            if (!L.lines[v].vertical) continue;
+            const int col = L.lines[v].fixed, row = L.lines[h].fixed;
+            if (ns.index_of.count(static_cast<uint64_t>(row) * L.nx + col)) continue;  // estimated: both read it
+            out.xi[h][col] = out.xi[v][row];
+            out.eta[h][col] = out.eta[v][row];
         }
     }
     return out;
