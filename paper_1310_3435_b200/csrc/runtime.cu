@@ -430,7 +430,10 @@ void raise_kernel_error(const Counters& hc) {
 //    SDDG_TAIL_PER_SM (16) walks per SM.
 // Every stage runs the same step functions on the same draws, so results do
 // not depend on where a walk finished.  SDDG_NO_TAIL=1: K1 alone.
-constexpr uint64_t kTailWalksPerLane = 128;  // one GPU's share of config 2 at N = 8 (62 per lane): -0.8%
+// The handoff check points cost the step loop ~1.8% of its warp instructions, so the
+// stages pay only while the tail is a large enough share: config 2 at 50 / 75 / 100 walks
+// per lane: +1.0% / 0 / -1.1% against the plain kernel (SDDG_TAIL_WALKS_PER_LANE, A/B)
+constexpr uint64_t kTailWalksPerLane = 72;
 
 DrainPlan enable_tail(sddg_ctx* c, WalkArgs& a, int precision, Counters* cnt, uint64_t lanes) {
     DrainPlan dp;
