@@ -250,6 +250,31 @@ def test_five_ring_performance_mode_tracks_reference_paths(ctx, scheme):
         assert np.max(np.abs(a["f"][same] - r["f"][same])) < 1e-6
 
 
+def test_fp32_linear_scheme_on_a_domain_outside_the_positive_quadrant(ctx):
+    # [-1, 1]^2: the integer inner-box test is disabled there (runtime.cu:
+    # box_hi / box_fi = INT32_MAX), so every step takes the band path -- the
+    # fp32 paths must still track the fp64 ones on the same streams, and the
+    # estimates agree statistically
+    dom = sdd.RectDomain(-1, 1, -1, 1)
+    m = sdd.MonitorFunction.five_ring(analytic=True)
+    bd = sdd.make_boundary_data(m, sdd.GridSpec(dom, 37, 37))
+    c64 = sdd.WalkConfig(scheme="linear", dt=2e-4, walks=1, seed=3)
+    c32 = sdd.WalkConfig(scheme="linear", dt=2e-4, walks=1, seed=3, precision="fp32")
+    a = sdd.walk_dump((-0.93, 0.9), 77, m, dom, bd, c64, 0, 2000, ctx=ctx)
+    b = sdd.walk_dump((-0.93, 0.9), 77, m, dom, bd, c32, 0, 2000, ctx=ctx)
+    same = (a["edge"] == b["edge"]) & (a["steps"] == b["steps"])
+    assert same.mean() >= 0.9
+    pts = [(x, y) for x in (-0.6, 0.4) for y in (-0.7, 0.65)]
+    e64 = sdd.mc_estimate_batch(pts, [1, 2, 3, 4], m, dom, bd,
+                                sdd.WalkConfig(scheme="linear", dt=2e-4, walks=20000, seed=21), ctx=ctx)
+    e32 = sdd.mc_estimate_batch(pts, [1, 2, 3, 4], m, dom, bd,
+                                sdd.WalkConfig(scheme="linear", dt=2e-4, walks=20000, seed=22, precision="fp32"),
+                                ctx=ctx)
+    z = np.concatenate([(e64["xi"] - e32["xi"]) / np.hypot(e64["se_xi"], e32["se_xi"]),
+                        (e64["eta"] - e32["eta"]) / np.hypot(e64["se_eta"], e32["se_eta"])])
+    assert np.all(np.abs(z) <= 4), z
+
+
 def test_five_ring_fp32_agrees_statistically_with_fp64(ctx):
     dom = sdd.RectDomain(-1, 1, -1, 1)
     m = sdd.MonitorFunction.five_ring(analytic=True)
