@@ -70,6 +70,30 @@ def test_config1_full_estimates_bit_faithful(ctx, c1_reference):
     assert (got["path_steps"] > 500 * 10_000).all()
 
 
+def test_config2_nodes_at_full_path_count_bit_faithful(ctx, refimpl):
+    # BASELINE config 2 (129^2, 4x4, dt = 2e-5) at its full 1e5 paths per node:
+    # an interface node near the domain's edge (shorter walks, so the
+    # reference's 1e5 paths take ~15 s on the host threads) in parity
+    # mode against the reference's mc_estimate: every one of the 391 chunks of
+    # a node's reduction, estimates within 1e-10, counts identical
+    m = sdd.MonitorFunction.ring()
+    spec = sdd.GridSpec(UNIT, 129, 129)
+    bd = sdd.make_boundary_data(m, spec)
+    nodes = [(96, 5)]
+    px = np.array([i / 128 for i, _ in nodes])
+    py = np.array([j / 128 for _, j in nodes])
+    pid = np.array([j * 129 + i for i, j in nodes], dtype=np.uint64)
+    tabs = refimpl.make_boundary(B.density(B.RING_W), ODOM, 129, 129)
+    ref = refimpl.mc_estimate_batch(B.density(B.RING_W), ODOM, tabs,
+                                    B.walk_cfg(dt=2e-5, walks=100_000, seed=1), px, py, pid, threads=0)
+    got = sdd.mc_estimate_batch(np.stack([px, py], 1), pid, m, UNIT, bd,
+                                sdd.WalkConfig(scheme="linear", dt=2e-5, walks=100_000, seed=1), ctx=ctx)
+    for f in ("xi", "eta", "se_xi", "se_eta"):
+        assert np.max(np.abs(got[f] - ref[f])) <= EST_TOL, f
+    for f in ("walks", "restarts", "warn", "edge_hits"):
+        assert np.array_equal(got[f], ref[f]), f
+
+
 def test_config1_full_interface_lines(ctx, refimpl, c1_reference):
     m, spec, lay, plan, px, py, pid = _config1()
     tabs, _ = c1_reference
