@@ -23,6 +23,11 @@ config 2's solve_interfaces: all 753 nodes at the config's 10^5 paths per node
            /root/reference/proj/src) on all host threads over a fixed node
            subsample of the same workload.
 
+--workload config3 runs BASELINE's multi-GPU scaling run instead (1025^2, 8x8,
+shock density, 14,273 nodes, fp32 walks with fp64 sums; --walks paths per node
+per step, default 10,000 of the config's 1e6), with the same timing, roofline
+(issue slots; fp32) and, under torchrun, the same sharded path.
+
 --impl reference runs the reference CPU implementation alone (rank 0), each
 step a bounded sample of the workload, and prints the same metric.
 Multi-GPU (torchrun, one process per GPU): strong scaling of the same
@@ -501,9 +506,12 @@ def main():
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"])
+    ap.add_argument("--workload", default="config2", choices=["config2", "config3"],
+                    help="config2: the metric's config (default); config3: BASELINE's multi-GPU scaling run "
+                         "(1025^2, 8x8, shock, 14,273 nodes, fp32 walks), --walks paths per node per step")
+    ap.add_argument("--precision", default=None, choices=["fp64", "fp32"])
     ap.add_argument("--drift", default="analytic", choices=["analytic", "reference"])
-    ap.add_argument("--walks", type=int, default=WALKS_PER_STEP)
+    ap.add_argument("--walks", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-mesh", action="store_true", help="skip the end-to-end mesh-gen timings")
@@ -513,6 +521,13 @@ def main():
     ap.add_argument("--paper-table", action="store_true",
                     help="the reference's own workload (paper table / acceptance c11) vs the reference CPU")
     args = ap.parse_args()
+    c3 = args.workload == "config3"
+    if args.precision is None:
+        args.precision = "fp32" if c3 else "fp64"
+    if args.walks is None:
+        args.walks = 10_000 if c3 else WALKS_PER_STEP
+    if c3:  # the config-2 side measurements do not apply
+        args.no_mesh = args.no_solver = args.no_cpu_baseline = True
     if args.impl == "reference":
         return run_reference(args)
     if args.paper_table:
@@ -543,11 +558,28 @@ def main():
         ctx = sdd.Context(local)
     stream = torch.cuda.current_stream()
 
-    m = sdd.MonitorFunction.ring(analytic=args.drift == "analytic")
     dom = sdd.RectDomain(0.0, 1.0, 0.0, 1.0)
-    spec = sdd.GridSpec(dom, GRID, GRID)
+    if c3:
+        # BASELINE config 3: 1025^2 grid split 8x8, shock-layer density, every
+        # interior node of the 14 interface lines, dt = 1e-5, fp32 walks
+        m = sdd.MonitorFunction.shock(analytic=args.drift == "analytic")
+        grid, dt_w, config_walks = 1025, 1e-5, 1_000_000
+        spec = sdd.GridSpec(dom, grid, grid)
+        lay3 = sdd.build_layout(spec, 8, 8)
+        px, py, pid = sdd.interface_nodes(m, lay3, sdd.plan_interface_points("all", 0, m, lay3))
+        pid = np.asarray(pid, dtype=np.uint64)
+        workload = ("BASELINE config 3 walk phase: 1025^2 grid, 8x8 subdomains, all 14,273 interface nodes, "
+                    "shock-layer density (analytic grad w / w), linear EM dt=1e-5 + bridge exit test; one step "
+                    f"= {args.walks} of the config's 1e6 paths per node")
+    else:
+        m = sdd.MonitorFunction.ring(analytic=args.drift == "analytic")
+        grid, dt_w, config_walks = GRID, DT, CONFIG_WALKS
+        spec = sdd.GridSpec(dom, GRID, GRID)
+        px, py, pid = config2_nodes()
+        workload = ("BASELINE config 2 walk phase (one step = the full config): 129^2 "
+                    "grid, 4x4 subdomains, all 753 interface nodes x 1e5 paths, ring "
+                    "density (analytic grad w / w), linear EM dt=2e-5 + bridge exit test")
     bd = sdd.make_boundary_data(m, spec)
-    px, py, pid = config2_nodes()
     n = len(px)
     d_px = torch.tensor(px, dtype=torch.float64, device="cuda")
     d_py = torch.tensor(py, dtype=torch.float64, device="cuda")
@@ -556,7 +588,7 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
     def cfg_for(step):
-        return sdd.WalkConfig(scheme="linear", dt=DT, walks=args.walks, seed=1 + step,
+        return sdd.WalkConfig(scheme="linear", dt=dt_w, walks=args.walks, seed=1 + step,
                               precision=args.precision)
 
     def one_step(step):
@@ -625,7 +657,7 @@ def main():
             et = torch.tensor([e_sec], dtype=torch.float64, device=cdev)
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
             e_sec = float(et[0])
-        tables_bytes = 8 * 4 * (GRID + GRID)
+        tables_bytes = 8 * 4 * (grid + grid)
         e2e = {"value": e_steps / e_sec, "unit": "path-steps/s",
                "h2d_bytes_per_step": int(n * 24 + tables_bytes),
                "d2h_bytes_per_step": int(n * sdd.ESTIMATE_DTYPE.itemsize),
@@ -658,7 +690,7 @@ def main():
     # parity mode, what a drop-in caller gets by default), end to end through
     # the public host-buffer API, one launch after a short warm-up launch
     parity_mode = None
-    if rank == 0 and world == 1 and not args.no_mesh and args.drift == "analytic":
+    if rank == 0 and world == 1 and not args.no_mesh and args.drift == "analytic" and not c3:
         m_ref = sdd.MonitorFunction.ring(analytic=False)
         pts2 = np.stack([px, py], axis=1)
         sdd.mc_estimate_batch(pts2, pid, m_ref, dom, bd,
@@ -746,7 +778,7 @@ def main():
                           "instructions/clk at the SM clock sampled in the timed region; fp_pipe: the "
                           "same for the step's FP64 instructions over SMs x 64 lanes/clk; ncu: the "
                           "warp-level counters of the committed capture at this config",
-            "traffic": traffic_per_launch(n * args.walks),
+            "traffic": traffic_per_launch(n * args.walks) if not c3 else None,
             "traffic_note": "DRAM read+write bytes per launch = ncu dram__bytes per walk "
                             "(profiles/ncu_walk_summary.json) x walks in this launch; "
                             "algorithmic: 20 B per walk record",
@@ -755,7 +787,8 @@ def main():
             "sm_clock_mhz": sm_mhz, "sm_clock_source": clock_source,
             "census": census,
             "pipes": pipes,
-            "ncu": ncu_summary()})
+            "ncu": ncu_summary() if not c3 else {"source": "profiles/r02_walk3_fp32_ncu.txt (ncu --set full of the fp32 "
+                                                              "shock kernel at 2,000 paths per node)"}})
         line = {
             "metric": "SDE walk path-steps/s", "value": value, "unit": "path-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -763,13 +796,11 @@ def main():
             "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic",
-            "config": {"workload": "BASELINE config 2 walk phase (one step = the full config): 129^2 "
-                                   "grid, 4x4 subdomains, all 753 interface nodes x 1e5 paths, ring "
-                                   "density (analytic grad w / w), linear EM dt=2e-5 + bridge exit test",
-                       "paths_per_node_per_step": args.walks, "config_paths_per_node": CONFIG_WALKS,
+            "config": {"workload": workload,
+                       "paths_per_node_per_step": args.walks, "config_paths_per_node": config_walks,
                        "nodes": n, "drift": args.drift, "precision": args.precision,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "parallelism": (f"dp{world}: the 753 nodes sharded over {world} GPUs by expected "
+                       "parallelism": (f"dp{world}: the {n} nodes sharded over {world} GPUs by expected "
                                        "cost (sddg_shard_plan), one ncclAllGather of the 128-B records "
                                        "per step inside the timed region (sddg_create_dist)")
                        if world > 1 else "single GPU"},
@@ -781,7 +812,7 @@ def main():
             "mesh_gen_seconds": mesh,
             "solver": solver,
             "parity_mode_walks": parity_mode,
-            "full_config_seconds_est": CONFIG_WALKS / args.walks * (total_steps / args.steps) / value,
+            "full_config_seconds_est": config_walks / args.walks * (total_steps / args.steps) / value,
             "shard_k1_ms": shard_k1,
         }
         print(json.dumps(line))
