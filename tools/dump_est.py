@@ -1,3 +1,6 @@
+"""Estimates of performance-mode (analytic drift) walks on a few nodes of the
+three BASELINE densities, as bytes (for bit-for-bit comparisons of library
+variants, SDDG_LIB_PATH): python tools/dump_est.py OUT"""
 import sys, numpy as np
 sys.path.insert(0, '.')
 from paper_1310_3435_b200 import sdd

@@ -1,3 +1,5 @@
+"""Wall time of sdd.quality_report (K5, host buffers in and out) on 513^2 and
+1025^2 meshes: python tools/quality_time.py"""
 import sys, numpy as np
 sys.path.insert(0,'.')
 from paper_1310_3435_b200 import sdd
